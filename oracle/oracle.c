@@ -1,0 +1,330 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU reference (TEST INFRASTRUCTURE).
+ * See oracle.h for the contract and the paper passages each function follows.
+ * Compiled with -O2 -ffp-contract=off -fno-fast-math -fopenmp (see oracle/build.py).
+ * Shares no code with the CUDA path.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define NT(t) ((t) > 0 ? (t) : 1)
+#ifdef _OPENMP
+#define OMP_THREADS(t) num_threads((t) > 0 ? (t) : omp_get_max_threads())
+#else
+#define OMP_THREADS(t)
+#endif
+
+/* ------------------------------------------------------------------ fp16 <-> fp64 */
+
+double oracle_f16_to_f64(uint16_t h) {
+  int sign = (h >> 15) & 1;
+  int e = (h >> 10) & 0x1f;
+  int m = h & 0x3ff;
+  double v;
+  if (e == 0) {
+    v = ldexp((double)m, -24); /* subnormal: m * 2^-24 */
+  } else if (e == 31) {
+    v = m ? NAN : INFINITY;
+  } else {
+    v = ldexp((double)(1024 + m), e - 25); /* (1.m) * 2^(e-15) */
+  }
+  return sign ? -v : v;
+}
+
+/* Round-to-nearest-even conversion fp64 -> fp16.  All scalings below are by powers
+ * of two (exact); rint() rounds half to even in the default rounding mode. */
+uint16_t oracle_f64_to_f16(double v) {
+  uint16_t sign = signbit(v) ? 0x8000 : 0;
+  double a = fabs(v);
+  if (isnan(v)) return 0x7e00;
+  if (a >= 65520.0) return sign | 0x7c00; /* 65520 is the tie between 65504 and 2^16 */
+  if (a < ldexp(1.0, -14)) {
+    double q = rint(a * 16777216.0); /* units of 2^-24; q may reach 1024 = min normal */
+    return sign | (uint16_t)q;
+  }
+  int e;
+  frexp(a, &e);        /* a = f * 2^e, f in [0.5, 1) */
+  e -= 1;              /* a = g * 2^e, g in [1, 2)   */
+  double m = rint(ldexp(a, 10 - e)); /* 11-bit significand in [1024, 2048] */
+  if (m == 2048.0) { m = 1024.0; e += 1; }
+  if (e > 15) return sign | 0x7c00;
+  return sign | (uint16_t)(((e + 15) << 10) | ((int)m - 1024));
+}
+
+/* ------------------------------------------------------------------ O-1 quantize */
+
+/* Round-half-to-even of the exact rational n/d, d > 0, n >= 0 (integers). */
+static int64_t rhe_div(int64_t n, int64_t d) {
+  int64_t q = n / d, r = n - q * d;
+  if (2 * r > d || (2 * r == d && (q & 1))) q += 1;
+  return q;
+}
+
+/* One row: x' = clip(x); a = max|x'|; q = rhe(7 x'/a) exactly; scale = fl32(a/7).
+ * fp16 values are integers times 2^-24, so 7x'/a = 7X/A with X, A integers (< 2^41). */
+static void quantize_row(const uint16_t* x, int64_t cols, double clip, int8_t* q, float* scale) {
+  double amax = 0.0;
+  for (int64_t j = 0; j < cols; ++j) {
+    double v = oracle_f16_to_f64(x[j]);
+    if (clip > 0.0) v = v > clip ? clip : (v < -clip ? -clip : v);
+    if (fabs(v) > amax) amax = fabs(v);
+  }
+  if (amax == 0.0) { /* degenerate token: scale 1, all codes 0 (R5) */
+    memset(q, 0, (size_t)cols);
+    *scale = 1.0f;
+    return;
+  }
+  int64_t A = (int64_t)ldexp(amax, 24);
+  for (int64_t j = 0; j < cols; ++j) {
+    double v = oracle_f16_to_f64(x[j]);
+    if (clip > 0.0) v = v > clip ? clip : (v < -clip ? -clip : v);
+    int64_t X = (int64_t)ldexp(fabs(v), 24);
+    int64_t c = rhe_div(7 * X, A);
+    if (v < 0) c = -c;
+    if (c > 7) c = 7;   /* clamp to [-2^(b-1), 2^(b-1)-1]; never binds */
+    if (c < -8) c = -8;
+    q[j] = (int8_t)c;
+  }
+  *scale = (float)amax / 7.0f; /* IEEE fp32 division, correctly rounded (R6) */
+}
+
+static void pack_row(const int8_t* q, int64_t cols, uint8_t* out) {
+  for (int64_t j = 0; j < (cols + 1) / 2; ++j) {
+    uint8_t lo = (uint8_t)(q[2 * j] & 0xF);
+    uint8_t hi = (2 * j + 1 < cols) ? (uint8_t)(q[2 * j + 1] & 0xF) : 0;
+    out[j] = (uint8_t)(lo | (hi << 4));
+  }
+}
+
+static int clip_is_f16(float clip) {
+  if (clip == 0.0f) return 1;
+  if (!(clip > 0.0f)) return 0;
+  return oracle_f16_to_f64(oracle_f64_to_f16((double)clip)) == (double)clip;
+}
+
+int oracle_quantize_rows(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x,
+                         float clip, uint8_t* codes, float* scales, int threads) {
+  if (rows < 0 || cols < 0 || ld_x < cols || !clip_is_f16(clip)) return -1;
+  int64_t pb = (cols + 1) / 2;
+#pragma omp parallel for schedule(static) OMP_THREADS(threads)
+  for (int64_t r = 0; r < rows; ++r) {
+    int8_t* q = (int8_t*)malloc((size_t)(cols > 0 ? cols : 1));
+    quantize_row(x + r * ld_x, cols, (double)clip, q, &scales[r]);
+    pack_row(q, cols, codes + r * pb);
+    free(q);
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ O-2 pack */
+
+int oracle_pack_int4(const int8_t* q, int64_t rows, int64_t cols, uint8_t* packed, int64_t* bad) {
+  for (int64_t i = 0; i < rows * cols; ++i) {
+    if (q[i] < -8 || q[i] > 7) {
+      if (bad) *bad = i;
+      return -1;
+    }
+  }
+  for (int64_t r = 0; r < rows; ++r) pack_row(q + r * cols, cols, packed + r * ((cols + 1) / 2));
+  return 0;
+}
+
+static int8_t nib(uint8_t v) { return (int8_t)((v & 0x8) ? (int)v - 16 : (int)v); }
+
+void oracle_unpack_int4(const uint8_t* packed, int64_t rows, int64_t cols, int8_t* q) {
+  int64_t pb = (cols + 1) / 2;
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t j = 0; j < cols; ++j) {
+      uint8_t b = packed[r * pb + j / 2];
+      q[r * cols + j] = nib((j & 1) ? (uint8_t)(b >> 4) : (uint8_t)(b & 0xF));
+    }
+}
+
+/* ------------------------------------------------------------------ O-4 GEMM */
+
+int oracle_gemm_i32(const uint8_t* a_codes, const uint8_t* w_codes, int64_t M, int64_t N,
+                    int64_t K, int32_t* acc, int threads) {
+  int8_t* qa = (int8_t*)malloc((size_t)(M * K > 0 ? M * K : 1));
+  int8_t* qw = (int8_t*)malloc((size_t)(N * K > 0 ? N * K : 1));
+  oracle_unpack_int4(a_codes, M, K, qa);
+  oracle_unpack_int4(w_codes, N, K, qw);
+  int overflow = 0;
+#pragma omp parallel for schedule(static) OMP_THREADS(threads) reduction(| : overflow)
+  for (int64_t m = 0; m < M; ++m) {
+    for (int64_t n = 0; n < N; ++n) {
+      int64_t s = 0;
+      for (int64_t k = 0; k < K; ++k) s += (int64_t)qa[m * K + k] * (int64_t)qw[n * K + k];
+      if (s > INT32_MAX || s < INT32_MIN) overflow = 1;
+      acc[m * N + n] = (int32_t)s;
+    }
+  }
+  free(qa);
+  free(qw);
+  return overflow ? -1 : 0;
+}
+
+/* ------------------------------------------------------------------ O-5..O-7 */
+
+static double gelu_erf(double t) { return 0.5 * t * (1.0 + erf(t / sqrt(2.0))); }
+
+int oracle_w4a4_linear(const uint8_t* a_codes, const float* a_scales,
+                       const uint8_t* w_codes, const float* w_scales,
+                       int64_t M, int64_t N, int64_t K, int epi_kind,
+                       const uint16_t* bias, const uint16_t* residual,
+                       const uint16_t* gamma, const uint16_t* beta, double ln_eps, float clip,
+                       int32_t* out_i32, uint16_t* out_f16, uint8_t* out_codes, float* out_scales,
+                       int threads) {
+  if (M < 0 || N <= 0 || K <= 0 || !clip_is_f16(clip)) return -1;
+  if (epi_kind == ORACLE_EPI_I32 && !out_i32) return -1;
+  if (epi_kind == ORACLE_EPI_F16 && !out_f16) return -1;
+  if (epi_kind == ORACLE_EPI_GELU_Q4 && (!out_codes || !out_scales)) return -1;
+  if (epi_kind == ORACLE_EPI_RESLN_Q4 &&
+      (!out_codes || !out_scales || !out_f16 || !residual || !gamma || !beta))
+    return -1;
+  int32_t* acc = (int32_t*)malloc((size_t)(M * N > 0 ? M * N : 1) * sizeof(int32_t));
+  int rc = oracle_gemm_i32(a_codes, w_codes, M, N, K, acc, threads);
+  if (rc) { free(acc); return rc; }
+  int64_t pb = (N + 1) / 2;
+#pragma omp parallel for schedule(static) OMP_THREADS(threads)
+  for (int64_t m = 0; m < M; ++m) {
+    double* t = (double*)malloc((size_t)N * sizeof(double));
+    uint16_t* y = (uint16_t*)malloc((size_t)N * sizeof(uint16_t));
+    int8_t* q = (int8_t*)malloc((size_t)N);
+    for (int64_t n = 0; n < N; ++n) {
+      /* dequantize with the token x channel scales, add bias */
+      t[n] = (double)acc[m * N + n] * (double)a_scales[m] * (double)w_scales[n] +
+             (bias ? oracle_f16_to_f64(bias[n]) : 0.0);
+    }
+    switch (epi_kind) {
+      case ORACLE_EPI_I32:
+        memcpy(out_i32 + m * N, acc + m * N, (size_t)N * sizeof(int32_t));
+        break;
+      case ORACLE_EPI_F16:
+        for (int64_t n = 0; n < N; ++n) out_f16[m * N + n] = oracle_f64_to_f16(t[n]);
+        break;
+      case ORACLE_EPI_GELU_Q4:
+        for (int64_t n = 0; n < N; ++n) y[n] = oracle_f64_to_f16(gelu_erf(t[n]));
+        if (out_f16) memcpy(out_f16 + m * N, y, (size_t)N * sizeof(uint16_t));
+        quantize_row(y, N, (double)clip, q, &out_scales[m]);
+        pack_row(q, N, out_codes + m * pb);
+        break;
+      case ORACLE_EPI_RESLN_Q4: {
+        double mu = 0.0, var = 0.0;
+        for (int64_t n = 0; n < N; ++n) {
+          t[n] += oracle_f16_to_f64(residual[m * N + n]); /* z = t + residual */
+          mu += t[n];
+        }
+        mu /= (double)N;
+        for (int64_t n = 0; n < N; ++n) var += (t[n] - mu) * (t[n] - mu);
+        var /= (double)N; /* biased variance */
+        double rstd = 1.0 / sqrt(var + ln_eps);
+        for (int64_t n = 0; n < N; ++n)
+          y[n] = oracle_f64_to_f16((t[n] - mu) * rstd * oracle_f16_to_f64(gamma[n]) +
+                                   oracle_f16_to_f64(beta[n]));
+        memcpy(out_f16 + m * N, y, (size_t)N * sizeof(uint16_t));
+        quantize_row(y, N, (double)clip, q, &out_scales[m]);
+        pack_row(q, N, out_codes + m * pb);
+        break;
+      }
+      default:
+        break;
+    }
+    free(t);
+    free(y);
+    free(q);
+  }
+  free(acc);
+  return (epi_kind >= ORACLE_EPI_I32 && epi_kind <= ORACLE_EPI_RESLN_Q4) ? 0 : -1;
+}
+
+/* ------------------------------------------------------------------ O-8 attention */
+
+int oracle_attention(const uint16_t* qkv, int64_t B, int64_t S, int heads, int head_dim,
+                     uint16_t* ctx_f16, uint8_t* ctx_codes, float* ctx_scales, int threads) {
+  if (B < 0 || S <= 0 || heads <= 0 || head_dim <= 0) return -1;
+  int64_t h = (int64_t)heads * head_dim, ld = 3 * h;
+  int64_t T = B * S;
+  uint16_t* ctx = (uint16_t*)malloc((size_t)(T * h > 0 ? T * h : 1) * sizeof(uint16_t));
+  double scale = 1.0 / sqrt((double)head_dim);
+#pragma omp parallel for schedule(static) OMP_THREADS(threads)
+  for (int64_t bi = 0; bi < B * (int64_t)heads; ++bi) {
+    int64_t b = bi / heads, j = bi % heads;
+    double* p = (double*)malloc((size_t)S * sizeof(double));
+    for (int64_t i = 0; i < S; ++i) {
+      const uint16_t* qrow = qkv + (b * S + i) * ld + j * head_dim;
+      double mx = -INFINITY;
+      for (int64_t k = 0; k < S; ++k) {
+        const uint16_t* krow = qkv + (b * S + k) * ld + h + j * head_dim;
+        double s = 0.0;
+        for (int d = 0; d < head_dim; ++d) s += oracle_f16_to_f64(qrow[d]) * oracle_f16_to_f64(krow[d]);
+        p[k] = s * scale;
+        if (p[k] > mx) mx = p[k];
+      }
+      double sum = 0.0;
+      for (int64_t k = 0; k < S; ++k) { p[k] = exp(p[k] - mx); sum += p[k]; }
+      for (int d = 0; d < head_dim; ++d) {
+        double o = 0.0;
+        for (int64_t k = 0; k < S; ++k)
+          o += p[k] * oracle_f16_to_f64(qkv[(b * S + k) * ld + 2 * h + j * head_dim + d]);
+        ctx[(b * S + i) * h + j * head_dim + d] = oracle_f64_to_f16(o / sum);
+      }
+    }
+    free(p);
+  }
+  if (ctx_f16) memcpy(ctx_f16, ctx, (size_t)(T * h) * sizeof(uint16_t));
+  int rc = oracle_quantize_rows(ctx, T, h, h, 0.0f, ctx_codes, ctx_scales, threads);
+  free(ctx);
+  return rc;
+}
+
+/* ------------------------------------------------------------------ O-9 layer */
+
+int oracle_encoder_layer(const oracle_layer_cfg* cfg, const oracle_layer_weights* w,
+                         int64_t B, int64_t S, const uint16_t* h_in, const uint8_t* hq_in,
+                         const float* hs_in, uint16_t* h_out, uint8_t* hq_out, float* hs_out,
+                         const oracle_taps* taps, int threads) {
+  int64_t M = B * S, h = cfg->hidden, f = cfg->ffn;
+  if ((int64_t)cfg->heads * cfg->head_dim != h) return -1;
+  uint16_t* qkv = (uint16_t*)malloc((size_t)(M * 3 * h) * 2);
+  uint16_t* ctx = (uint16_t*)malloc((size_t)(M * h) * 2);
+  uint8_t* cq = (uint8_t*)malloc((size_t)(M * h / 2));
+  float* cs = (float*)malloc((size_t)M * 4);
+  uint16_t* h1 = (uint16_t*)malloc((size_t)(M * h) * 2);
+  uint8_t* h1q = (uint8_t*)malloc((size_t)(M * h / 2));
+  float* h1s = (float*)malloc((size_t)M * 4);
+  uint16_t* ff = (uint16_t*)malloc((size_t)(M * f) * 2);
+  uint8_t* fq = (uint8_t*)malloc((size_t)(M * f / 2));
+  float* fs = (float*)malloc((size_t)M * 4);
+  int rc = 0;
+  rc |= oracle_w4a4_linear(hq_in, hs_in, w->wqkv, w->sqkv, M, 3 * h, h, ORACLE_EPI_F16, w->bqkv,
+                           NULL, NULL, NULL, 0.0, 0.0f, NULL, qkv, NULL, NULL, threads);
+  rc |= oracle_attention(qkv, B, S, cfg->heads, cfg->head_dim, ctx, cq, cs, threads);
+  rc |= oracle_w4a4_linear(cq, cs, w->wo, w->so, M, h, h, ORACLE_EPI_RESLN_Q4, w->bo, h_in,
+                           w->ln1_g, w->ln1_b, cfg->ln_eps, 0.0f, NULL, h1, h1q, h1s, threads);
+  rc |= oracle_w4a4_linear(h1q, h1s, w->w1, w->s1, M, f, h, ORACLE_EPI_GELU_Q4, w->b1, NULL, NULL,
+                           NULL, 0.0, 0.0f, NULL, ff, fq, fs, threads);
+  rc |= oracle_w4a4_linear(fq, fs, w->w2, w->s2, M, h, f, ORACLE_EPI_RESLN_Q4, w->b2, h1,
+                           w->ln2_g, w->ln2_b, cfg->ln_eps, 0.0f, NULL, h_out, hq_out, hs_out,
+                           threads);
+  if (taps) {
+    if (taps->qkv) memcpy(taps->qkv, qkv, (size_t)(M * 3 * h) * 2);
+    if (taps->ctx) memcpy(taps->ctx, ctx, (size_t)(M * h) * 2);
+    if (taps->ctx_codes) memcpy(taps->ctx_codes, cq, (size_t)(M * h / 2));
+    if (taps->ctx_scales) memcpy(taps->ctx_scales, cs, (size_t)M * 4);
+    if (taps->h1) memcpy(taps->h1, h1, (size_t)(M * h) * 2);
+    if (taps->h1_codes) memcpy(taps->h1_codes, h1q, (size_t)(M * h / 2));
+    if (taps->h1_scales) memcpy(taps->h1_scales, h1s, (size_t)M * 4);
+    if (taps->ffn1) memcpy(taps->ffn1, ff, (size_t)(M * f) * 2);
+    if (taps->f_codes) memcpy(taps->f_codes, fq, (size_t)(M * f / 2));
+    if (taps->f_scales) memcpy(taps->f_scales, fs, (size_t)M * 4);
+  }
+  free(qkv); free(ctx); free(cq); free(cs); free(h1); free(h1q); free(h1s);
+  free(ff); free(fq); free(fs);
+  return rc ? -1 : 0;
+}
