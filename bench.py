@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""bench.py -- W4A4 BERT encoder throughput on B200 (BASELINE.json configs[3]):
+BERT-large, 24 layers, batch 256 per GPU, seq 128, all four linears W4A4 ("qall"),
+batch-sharded data parallel over N GPUs (weak scaling: each rank runs its own 256
+sequences; no collective in the data path).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N ... bench.py --gpus N ...
+
+One step = one pass of the whole hot path: initial activation
+quantize + 24 x [QKV W4A4 GEMM, FP16 attention + ctx quantize, attn-out W4A4 GEMM +
+residual/LN/requant, FFN1 W4A4 GEMM + GELU/requant, FFN2 W4A4 GEMM + residual/LN/requant]
+over 256 x 128 tokens per GPU, replayed as one CUDA graph with inputs resident in HBM.
+Rank 0 prints ONE JSON line (keys documented in DESIGN.md "Measurement")."""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+WORKLOAD = json.load(open(os.path.join(ROOT, "BASELINE.json")))["configs"][3]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="large", choices=["base", "large"])
+    ap.add_argument("--batch", type=int, default=256, help="sequences per GPU")
+    ap.add_argument("--seq", type=int, default=128)
+    ap.add_argument("--layers", type=int, default=0, help="0 = the model's own depth")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip latency / GEMM side measurements")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", ",".join(str(g) for g in self.gpus)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out = self.p.communicate(timeout=5)[0]
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = p.get("hbm_gbs", 6650.0)
+    bf16 = p.get("bf16_tflops_sustained", 1400.0)
+    src = "measured" if p else "fallback"
+    # dense INT8 = 2 x dense bf16 nominal (4.5 vs 2.25 POPS); applied to the measured bf16 figure
+    return {"hbm_gbs": hbm, "int8_tops": 2.0 * bf16, "bf16_tflops": bf16, "source": src}
+
+
+def gemm_work(M, N, K, kind):
+    """Algorithmic ops and bytes of one W4A4 linear launch."""
+    ops = 2.0 * M * N * K
+    by = M * K / 2 + N * K / 2 + 4 * M + 4 * N + 2 * N  # A codes, W codes, scales, bias
+    if kind == "f16":
+        by += 2.0 * M * N
+    elif kind == "gelu_q4":
+        by += M * N / 2 + 4 * M
+    elif kind == "resln_q4":
+        by += 2.0 * M * N + 4 * N + 2.0 * M * N + M * N / 2 + 4 * M  # residual, gamma/beta, f16 out, codes
+    return ops, by
+
+
+def attention_work(B, S, H, d=64):
+    h = H * d
+    ops = 4.0 * B * H * S * S * d
+    by = B * S * 3 * h * 2 + B * S * h / 2 + 4 * B * S  # qkv in, codes + scales out
+    return ops, by
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_sample(cfg, n_seq, S, threads=0):
+    """Time the CPU oracle (as it stands) on one encoder layer over n_seq sequences."""
+    import numpy as np
+    import oracle as orc
+    from paper_2301_12017_b200 import synth
+    p = synth.layer_params(cfg, 0, "bert")
+    w = dict(p)
+    for k in ("wqkv", "wo", "w1", "w2"):
+        w[k], w["s" + k[1:]] = orc.quantize_rows(p[k], threads=threads)
+    x = np.concatenate([synth.hidden(S, cfg["hidden"], "input", b) for b in range(n_seq)])
+    t0 = time.perf_counter()
+    xq, xs = orc.quantize_rows(x, threads=threads)
+    orc.encoder_layer(cfg, w, n_seq, S, x, xq, xs, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0  # under torchrun only rank 0 runs the CPU oracle
+    from paper_2301_12017_b200 import synth
+    cfg = dict(synth.BERT[args.model])
+    L = args.layers or cfg["layers"]
+    cores = cpu_cores()
+    n_seq = 1
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = oracle_sample(cfg, n_seq, args.seq)
+        if i >= args.warmup:
+            times.append(t)
+    t = statistics.median(times)
+    value = n_seq / (t * L)  # seq/s of the full L-layer encoder (layers are identical work)
+    sample = f"1 {args.model} encoder layer x {n_seq} seq x {args.seq} tok per step, extrapolated x{L} layers"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "seq/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64 (CPU oracle)", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "model": f"bert-{args.model}", "layers": L,
+                       "batch_per_gpu": args.batch, "seq_len": args.seq},
+            "cpu_baseline": {"value": value, "unit": "seq/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "seq/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_12017_b200 as q4
+    from paper_2301_12017_b200 import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    N = world
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    cfg = dict(synth.BERT[args.model])
+    L = args.layers or cfg["layers"]
+    B, S, h = args.batch, args.seq, cfg["hidden"]
+    M = B * S
+    layers = [synth.layer_params(cfg, l, "bert") for l in range(L)]
+    enc = q4.W4A4Encoder(cfg, layers, device=dev)
+    del layers
+    # this rank's shard of the global batch: sequences [rank*B, (rank+1)*B)
+    x = np.concatenate([synth.hidden(S, h, "input", rank * B + b) for b in range(B)])
+    xd = torch.from_numpy(x).to(dev)
+    out = torch.empty_like(xd)
+
+    # kernels per step (counted through the library, one eager forward)
+    n0 = q4.launch_count()
+    enc.forward(xd, out, B, S)
+    torch.cuda.synchronize()
+    launches_per_step = q4.launch_count() - n0
+
+    enc.capture(xd, out, B, S)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        enc.replay()
+    torch.cuda.synchronize()
+
+    # ------------------------------------------------------------------ timed region
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(list(range(N)) if rank == 0 else [local]) as clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            enc.replay()
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    ms_per_step = max_over_ranks(total_ms / args.steps)
+    p50 = max_over_ranks(statistics.median(step_ms))
+    value = N * B / (ms_per_step / 1e3)
+    clocks = clk.summary()
+
+    # ------------------------------------------------------------------ end to end (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(x).pin_memory()
+        oh = torch.empty(xh.shape, dtype=torch.float16).pin_memory()
+        for _ in range(max(1, args.warmup)):
+            enc.forward(xh, oh, B, S)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            enc.forward(xh, oh, B, S)  # H2D copy + L layers + D2H copy, all in the C call
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        ok = torch.equal(oh, out.cpu())
+        e2e = {"value": N * B / (e2e_ms / 1e3), "unit": "seq/s", "h2d_bytes_per_step": M * h * 2,
+               "d2h_bytes_per_step": M * h * 2, "ms_per_step": e2e_ms, "matches_device_path": ok}
+
+    # ------------------------------------------------------------------ per-kernel breakdown
+    # One instrumented forward: the same launches as the graph, issued one by one with CUDA
+    # events on the launching stream around each, averaged over the L layers.
+    pk = peaks()
+    kinds = {}
+    w0 = enc.weights
+    hq, hs = q4.quantize_rows(xd)
+    hcur = xd
+    f = cfg["ffn"]
+
+    def timed(name, fn, work):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        r = fn()
+        b.record(stream)
+        kinds.setdefault(name, {"events": [], "work": work})["events"].append((a, b))
+        return r
+
+    for rep in range(2):  # pass 0 warms the caching allocator; pass 1 is measured
+      kinds.clear()
+      hq, hs = q4.quantize_rows(xd)
+      hcur = xd
+      for l in range(L):
+        w = w0[l]
+        qkv = timed("qkv_gemm_f16", lambda: q4.w4a4_linear(hq, hs, w["wqkv"], w["sqkv"], q4.EPI_F16, bias=w["bqkv"]),
+                    gemm_work(M, 3 * h, h, "f16"))["f16"]
+        cq, cs = timed("attention_q4", lambda: q4.attention_f16_q4(qkv, B, S, cfg["heads"]),
+                       attention_work(B, S, cfg["heads"]))
+        o1 = timed("attn_out_gemm_resln_q4", lambda: q4.w4a4_linear(cq, cs, w["wo"], w["so"], q4.EPI_RESLN_Q4, bias=w["bo"],
+                   residual=hcur, gamma=w["ln1_g"], beta=w["ln1_b"]), gemm_work(M, h, h, "resln_q4"))
+        o2 = timed("ffn1_gemm_gelu_q4", lambda: q4.w4a4_linear(o1["codes"], o1["scales"], w["w1"], w["s1"], q4.EPI_GELU_Q4,
+                   bias=w["b1"]), gemm_work(M, f, h, "gelu_q4"))
+        o3 = timed("ffn2_gemm_resln_q4", lambda: q4.w4a4_linear(o2["codes"], o2["scales"], w["w2"], w["s2"], q4.EPI_RESLN_Q4,
+                   bias=w["b2"], residual=o1["f16"], gamma=w["ln2_g"], beta=w["ln2_b"]), gemm_work(M, h, f, "resln_q4"))
+        hcur, hq, hs = o3["f16"], o3["codes"], o3["scales"]
+      torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    breakdown = {}
+    for name, d in kinds.items():
+        t = statistics.median(a.elapsed_time(b) for a, b in d["events"])  # ms per launch
+        ops, by = d["work"]
+        breakdown[name] = {"ms": t, "TOPS": ops / (t * 1e-3) / 1e12, "GBps": by / (t * 1e-3) / 1e9,
+                           "ops": ops, "bytes": by}
+    step_sum = sum(v["ms"] for v in breakdown.values()) * L
+    for v in breakdown.values():
+        v["share"] = v["ms"] * L / step_sum
+    dom = max(breakdown, key=lambda k: breakdown[k]["ms"])
+    d = breakdown[dom]
+    ridge = pk["int8_tops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
+    if d["ops"] / d["bytes"] > ridge and "gemm" in dom:
+        roof = {"bound": "tensor", "achieved": d["TOPS"], "peak": pk["int8_tops"], "unit": "TOPS",
+                "frac": d["TOPS"] / pk["int8_tops"]}
+    else:
+        roof = {"bound": "hbm", "achieved": d["GBps"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": d["GBps"] / pk["hbm_gbs"]}
+    roof.update({"kernel": dom, "traffic": None, "share_of_step": d["share"],
+                 "peak_source": f"{pk['source']}: " + ("2 x bf16_tflops_sustained (int8 = 2x bf16 nominal)"
+                                                       if roof["bound"] == "tensor" else "hbm_gbs")})
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        tr = json.load(open(tp)).get(f"{args.model}:{dom}:M{M}")
+        if tr:
+            roof["traffic"] = tr
+
+    # ------------------------------------------------------------------ extras (rank 0, N=1 shapes)
+    extras = {}
+    if not args.no_extras and rank == 0:
+        extras = side_measurements(q4, synth, torch, np, dev, args)
+
+    # ------------------------------------------------------------------ CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        n_seq = 1
+        t1 = oracle_sample(cfg, n_seq, S)
+        reps = max(1, min(8, int(15.0 / max(t1, 1e-3))))  # ~15 s of CPU work
+        ts = [oracle_sample(cfg, n_seq, S) for _ in range(reps)]
+        t = statistics.median(ts)
+        cpu = {"value": n_seq / (t * L), "unit": "seq/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"1 {args.model} layer x {n_seq} seq x {S} tok, median of {reps}, extrapolated x{L} layers"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "seq/s", "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "p50_ms": p50, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int4 (W4A4, s8 tensor-core MMA, s32 acc)",
+            "data": "synthetic (seeded, random-init weights)",
+            "config": {"workload": WORKLOAD, "model": f"bert-{args.model}", "layers": L, "batch_per_gpu": B,
+                       "global_batch": B * N, "seq_len": S, "parallelism": f"dp{N} (batch-sharded replicas, no collective)",
+                       "l2": f"no flush: per-step working set {(M * h * 2 * 6 + M * cfg['ffn'] / 2) / 1e9:.2f} GB "
+                             f"of activations + {sum(v.numel() for w in enc.weights for v in w.values()) / 1e6:.0f} MB "
+                             f"weights >> 126 MB L2", "cuda_graph": True},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks, "kernels": breakdown, "extras": extras, "lib": q4.version(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def side_measurements(q4, synth, torch, np, dev, args):
+    """Latency configs (BASELINE configs[1], [2]) and the FFN GEMM TOPS (configs[4])."""
+    out = {}
+    stream = torch.cuda.current_stream()
+    base = dict(synth.BERT["base"])
+    for L, name in ((1, "bert_base_1layer_bs1_p50_ms"), (12, "bert_base_12layer_bs1_p50_ms")):
+        enc = q4.W4A4Encoder(base, [synth.layer_params(base, l, "bert") for l in range(L)], device=dev)
+        x = torch.from_numpy(synth.hidden(128, 768, "input", 0)).to(dev)
+        o = torch.empty_like(x)
+        enc.capture(x, o, 1, 128)
+        for _ in range(20):
+            enc.replay()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(201)]
+        torch.cuda.synchronize()
+        evs[0].record(stream)
+        for i in range(200):
+            enc.replay()
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        t = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(200))
+        out[name] = t[100]
+        out[name.replace("p50", "p10")] = t[20]
+        out[name.replace("p50", "p90")] = t[180]
+    # GEMM TOPS at the BERT-large FFN shapes, M = 32768 (tcgen05 vs legacy mma.sync)
+    pk = peaks()
+    for (Nn, K) in ((4096, 1024), (1024, 4096)):
+        M = 32768
+        a = torch.from_numpy(synth.random_packed(M, K, f"sw_a{K}")).to(dev)
+        w = torch.from_numpy(synth.random_packed(Nn, K, f"sw_w{Nn}")).to(dev)
+        sa = torch.from_numpy(synth.random_scales(M, "sw_sa")).to(dev)
+        sw = torch.from_numpy(synth.random_scales(Nn, "sw_sw")).to(dev)
+        for ml, mname in ((1, "tcgen05"), (2, "mma_sync_s8"), (3, "mma_sync_s4")):
+            o = q4.w4a4_linear(a, sa, w, sw, q4.EPI_F16, mainloop=ml)
+            for _ in range(3):
+                q4.w4a4_linear(a, sa, w, sw, q4.EPI_F16, mainloop=ml, out=o)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(10):
+                q4.w4a4_linear(a, sa, w, sw, q4.EPI_F16, mainloop=ml, out=o)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 10
+            tops = 2.0 * M * Nn * K / (t * 1e-3) / 1e12
+            out[f"gemm_f16_M{M}_N{Nn}_K{K}_{mname}_TOPS"] = tops
+            out[f"gemm_f16_M{M}_N{Nn}_K{K}_{mname}_frac_int8_peak"] = tops / pk["int8_tops"]
+    return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())

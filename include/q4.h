@@ -1,0 +1,191 @@
+/*
+ * q4.h -- C ABI of the B200 (sm_100a) W4A4 encoder hot path.
+ *
+ * Paper: arXiv 2301.12017, "Highly Optimized INT4 Encoder Inference",
+ * PAPER.md:402-511, and App. A "Quantization Algorithms".
+ * Readings of garbled / silent passages are numbered R1..R17 in DESIGN.md.
+ *
+ * Conventions (all entry points)
+ *   - fp16 tensors are IEEE binary16, passed as `uint16_t*`; fp32 as `float*`.
+ *   - Packed INT4 ("we pack INT4 data into INT8 tensors"): byte j of a
+ *     row holds element 2j in the low nibble and 2j+1 in the high nibble, two's
+ *     complement (R9).  A row of `cols` INT4 values occupies cols/2 bytes.
+ *   - All matrices are row-major and contiguous unless an ld_* argument is given.
+ *     Weights use the nn.Linear [out, in] orientation, i.e. [N, K]: both GEMM
+ *     operands are K-major and nibble-packed along K.
+ *   - Pointers are caller-owned DEVICE memory unless stated (q4_encoder_stack also
+ *     accepts host memory for its input/output).  The library never allocates in
+ *     these calls; scratch comes in through `workspace`, sized by *_workspace().
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Calls are stream-ordered and asynchronous: no host synchronisation, no
+ *     allocation, no host-side state change, so they can be captured in CUDA graphs
+ *     (except q4_encoder_stack with host buffers, which enqueues copies).
+ *   - Errors: argument validation is synchronous and returns Q4_E*; the text naming
+ *     the argument, shape or coordinate is in q4_last_error() (thread-local).  A
+ *     launch failure returns Q4_ECUDA; asynchronous kernel faults surface at the
+ *     caller's next synchronisation.  The library never aborts the process.
+ */
+#ifndef Q4_H
+#define Q4_H
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define Q4_API __attribute__((visibility("default")))
+#else
+#define Q4_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  Q4_OK = 0,
+  Q4_EINVAL = 1,       /* bad argument value (NULL where required, bad clip, bad kind) */
+  Q4_ESHAPE = 2,       /* inconsistent or unsupported dimensions                       */
+  Q4_EALIGN = 3,       /* pointer / leading-dimension alignment (TMA needs 16 B)       */
+  Q4_EUNSUPPORTED = 4, /* valid request this build does not implement                 */
+  Q4_ECUDA = 5         /* CUDA runtime / driver error (text has cudaGetErrorString)    */
+} q4_status;
+
+/* Thread-local description of the last error of this thread ("" if none). */
+Q4_API const char* q4_last_error(void);
+/* Library version / build string (architecture it was compiled for). */
+Q4_API const char* q4_version(void);
+/* Number of kernels this process launched through the library (all threads). */
+Q4_API uint64_t q4_launch_count(void);
+
+/* ---------------------------------------------------------------------------------
+ * a1/a2  Symmetric per-row INT4 quantization + packing.
+ * PAPER.md:703-708 (sym. equation) with S = amax / (2^(b-1) - 1) = amax/7 (R1),
+ * round half to even (R2), x/S evaluated exactly (R3): q = rint(div.rn(7x, amax)),
+ * which equals the exact rational rounding for every fp16 pair (tests pin this).
+ * Rows are tokens for activations ("token-wise dynamic quantization",
+ * PAPER.md:520-522) or output channels for weights ("row-wise", R7).
+ *   x       [rows, ld_x] fp16; the first `cols` of each row are quantized
+ *   clip    0 = none; else an fp16-representable value > 0, x clamped to
+ *           [-clip, clip] before the scale is taken ("Clip Values", R10)
+ *   codes   [rows, cols/2] packed INT4 (output)
+ *   scales  [rows] fp32 = fl32(amax/7); an all-zero row gets scale 1, codes 0 (R5)
+ * Requirements: cols % 8 == 0, ld_x % 8 == 0, x 16-byte aligned, codes 4-byte aligned.
+ * rows == 0 is a no-op. */
+Q4_API q4_status q4_quantize_rows(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x,
+                           float clip, uint8_t* codes, float* scales, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * a3-a6  W4A4 linear: exact INT32 GEMM + fused epilogue.
+ *   acc[m,n] = sum_k qa[m,k] * qw[n,k]                  (exact)
+ *   t[m,n]   = acc * a_scales[m] * w_scales[n] + bias[n]   (fp32; "fuse the
+ *              dequantization operation with the INT4 GEMM kernel")
+ * Epilogues ("fuse the quantization operation for activation with its previous
+ * element-bias-add, GELU, or layer normalization operation"):
+ *   Q4_EPI_I32      out_i32 = acc                              (debug / parity tap)
+ *   Q4_EPI_F16      out_f16 = fp16(t)                          (QKV projection)
+ *   Q4_EPI_GELU_Q4  y = fp16(gelu_erf(t)) (R11); (out_codes, out_scales) = a1(y)
+ *                   per row; out_f16 = y if non-NULL (tap)     (MLP intermediate)
+ *   Q4_EPI_RESLN_Q4 z = t + residual; y = fp16(LayerNorm(z) * gamma + beta), biased
+ *                   variance, eps = ln_eps (R12), post-LN;
+ *                   out_f16 = y (required: next residual); (out_codes, out_scales)
+ *                   = a1(y)                                    (attn-out, MLP-out)
+ * The *_Q4 epilogues reduce over a whole output row; they need N <= 4096.
+ */
+typedef enum { Q4_EPI_I32 = 0, Q4_EPI_F16 = 1, Q4_EPI_GELU_Q4 = 2, Q4_EPI_RESLN_Q4 = 3 } q4_epi_kind;
+
+/* GEMM mainloop variant (benchmark knob; results are identical by construction).
+ *   AUTO        choose by shape (currently TCGEN05)
+ *   TCGEN05     TMA -> smem nibble->int8 unpack -> tcgen05.mma kind::i8 -> TMEM
+ *   MMA_SYNC_S8 legacy: cp.async -> ldmatrix -> register unpack -> mma.sync s8
+ *   MMA_SYNC_S4 legacy: cp.async -> ldmatrix -> mma.sync m16n8k64 .s4 (emulated on sm_100a)
+ * The legacy variants implement Q4_EPI_I32 and Q4_EPI_F16 only. */
+typedef enum { Q4_MAINLOOP_AUTO = 0, Q4_MAINLOOP_TCGEN05 = 1, Q4_MAINLOOP_MMA_SYNC_S8 = 2,
+               Q4_MAINLOOP_MMA_SYNC_S4 = 3 } q4_mainloop;
+
+typedef struct {
+  int32_t kind;              /* q4_epi_kind                                              */
+  int32_t mainloop;          /* q4_mainloop (0 = auto)                                   */
+  const uint16_t* bias;      /* [N] fp16; NULL = 0                                       */
+  const uint16_t* residual;  /* [M, N] fp16; RESLN only                                  */
+  const uint16_t* gamma;     /* [N] fp16; RESLN only                                     */
+  const uint16_t* beta;      /* [N] fp16; RESLN only                                     */
+  float ln_eps;              /* RESLN; BERT uses 1e-12                                   */
+  float requant_clip;        /* *_Q4: as q4_quantize_rows' clip; 0 = none                */
+  int32_t* out_i32;          /* [M, N]   I32                                             */
+  uint16_t* out_f16;         /* [M, N]   F16, RESLN (required); GELU_Q4 optional tap      */
+  uint8_t* out_codes;        /* [M, N/2] *_Q4                                            */
+  float* out_scales;         /* [M]      *_Q4                                            */
+} q4_epilogue;
+
+/* Requirements: M >= 0; N % 32 == 0; K % 32 == 0; K <= 8192 (the INT32 accumulator
+ * bound |acc| <= 64 K); all pointers 16-byte aligned.  Workspace: none today
+ * (returns 0); pass any pointer. */
+Q4_API size_t q4_w4a4_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind);
+Q4_API q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, /* [M,K/2], [M] */
+                         const uint8_t* w_codes, const float* w_scales, /* [N,K/2], [N] */
+                         int64_t M, int64_t N, int64_t K, const q4_epilogue* epi,
+                         void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * a7  FP16 attention between the quantized GEMMs (the
+ * pipeline keeps attention in FP16 -- "we use FP16 FlashAttention") with the
+ * per-token quantize of the context fused into the same kernel.
+ *   qkv        [B*S, 3*heads*head_dim] fp16 (Q | K | V column blocks, head j at
+ *              columns [j*head_dim, (j+1)*head_dim) of each block)
+ *   ctx        = softmax(Q K^T / sqrt(head_dim)) V, no mask (R14), fp16
+ *   ctx_f16    [B*S, heads*head_dim] optional tap (NULL = not written)
+ *   ctx_codes  [B*S, heads*head_dim/2], ctx_scales [B*S]: a1 applied per token over
+ *              all heads of the fp16 ctx
+ * Requirements: head_dim == 64, 1 <= S <= 128, heads*64 <= 1024. */
+Q4_API q4_status q4_attention_f16_q4(const uint16_t* qkv, int64_t B, int64_t S, int32_t heads,
+                              int32_t head_dim, uint16_t* ctx_f16, uint8_t* ctx_codes,
+                              float* ctx_scales, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * a8  One post-LN BERT encoder layer, all four linears W4A4 ("qall",
+ * PAPER.md:429-431, 483-493, R15):
+ *   qkv   = linear(hq_in;  Wqkv, F16)                 [M, 3h]
+ *   ctx   = attention(qkv) -> codes                   [M, h]
+ *   h1    = linear(ctx;    Wo,  RESLN_Q4, res=h_in, ln1)
+ *   f     = linear(h1;     W1,  GELU_Q4)              [M, ffn]
+ *   h_out = linear(f;      W2,  RESLN_Q4, res=h1,   ln2)  (+ hq_out, hs_out)
+ * (hq_in, hs_in) must be a1(h_in): the previous layer's RESLN_Q4 output, or
+ * q4_quantize_rows for layer 0.  M = B*S.  Taps (each nullable) receive copies of the
+ * intermediates for teacher-forced parity; acc_* taps cost one extra I32 GEMM each. */
+typedef struct {
+  int32_t hidden, heads, head_dim, ffn;
+  float ln_eps;
+} q4_layer_cfg;
+typedef struct {
+  const uint8_t *wqkv, *wo, *w1, *w2;   /* packed [3h,h/2], [h,h/2], [ffn,h/2], [h,ffn/2] */
+  const float *sqkv, *so, *s1, *s2;     /* per-output-channel scales                       */
+  const uint16_t *bqkv, *bo, *b1, *b2;  /* fp16 biases                                      */
+  const uint16_t *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+} q4_layer_weights;
+typedef struct {
+  uint16_t *qkv, *ctx, *h1, *ffn1;
+  int32_t *acc_qkv, *acc_o, *acc_1, *acc_2;
+  uint8_t *ctx_codes, *h1_codes, *f_codes;
+  float *ctx_scales, *h1_scales, *f_scales;
+} q4_taps;
+Q4_API size_t q4_encoder_layer_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S);
+Q4_API q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B,
+                           int64_t S, const uint16_t* h_in, const uint8_t* hq_in,
+                           const float* hs_in, uint16_t* h_out, uint8_t* hq_out, float* hs_out,
+                           void* workspace, size_t ws_bytes, const q4_taps* taps, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * a8  L-layer encoder forward (the paper's E2E pipeline):
+ * a1(h_in) once, then L x q4_encoder_layer, ping-ponging hidden states in the
+ * workspace.  h_in / h_out may be HOST (pinned or pageable) or DEVICE pointers; host
+ * buffers are copied with cudaMemcpyAsync on `stream` inside the call (this is the
+ * end-to-end entry point).  `layers` is a host array of L weight structs (device
+ * pointers inside).  All-device calls are CUDA-graph capturable. */
+Q4_API size_t q4_encoder_stack_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S);
+Q4_API q4_status q4_encoder_stack(const q4_layer_cfg* cfg, const q4_layer_weights* layers, int32_t L,
+                           int64_t B, int64_t S, const uint16_t* h_in, uint16_t* h_out,
+                           void* workspace, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* Q4_H */

@@ -1,0 +1,342 @@
+// q4_api.cu -- the C ABI (include/q4.h): argument validation, error reporting, kernel
+// dispatch, and the host-side orchestration of the encoder layer / stack (a8).
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/q4.h"
+#include "kernels.h"
+
+namespace q4 {
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+}  // namespace q4
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+q4_status fail(q4_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return s;
+}
+q4_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(Q4_ECUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+bool al4(const void* p) { return ((uintptr_t)p & 3) == 0; }
+
+bool clip_ok(float c) {
+  if (c == 0.f) return true;
+  if (!(c > 0.f)) return false;
+  __half h = __float2half_rn(c);
+  return __half2float(h) == c;
+}
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+extern "C" {
+
+const char* q4_last_error(void) { return g_err; }
+const char* q4_version(void) { return "q4-b200 0.1 (sm_100a; tcgen05 kind::i8 W4A4)"; }
+uint64_t q4_launch_count(void) { return q4::g_launches.load(); }
+
+q4_status q4_quantize_rows(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x, float clip,
+                           uint8_t* codes, float* scales, void* stream) {
+  g_err[0] = 0;
+  if (rows < 0 || cols <= 0 || ld_x < cols)
+    return fail(Q4_ESHAPE, "q4_quantize_rows: rows=%lld cols=%lld ld_x=%lld (need rows>=0, cols>0, ld_x>=cols)",
+                (long long)rows, (long long)cols, (long long)ld_x);
+  if (cols % 8 || ld_x % 8)
+    return fail(Q4_ESHAPE, "q4_quantize_rows: cols=%lld and ld_x=%lld must be multiples of 8",
+                (long long)cols, (long long)ld_x);
+  if (cols > (1 << 30)) return fail(Q4_ESHAPE, "q4_quantize_rows: cols=%lld too large", (long long)cols);
+  if (rows == 0) return Q4_OK;
+  if (!x || !codes || !scales) return fail(Q4_EINVAL, "q4_quantize_rows: NULL x/codes/scales");
+  if (!al16(x) || !al4(codes) || !al4(scales))
+    return fail(Q4_EALIGN, "q4_quantize_rows: x must be 16-byte aligned, codes/scales 4-byte aligned");
+  if (!clip_ok(clip)) return fail(Q4_EINVAL, "q4_quantize_rows: clip=%g is not 0 or a positive fp16 value", clip);
+  cudaError_t e = q4::launch_quantize_rows(reinterpret_cast<const __half*>(x), rows, (int)cols, ld_x, clip,
+                                           codes, scales, (cudaStream_t)stream);
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_quantize_rows");
+}
+
+size_t q4_w4a4_linear_workspace(int64_t, int64_t, int64_t, int32_t) { return 0; }
+
+q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const uint8_t* w_codes,
+                         const float* w_scales, int64_t M, int64_t N, int64_t K, const q4_epilogue* epi,
+                         void* workspace, size_t ws_bytes, void* stream) {
+  (void)workspace;
+  (void)ws_bytes;
+  g_err[0] = 0;
+  if (!epi) return fail(Q4_EINVAL, "q4_w4a4_linear: epi is NULL");
+  if (M < 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1 << 24))
+    return fail(Q4_ESHAPE, "q4_w4a4_linear: bad shape M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
+  if (N % 32) return fail(Q4_ESHAPE, "q4_w4a4_linear: N=%lld must be a multiple of 32", (long long)N);
+  if (K % 32) return fail(Q4_ESHAPE, "q4_w4a4_linear: K=%lld must be a multiple of 32 (16-byte packed rows)", (long long)K);
+  if (K > 8192) return fail(Q4_ESHAPE, "q4_w4a4_linear: K=%lld > 8192 would break the INT32 accumulator bound", (long long)K);
+  const int kind = epi->kind;
+  if (kind < Q4_EPI_I32 || kind > Q4_EPI_RESLN_Q4) return fail(Q4_EINVAL, "q4_w4a4_linear: unknown epilogue kind %d", kind);
+  if (M == 0) return Q4_OK;
+  if (!a_codes || !a_scales || !w_codes || !w_scales)
+    return fail(Q4_EINVAL, "q4_w4a4_linear: NULL operand (a_codes/a_scales/w_codes/w_scales)");
+  if (!al16(a_codes) || !al16(w_codes) || !al4(a_scales) || !al4(w_scales))
+    return fail(Q4_EALIGN, "q4_w4a4_linear: codes must be 16-byte aligned, scales 4-byte aligned");
+  switch (kind) {
+    case Q4_EPI_I32:
+      if (!epi->out_i32 || !al16(epi->out_i32)) return fail(Q4_EINVAL, "q4_w4a4_linear(I32): out_i32 NULL or not 16-byte aligned");
+      break;
+    case Q4_EPI_F16:
+      if (!epi->out_f16 || !al16(epi->out_f16)) return fail(Q4_EINVAL, "q4_w4a4_linear(F16): out_f16 NULL or not 16-byte aligned");
+      break;
+    case Q4_EPI_GELU_Q4:
+      if (!epi->out_codes || !epi->out_scales) return fail(Q4_EINVAL, "q4_w4a4_linear(GELU_Q4): out_codes/out_scales NULL");
+      if (!al16(epi->out_codes) || (epi->out_f16 && !al16(epi->out_f16)))
+        return fail(Q4_EALIGN, "q4_w4a4_linear(GELU_Q4): outputs must be 16-byte aligned");
+      break;
+    case Q4_EPI_RESLN_Q4:
+      if (!epi->out_codes || !epi->out_scales || !epi->out_f16 || !epi->residual || !epi->gamma || !epi->beta)
+        return fail(Q4_EINVAL, "q4_w4a4_linear(RESLN_Q4): out_f16/out_codes/out_scales/residual/gamma/beta must be non-NULL");
+      if (!al16(epi->out_codes) || !al16(epi->out_f16) || !al16(epi->residual))
+        return fail(Q4_EALIGN, "q4_w4a4_linear(RESLN_Q4): out_f16/out_codes/residual must be 16-byte aligned");
+      if (!(epi->ln_eps >= 0.f)) return fail(Q4_EINVAL, "q4_w4a4_linear(RESLN_Q4): ln_eps=%g", epi->ln_eps);
+      break;
+  }
+  if (!clip_ok(epi->requant_clip)) return fail(Q4_EINVAL, "q4_w4a4_linear: requant_clip=%g is not 0 or a positive fp16 value", epi->requant_clip);
+  q4::GemmArgs g;
+  g.a_codes = a_codes; g.a_scales = a_scales; g.w_codes = w_codes; g.w_scales = w_scales;
+  g.M = (int)M; g.N = (int)N; g.K = (int)K; g.kind = kind; g.mainloop = epi->mainloop;
+  g.bias = reinterpret_cast<const __half*>(epi->bias);
+  g.residual = reinterpret_cast<const __half*>(epi->residual);
+  g.gamma = reinterpret_cast<const __half*>(epi->gamma);
+  g.beta = reinterpret_cast<const __half*>(epi->beta);
+  g.ln_eps = epi->ln_eps; g.clip = epi->requant_clip;
+  g.out_i32 = epi->out_i32; g.out_f16 = reinterpret_cast<__half*>(epi->out_f16);
+  g.out_codes = epi->out_codes; g.out_scales = epi->out_scales;
+  const char* why = "";
+  cudaError_t e;
+  switch (epi->mainloop) {
+    case Q4_MAINLOOP_AUTO:
+    case Q4_MAINLOOP_TCGEN05: e = q4::launch_w4a4_tc(g, (cudaStream_t)stream, &why); break;
+    case Q4_MAINLOOP_MMA_SYNC_S8: e = q4::launch_w4a4_legacy(g, false, (cudaStream_t)stream, &why); break;
+    case Q4_MAINLOOP_MMA_SYNC_S4: e = q4::launch_w4a4_legacy(g, true, (cudaStream_t)stream, &why); break;
+    default: return fail(Q4_EINVAL, "q4_w4a4_linear: unknown mainloop %d", epi->mainloop);
+  }
+  if (e == cudaErrorNotSupported) return fail(Q4_EUNSUPPORTED, "q4_w4a4_linear: %s (M=%lld N=%lld K=%lld)", why, (long long)M, (long long)N, (long long)K);
+  if (e != cudaSuccess) return fail(Q4_ECUDA, "q4_w4a4_linear: %s %s", cudaGetErrorString(e), why);
+  return Q4_OK;
+}
+
+q4_status q4_attention_f16_q4(const uint16_t* qkv, int64_t B, int64_t S, int32_t heads, int32_t head_dim,
+                              uint16_t* ctx_f16, uint8_t* ctx_codes, float* ctx_scales, void* stream) {
+  g_err[0] = 0;
+  if (head_dim != 64) return fail(Q4_EUNSUPPORTED, "q4_attention_f16_q4: head_dim=%d (only 64)", head_dim);
+  if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "q4_attention_f16_q4: B=%lld S=%lld (need B>=0, 1<=S<=128)", (long long)B, (long long)S);
+  if (heads < 1 || heads * 64 > 1024) return fail(Q4_ESHAPE, "q4_attention_f16_q4: heads=%d (need 1..16)", heads);
+  if (B > 65535) return fail(Q4_ESHAPE, "q4_attention_f16_q4: B=%lld > 65535", (long long)B);
+  if (B == 0) return Q4_OK;
+  if (!qkv || !ctx_codes || !ctx_scales) return fail(Q4_EINVAL, "q4_attention_f16_q4: NULL qkv/ctx_codes/ctx_scales");
+  if (!al16(qkv) || !al4(ctx_codes) || (ctx_f16 && !al16(ctx_f16)))
+    return fail(Q4_EALIGN, "q4_attention_f16_q4: qkv/ctx_f16 must be 16-byte aligned, codes 4-byte");
+  cudaError_t e = q4::launch_attention(reinterpret_cast<const __half*>(qkv), (int)B, (int)S, heads,
+                                       reinterpret_cast<__half*>(ctx_f16), ctx_codes, ctx_scales, (cudaStream_t)stream);
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_attention_f16_q4");
+}
+
+// ------------------------------------------------------------------ encoder layer
+
+namespace {
+struct LayerWs {
+  uint16_t* qkv;
+  uint8_t* ctx_codes;
+  float* ctx_scales;
+  uint16_t* h1;
+  uint8_t* h1_codes;
+  float* h1_scales;
+  uint8_t* f_codes;
+  float* f_scales;
+  size_t bytes;
+};
+LayerWs layer_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base) {
+  LayerWs w;
+  size_t o = 0;
+  const int64_t h = c->hidden, f = c->ffn;
+  auto take = [&](size_t n) { size_t r = o; o = align_up(o + n); return base ? base + r : nullptr; };
+  w.qkv = (uint16_t*)take((size_t)M * 3 * h * 2);
+  w.ctx_codes = take((size_t)M * h / 2);
+  w.ctx_scales = (float*)take((size_t)M * 4);
+  w.h1 = (uint16_t*)take((size_t)M * h * 2);
+  w.h1_codes = take((size_t)M * h / 2);
+  w.h1_scales = (float*)take((size_t)M * 4);
+  w.f_codes = take((size_t)M * f / 2);
+  w.f_scales = (float*)take((size_t)M * 4);
+  w.bytes = o;
+  return w;
+}
+q4_status check_cfg(const q4_layer_cfg* c, const char* who) {
+  if (!c) return fail(Q4_EINVAL, "%s: cfg is NULL", who);
+  if (c->head_dim != 64 || c->heads < 1 || c->heads * 64 != c->hidden || c->hidden > 1024)
+    return fail(Q4_EUNSUPPORTED, "%s: hidden=%d heads=%d head_dim=%d (need head_dim 64, hidden = 64*heads <= 1024)",
+                who, c->hidden, c->heads, c->head_dim);
+  if (c->ffn % 32 || c->ffn <= 0 || c->ffn > 4096) return fail(Q4_ESHAPE, "%s: ffn=%d (need multiple of 32, <= 4096)", who, c->ffn);
+  return Q4_OK;
+}
+}  // namespace
+
+size_t q4_encoder_layer_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S) {
+  if (!cfg) return 0;
+  return layer_ws(cfg, B * S, nullptr).bytes;
+}
+
+q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B, int64_t S,
+                           const uint16_t* h_in, const uint8_t* hq_in, const float* hs_in, uint16_t* h_out,
+                           uint8_t* hq_out, float* hs_out, void* workspace, size_t ws_bytes, const q4_taps* taps,
+                           void* stream) {
+  g_err[0] = 0;
+  q4_status st = check_cfg(cfg, "q4_encoder_layer");
+  if (st) return st;
+  if (!w) return fail(Q4_EINVAL, "q4_encoder_layer: weights NULL");
+  if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "q4_encoder_layer: B=%lld S=%lld", (long long)B, (long long)S);
+  const int64_t M = B * S, h = cfg->hidden, f = cfg->ffn;
+  if (M == 0) return Q4_OK;
+  LayerWs ws = layer_ws(cfg, M, (uint8_t*)workspace);
+  if (!workspace || ws_bytes < ws.bytes)
+    return fail(Q4_EINVAL, "q4_encoder_layer: workspace %zu bytes < required %zu", ws_bytes, ws.bytes);
+  q4_taps tp;
+  memset(&tp, 0, sizeof tp);
+  if (taps) tp = *taps;
+  // taps redirect the intermediates that have a tap buffer of the same layout
+  uint16_t* qkv = tp.qkv ? tp.qkv : ws.qkv;
+  uint8_t* ctx_codes = tp.ctx_codes ? tp.ctx_codes : ws.ctx_codes;
+  float* ctx_scales = tp.ctx_scales ? tp.ctx_scales : ws.ctx_scales;
+  uint16_t* h1 = tp.h1 ? tp.h1 : ws.h1;
+  uint8_t* h1_codes = tp.h1_codes ? tp.h1_codes : ws.h1_codes;
+  float* h1_scales = tp.h1_scales ? tp.h1_scales : ws.h1_scales;
+  uint8_t* f_codes = tp.f_codes ? tp.f_codes : ws.f_codes;
+  float* f_scales = tp.f_scales ? tp.f_scales : ws.f_scales;
+
+  auto lin = [&](const uint8_t* ac, const float* as, const uint8_t* wc, const float* wsc, int64_t N, int64_t K,
+                 q4_epilogue e) -> q4_status { return q4_w4a4_linear(ac, as, wc, wsc, M, N, K, &e, nullptr, 0, stream); };
+  auto acc_tap = [&](const uint8_t* ac, const float* as, const uint8_t* wc, const float* wsc, int64_t N, int64_t K,
+                     int32_t* out) -> q4_status {
+    if (!out) return Q4_OK;
+    q4_epilogue e;
+    memset(&e, 0, sizeof e);
+    e.kind = Q4_EPI_I32;
+    e.out_i32 = out;
+    return q4_w4a4_linear(ac, as, wc, wsc, M, N, K, &e, nullptr, 0, stream);
+  };
+  q4_epilogue e;
+  // QKV projection: dequant + bias -> fp16
+  memset(&e, 0, sizeof e);
+  e.kind = Q4_EPI_F16; e.bias = w->bqkv; e.out_f16 = qkv;
+  if ((st = lin(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, e))) return st;
+  if ((st = acc_tap(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, tp.acc_qkv))) return st;
+  // FP16 attention + fused per-token ctx quantize
+  if ((st = q4_attention_f16_q4(qkv, B, S, cfg->heads, cfg->head_dim, tp.ctx, ctx_codes, ctx_scales, stream))) return st;
+  // attention output: dequant + bias + residual(h_in) + LN1 + requant
+  memset(&e, 0, sizeof e);
+  e.kind = Q4_EPI_RESLN_Q4; e.bias = w->bo; e.residual = h_in; e.gamma = w->ln1_g; e.beta = w->ln1_b;
+  e.ln_eps = cfg->ln_eps; e.out_f16 = h1; e.out_codes = h1_codes; e.out_scales = h1_scales;
+  if ((st = lin(ctx_codes, ctx_scales, w->wo, w->so, h, h, e))) return st;
+  if ((st = acc_tap(ctx_codes, ctx_scales, w->wo, w->so, h, h, tp.acc_o))) return st;
+  // MLP intermediate: dequant + bias + GELU + requant
+  memset(&e, 0, sizeof e);
+  e.kind = Q4_EPI_GELU_Q4; e.bias = w->b1; e.out_f16 = tp.ffn1; e.out_codes = f_codes; e.out_scales = f_scales;
+  if ((st = lin(h1_codes, h1_scales, w->w1, w->s1, f, h, e))) return st;
+  if ((st = acc_tap(h1_codes, h1_scales, w->w1, w->s1, f, h, tp.acc_1))) return st;
+  // MLP output: dequant + bias + residual(h1) + LN2 + requant
+  memset(&e, 0, sizeof e);
+  e.kind = Q4_EPI_RESLN_Q4; e.bias = w->b2; e.residual = h1; e.gamma = w->ln2_g; e.beta = w->ln2_b;
+  e.ln_eps = cfg->ln_eps; e.out_f16 = h_out; e.out_codes = hq_out; e.out_scales = hs_out;
+  if ((st = lin(f_codes, f_scales, w->w2, w->s2, h, f, e))) return st;
+  if ((st = acc_tap(f_codes, f_scales, w->w2, w->s2, h, f, tp.acc_2))) return st;
+  return Q4_OK;
+}
+
+// ------------------------------------------------------------------ encoder stack
+
+namespace {
+struct StackWs {
+  uint16_t* hid[2];
+  uint8_t* hq[2];
+  float* hs[2];
+  uint8_t* layer;
+  size_t layer_bytes, bytes;
+};
+StackWs stack_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base) {
+  StackWs w;
+  size_t o = 0;
+  auto take = [&](size_t n) { size_t r = o; o = align_up(o + n); return base ? base + r : nullptr; };
+  for (int i = 0; i < 2; ++i) {
+    w.hid[i] = (uint16_t*)take((size_t)M * c->hidden * 2);
+    w.hq[i] = take((size_t)M * c->hidden / 2);
+    w.hs[i] = (float*)take((size_t)M * 4);
+  }
+  w.layer_bytes = layer_ws(c, M, nullptr).bytes;
+  w.layer = take(w.layer_bytes);
+  w.bytes = o;
+  return w;
+}
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+}  // namespace
+
+size_t q4_encoder_stack_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S) {
+  if (!cfg) return 0;
+  return stack_ws(cfg, B * S, nullptr).bytes;
+}
+
+q4_status q4_encoder_stack(const q4_layer_cfg* cfg, const q4_layer_weights* layers, int32_t L, int64_t B, int64_t S,
+                           const uint16_t* h_in, uint16_t* h_out, void* workspace, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  q4_status st = check_cfg(cfg, "q4_encoder_stack");
+  if (st) return st;
+  if (L < 1 || !layers) return fail(Q4_EINVAL, "q4_encoder_stack: L=%d layers=%p", L, (const void*)layers);
+  if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "q4_encoder_stack: B=%lld S=%lld", (long long)B, (long long)S);
+  const int64_t M = B * S, h = cfg->hidden;
+  if (M == 0) return Q4_OK;
+  if (!h_in || !h_out) return fail(Q4_EINVAL, "q4_encoder_stack: NULL h_in/h_out");
+  StackWs ws = stack_ws(cfg, M, (uint8_t*)workspace);
+  if (!workspace || ws_bytes < ws.bytes)
+    return fail(Q4_EINVAL, "q4_encoder_stack: workspace %zu bytes < required %zu", ws_bytes, ws.bytes);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t hbytes = (size_t)M * h * 2;
+  const uint16_t* x = h_in;
+  if (!is_device_ptr(h_in)) {  // end-to-end entry: host input copied inside the call
+    cudaError_t e = cudaMemcpyAsync(ws.hid[1], h_in, hbytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "q4_encoder_stack: H2D copy");
+    x = ws.hid[1];
+  } else if (!al16(h_in)) {
+    return fail(Q4_EALIGN, "q4_encoder_stack: h_in must be 16-byte aligned");
+  }
+  // layer-0 activation quantize (the only standalone quantize in the forward)
+  if ((st = q4_quantize_rows(x, M, h, h, 0.f, ws.hq[1], ws.hs[1], stream))) return st;
+  const bool out_dev = is_device_ptr(h_out);
+  for (int l = 0; l < L; ++l) {
+    const int o = l & 1;
+    const uint16_t* hin = (l == 0) ? x : ws.hid[1 - o];
+    uint16_t* hout = (l == L - 1 && out_dev) ? h_out : ws.hid[o];
+    if ((st = q4_encoder_layer(cfg, &layers[l], B, S, hin, ws.hq[1 - o], ws.hs[1 - o], hout, ws.hq[o], ws.hs[o],
+                               ws.layer, ws.layer_bytes, nullptr, stream)))
+      return st;
+  }
+  if (!out_dev) {
+    cudaError_t e = cudaMemcpyAsync(h_out, ws.hid[(L - 1) & 1], hbytes, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "q4_encoder_stack: D2H copy");
+  }
+  return Q4_OK;
+}
+
+}  // extern "C"

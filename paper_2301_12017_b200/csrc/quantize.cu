@@ -1,0 +1,126 @@
+// quantize.cu -- a1/a2: symmetric per-row INT4 quantize + pack (PAPER.md:703-708,
+// 517-522; readings R1-R3, R5, R10).  Memory-bound: 2 B/elem in, 0.5 B/elem + 4 B/row out.
+//
+// One warp per row.  Each lane owns 16-byte vectors (8 halves) v = lane + 32*i, kept
+// in registers between the two passes (warp-shuffle max-abs, then codes), so x is read
+// from HBM exactly once.  Codes: rint(div.rn(7x, amax)) -- the IEEE-exact form that
+// equals round-half-even of the rational 7x/amax for every fp16 pair (R3).
+#include "kernels.h"
+
+namespace q4 {
+
+template <int MAXV>
+__global__ void __launch_bounds__(256) quantize_rows_kernel(const __half* __restrict__ x,
+                                                            int64_t rows, int cols, int64_t ld_x,
+                                                            float clip, uint8_t* __restrict__ codes,
+                                                            float* __restrict__ scales) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nvec = cols >> 3;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * ld_x);
+  uint4 v[MAXV];
+  float amax = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int vi = lane + 32 * i;
+    if (vi < nvec) {
+      v[i] = __ldg(xr + vi);
+      const uint32_t* u = reinterpret_cast<const uint32_t*>(&v[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = unpack_half2(u[j]);
+        if (clip > 0.f) {
+          f.x = fminf(fmaxf(f.x, -clip), clip);
+          f.y = fminf(fmaxf(f.y, -clip), clip);
+        }
+        amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  uint32_t* cr = reinterpret_cast<uint32_t*>(codes + row * (int64_t)(cols >> 1));
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int vi = lane + 32 * i;
+    if (vi < nvec) {
+      const uint32_t* u = reinterpret_cast<const uint32_t*>(&v[i]);
+      int q[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = unpack_half2(u[j]);
+        if (clip > 0.f) {
+          f.x = fminf(fmaxf(f.x, -clip), clip);
+          f.y = fminf(fmaxf(f.y, -clip), clip);
+        }
+        q[2 * j] = amax > 0.f ? q4_code(f.x, amax) : 0;
+        q[2 * j + 1] = amax > 0.f ? q4_code(f.y, amax) : 0;
+      }
+      cr[vi] = pack8(q);
+    }
+  }
+  if (lane == 0) scales[row] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
+}
+
+// Rows longer than 32*16*8 = 4096: two passes over global memory.
+__global__ void __launch_bounds__(256) quantize_rows_long_kernel(const __half* __restrict__ x,
+                                                                 int64_t rows, int cols,
+                                                                 int64_t ld_x, float clip,
+                                                                 uint8_t* __restrict__ codes,
+                                                                 float* __restrict__ scales) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nvec = cols >> 3;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * ld_x);
+  float amax = 0.f;
+  for (int vi = lane; vi < nvec; vi += 32) {
+    uint4 vv = __ldg(xr + vi);
+    const uint32_t* u = reinterpret_cast<const uint32_t*>(&vv);
+    for (int j = 0; j < 4; ++j) {
+      float2 f = unpack_half2(u[j]);
+      if (clip > 0.f) {
+        f.x = fminf(fmaxf(f.x, -clip), clip);
+        f.y = fminf(fmaxf(f.y, -clip), clip);
+      }
+      amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  uint32_t* cr = reinterpret_cast<uint32_t*>(codes + row * (int64_t)(cols >> 1));
+  for (int vi = lane; vi < nvec; vi += 32) {
+    uint4 vv = __ldg(xr + vi);
+    const uint32_t* u = reinterpret_cast<const uint32_t*>(&vv);
+    int q[8];
+    for (int j = 0; j < 4; ++j) {
+      float2 f = unpack_half2(u[j]);
+      if (clip > 0.f) {
+        f.x = fminf(fmaxf(f.x, -clip), clip);
+        f.y = fminf(fmaxf(f.y, -clip), clip);
+      }
+      q[2 * j] = amax > 0.f ? q4_code(f.x, amax) : 0;
+      q[2 * j + 1] = amax > 0.f ? q4_code(f.y, amax) : 0;
+    }
+    cr[vi] = pack8(q);
+  }
+  if (lane == 0) scales[row] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
+}
+
+cudaError_t launch_quantize_rows(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
+                                 uint8_t* codes, float* scales, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  const int warps = 8;
+  const dim3 grid((unsigned)((rows + warps - 1) / warps)), block(32 * warps);
+  const int nvec = cols / 8;
+  note_launch();
+  if (nvec <= 32) quantize_rows_kernel<1><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
+  else if (nvec <= 64) quantize_rows_kernel<2><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
+  else if (nvec <= 128) quantize_rows_kernel<4><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
+  else if (nvec <= 256) quantize_rows_kernel<8><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
+  else if (nvec <= 512) quantize_rows_kernel<16><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
+  else quantize_rows_long_kernel<<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
+  return cudaGetLastError();
+}
+
+}  // namespace q4

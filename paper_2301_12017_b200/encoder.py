@@ -1,0 +1,62 @@
+"""a8: the L-layer W4A4 BERT encoder: one q4_encoder_stack call per
+forward -- initial activation quantize + L x [QKV, attention, attn-out, FFN1, FFN2] --
+optionally captured once into a CUDA graph and replayed ("we enable CUDA graph in our
+inference pipeline to minimize such overhead").  Marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import ops
+from ._lib import LayerWeights, check, lib
+
+
+class W4A4Encoder:
+    def __init__(self, cfg: dict, layers: list, device="cuda"):
+        """cfg: BERT dims (hidden, heads, head_dim, ffn, ln_eps); layers: per-layer fp16
+        parameter dicts (synth.layer_params) -- quantized on the device here (offline)."""
+        self.cfg = dict(cfg)
+        self.device = torch.device(device)
+        self.weights = [ops.quantize_layer(p, self.device) for p in layers]
+        self.L = len(self.weights)
+        self._lw = (LayerWeights * self.L)(*[ops.layer_weights(w) for w in self.weights])
+        self._lc = ops.layer_cfg(self.cfg)
+        self._ws = None
+        self._ws_shape = None
+        self.graph = None
+
+    def workspace(self, B: int, S: int) -> torch.Tensor:
+        if self._ws_shape != (B, S):
+            n = lib().q4_encoder_stack_workspace(C.byref(self._lc), B, S)
+            self._ws = torch.empty(max(n, 1), dtype=torch.uint8, device=self.device)
+            self._ws_shape = (B, S)
+        return self._ws
+
+    def forward(self, h_in: torch.Tensor, h_out: torch.Tensor, B: int, S: int):
+        """h_in / h_out: fp16 [B*S, hidden], CUDA tensors or (pinned) CPU tensors -- with
+        host tensors the H2D / D2H copies happen inside the C call (end-to-end path)."""
+        ws = self.workspace(B, S)
+        check(lib().q4_encoder_stack(C.byref(self._lc), self._lw, self.L, B, S,
+                                     C.c_void_p(h_in.data_ptr()), C.c_void_p(h_out.data_ptr()),
+                                     C.c_void_p(ws.data_ptr()), ws.numel(),
+                                     C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return h_out
+
+    def capture(self, h_in: torch.Tensor, h_out: torch.Tensor, B: int, S: int, warmup: int = 1):
+        """Capture forward(h_in -> h_out) (device buffers) into a CUDA graph."""
+        self.workspace(B, S)
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.forward(h_in, h_out, B, S)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.forward(h_in, h_out, B, S)
+        self.graph = g
+        return g
+
+    def replay(self):
+        self.graph.replay()

@@ -1,0 +1,145 @@
+"""torch-facing wrappers over the C ABI (include/q4.h) -- marshalling only.
+
+Tensors must be CUDA tensors of the documented dtype/shape; outputs are allocated with
+torch and filled by the library on torch's current stream."""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from ._lib import (EPI_F16, EPI_GELU_Q4, EPI_I32, EPI_RESLN_Q4, Epilogue, LayerCfg,
+                   LayerWeights, Taps, check, lib)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _need(t, dtype, name, dims=None):
+    if t is None:
+        return
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dims is not None and t.dim() != dims:
+        raise ValueError(f"{name} must be {dims}-D, got shape {tuple(t.shape)}")
+
+
+def quantize_rows(x: torch.Tensor, clip: float = 0.0, codes=None, scales=None):
+    """a1/a2: fp16 [rows, cols] -> (packed INT4 codes uint8 [rows, cols/2], fp32 scales [rows])."""
+    _need(x, torch.float16, "x", 2)
+    rows, cols = x.shape
+    if codes is None:
+        codes = torch.empty(rows, cols // 2, dtype=torch.uint8, device=x.device)
+    if scales is None:
+        scales = torch.empty(rows, dtype=torch.float32, device=x.device)
+    check(lib().q4_quantize_rows(_ptr(x), rows, cols, cols, clip, _ptr(codes), _ptr(scales), _stream()))
+    return codes, scales
+
+
+def w4a4_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None, residual=None,
+                gamma=None, beta=None, ln_eps=1e-12, clip=0.0, mainloop=0, f16_tap=False,
+                out=None):
+    """a3-a6: INT4 x INT4 -> exact INT32 -> fused epilogue.  Returns a dict with the
+    outputs of the epilogue kind: i32 | f16 | (codes, scales[, f16])."""
+    _need(a_codes, torch.uint8, "a_codes", 2)
+    _need(w_codes, torch.uint8, "w_codes", 2)
+    _need(a_scales, torch.float32, "a_scales", 1)
+    _need(w_scales, torch.float32, "w_scales", 1)
+    for n, t in (("bias", bias), ("residual", residual), ("gamma", gamma), ("beta", beta)):
+        _need(t, torch.float16, n)
+    M, K = a_codes.shape[0], a_codes.shape[1] * 2
+    N = w_codes.shape[0]
+    if w_codes.shape[1] * 2 != K:
+        raise ValueError(f"K mismatch: a_codes {tuple(a_codes.shape)} vs w_codes {tuple(w_codes.shape)}")
+    dev = a_codes.device
+    o = dict(out or {})
+    if kind == EPI_I32:
+        o.setdefault("i32", torch.empty(M, N, dtype=torch.int32, device=dev))
+    if kind in (EPI_F16, EPI_RESLN_Q4) or (kind == EPI_GELU_Q4 and f16_tap):
+        o.setdefault("f16", torch.empty(M, N, dtype=torch.float16, device=dev))
+    if kind in (EPI_GELU_Q4, EPI_RESLN_Q4):
+        o.setdefault("codes", torch.empty(M, N // 2, dtype=torch.uint8, device=dev))
+        o.setdefault("scales", torch.empty(M, dtype=torch.float32, device=dev))
+    e = Epilogue(kind=kind, mainloop=mainloop, bias=_ptr(bias), residual=_ptr(residual),
+                 gamma=_ptr(gamma), beta=_ptr(beta), ln_eps=ln_eps, requant_clip=clip,
+                 out_i32=_ptr(o.get("i32")), out_f16=_ptr(o.get("f16")),
+                 out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")))
+    check(lib().q4_w4a4_linear(_ptr(a_codes), _ptr(a_scales), _ptr(w_codes), _ptr(w_scales),
+                               M, N, K, C.byref(e), None, 0, _stream()))
+    return o
+
+
+def attention_f16_q4(qkv, B, S, heads, head_dim=64, f16_tap=False):
+    """a7: fp16 QKV [B*S, 3h] -> (ctx codes [B*S, h/2], ctx scales [B*S][, ctx fp16])."""
+    _need(qkv, torch.float16, "qkv", 2)
+    h = heads * head_dim
+    dev = qkv.device
+    codes = torch.empty(B * S, h // 2, dtype=torch.uint8, device=dev)
+    scales = torch.empty(B * S, dtype=torch.float32, device=dev)
+    ctx = torch.empty(B * S, h, dtype=torch.float16, device=dev) if f16_tap else None
+    check(lib().q4_attention_f16_q4(_ptr(qkv), B, S, heads, head_dim, _ptr(ctx), _ptr(codes),
+                                    _ptr(scales), _stream()))
+    return (codes, scales, ctx) if f16_tap else (codes, scales)
+
+
+def layer_cfg(cfg: dict) -> LayerCfg:
+    return LayerCfg(cfg["hidden"], cfg["heads"], cfg["head_dim"], cfg["ffn"], cfg.get("ln_eps", 1e-12))
+
+
+def layer_weights(w: dict) -> LayerWeights:
+    """w: dict of CUDA tensors (codes uint8, scales fp32, biases / LN params fp16)."""
+    return LayerWeights(**{k: w[k].data_ptr() for k in _lib.WEIGHT_FIELDS})
+
+
+def quantize_layer(params: dict, device="cuda") -> dict:
+    """Offline weight prep (a2, not timed): fp16 [out, in] weights -> per-output-channel
+    INT4 codes + scales on the device; biases and LN parameters copied as fp16."""
+    w = {}
+    for k in ("wqkv", "wo", "w1", "w2"):
+        t = torch.as_tensor(params[k]).to(device=device, dtype=torch.float16).contiguous()
+        w[k], w["s" + k[1:]] = quantize_rows(t)
+    for k in ("bqkv", "bo", "b1", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b"):
+        w[k] = torch.as_tensor(params[k]).to(device=device, dtype=torch.float16).contiguous()
+    return w
+
+
+def encoder_layer(cfg: dict, w: dict, B: int, S: int, h_in, hq_in, hs_in, taps: bool = False,
+                  workspace=None):
+    """a8: one post-LN BERT layer (qall).  Returns dict(h_out, hq_out, hs_out[, taps...])."""
+    M, h, f = B * S, cfg["hidden"], cfg["ffn"]
+    dev = h_in.device
+    lc = layer_cfg(cfg)
+    ws_bytes = lib().q4_encoder_layer_workspace(C.byref(lc), B, S)
+    if workspace is None:
+        workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    out = {"h_out": torch.empty(M, h, dtype=torch.float16, device=dev),
+           "hq_out": torch.empty(M, h // 2, dtype=torch.uint8, device=dev),
+           "hs_out": torch.empty(M, dtype=torch.float32, device=dev)}
+    tp = None
+    if taps:
+        shapes = {"qkv": ((M, 3 * h), torch.float16), "ctx": ((M, h), torch.float16),
+                  "h1": ((M, h), torch.float16), "ffn1": ((M, f), torch.float16),
+                  "acc_qkv": ((M, 3 * h), torch.int32), "acc_o": ((M, h), torch.int32),
+                  "acc_1": ((M, f), torch.int32), "acc_2": ((M, h), torch.int32),
+                  "ctx_codes": ((M, h // 2), torch.uint8), "h1_codes": ((M, h // 2), torch.uint8),
+                  "f_codes": ((M, f // 2), torch.uint8), "ctx_scales": ((M,), torch.float32),
+                  "h1_scales": ((M,), torch.float32), "f_scales": ((M,), torch.float32)}
+        for k, (shp, dt) in shapes.items():
+            out[k] = torch.empty(shp, dtype=dt, device=dev)
+        tp = Taps(**{k: out[k].data_ptr() for k in _lib.TAP_FIELDS})
+    lw = layer_weights(w)
+    check(lib().q4_encoder_layer(C.byref(lc), C.byref(lw), B, S, _ptr(h_in), _ptr(hq_in),
+                                 _ptr(hs_in), _ptr(out["h_out"]), _ptr(out["hq_out"]),
+                                 _ptr(out["hs_out"]), _ptr(workspace), workspace.numel(),
+                                 C.byref(tp) if tp is not None else None, _stream()))
+    return out

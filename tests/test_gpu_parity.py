@@ -1,0 +1,313 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Bars (BASELINE.json north_star): INT4 codes, scales and INT32
+accumulators bit-exact; fp16 outputs within |gpu - ref| <= 1e-3 + 2e-3 |ref|.
+Where fp16 decides an integer (requant codes), both sides decide from the GPU's fp16
+value: codes == oracle.quantize_rows(gpu fp16)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from paper_2301_12017_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 2e-3, 1e-3
+
+
+@pytest.fixture(scope="module")
+def q4():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2301_12017_b200 as q4
+    q4.lib()
+    return q4
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def assert_f16_close(got, ref, what=""):
+    g, r = got.astype(np.float64), ref.astype(np.float64)
+    err = np.abs(g - r) - (ATOL + RTOL * np.abs(r))
+    bad = np.argwhere(err > 0)
+    assert bad.size == 0, f"{what}: {len(bad)} elements out of tolerance, first {bad[:3].tolist()} " \
+                          f"got {g[tuple(bad[0])]} ref {r[tuple(bad[0])]}"
+
+
+def edge_rows(cols):
+    """all-zero, single outlier, exact ties, +-amax, tiny (subnormal) rows."""
+    z = np.zeros((6, cols), np.float32)
+    z[1, 3] = 40.0
+    z[1, 5:] = 0.01
+    z[2, :] = np.resize([7.0, 2.5, -2.5, 0.5, -0.5, 1.5, -1.5, 6.5], cols)
+    z[3, :] = np.resize([3.0, -3.0], cols)
+    z[4, :] = np.resize([6e-8, -1.2e-7, 3e-8], cols)
+    z[5, :] = 65504.0
+    return z.astype(np.float16)
+
+
+# ------------------------------------------------------------------ a1 quantize
+@pytest.mark.parametrize("rows,cols", [(1, 768), (127, 1024), (129, 3072), (513, 4096), (64, 8192), (3, 64)])
+def test_quantize_rows_bit_exact(q4, rows, cols):
+    x = np.concatenate([synth.hidden(rows, cols, f"tq{rows}_{cols}"), edge_rows(cols)])
+    c, s = q4.quantize_rows(dev(x))
+    rc, rs = orc.quantize_rows(x)
+    assert np.array_equal(host(c), rc)
+    assert np.array_equal(host(s), rs)
+
+
+def test_quantize_rows_clip(q4):
+    x = synth.hidden(300, 1024, "tqclip")
+    c, s = q4.quantize_rows(dev(x), clip=5.0)
+    rc, rs = orc.quantize_rows(x, clip=5.0)
+    assert np.array_equal(host(c), rc) and np.array_equal(host(s), rs)
+
+
+# ------------------------------------------------------------------ a3 integer GEMM
+SHAPES = [(1, 256, 256), (127, 768, 768), (129, 3072, 768), (300, 768, 3072), (256, 4096, 1024),
+          (200, 2304, 768), (64, 1024, 4096), (130, 96, 1024), (128, 32, 32)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("mainloop", [1, 2, 3], ids=["tcgen05", "mma_s8", "mma_s4"])
+def test_gemm_i32_bit_exact(q4, M, N, K, mainloop):
+    a = synth.random_packed(M, K, f"ga{M}_{K}", full_range=True)
+    w = synth.random_packed(N, K, f"gw{N}_{K}", full_range=True)
+    sa, sw = synth.random_scales(M, "gsa"), synth.random_scales(N, "gsw")
+    out = q4.w4a4_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_I32, mainloop=mainloop)
+    ref = orc.gemm_i32(a, w, M, N, K)
+    got = host(out["i32"])
+    assert np.array_equal(got, ref), f"{np.count_nonzero(got != ref)} mismatches"
+
+
+def test_gemm_extreme_codes(q4):
+    M, N, K = 130, 256, 4096
+    a = np.full((M, K // 2), 0x88, np.uint8)  # all -8: |acc| = 64 K, the INT32 bound
+    w = np.full((N, K // 2), 0x88, np.uint8)
+    w[1::2] = 0x77
+    one = np.ones(max(M, N), np.float32)
+    out = q4.w4a4_linear(dev(a), dev(one[:M]), dev(w), dev(one[:N]), q4.EPI_I32)
+    assert np.array_equal(host(out["i32"]), orc.gemm_i32(a, w, M, N, K))
+
+
+# ------------------------------------------------------------------ a4 dequant epilogue
+@pytest.mark.parametrize("M,N,K", [(1, 768, 768), (129, 2304, 768), (300, 3072, 1024), (77, 1024, 4096)])
+@pytest.mark.parametrize("mainloop", [1, 2], ids=["tcgen05", "mma_s8"])
+def test_linear_f16(q4, M, N, K, mainloop):
+    x, wt, b = synth.hidden(M, K, f"fx{M}"), synth.weight(N, K, f"fw{N}_{K}"), synth.bias(N, f"fb{N}")
+    a, sa = orc.quantize_rows(x)
+    w, sw = orc.quantize_rows(wt)
+    out = q4.w4a4_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_F16, bias=dev(b), mainloop=mainloop)
+    ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, orc.EPI_F16, bias=b)["f16"]
+    assert_f16_close(host(out["f16"]), ref, "F16")
+
+
+# ------------------------------------------------------------------ a5 GELU + requant
+@pytest.mark.parametrize("M,N,K", [(128, 3072, 768), (257, 4096, 1024), (33, 768, 768), (5, 256, 256), (100, 2048, 512)])
+def test_linear_gelu_q4(q4, M, N, K):
+    x, wt, b = synth.hidden(M, K, f"gx{M}"), synth.weight(N, K, f"gw{N}_{K}"), synth.bias(N, f"gb{N}")
+    a, sa = orc.quantize_rows(x)
+    w, sw = orc.quantize_rows(wt)
+    out = q4.w4a4_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_GELU_Q4, bias=dev(b), f16_tap=True)
+    ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, orc.EPI_GELU_Q4, bias=b)
+    y = host(out["f16"])
+    assert_f16_close(y, ref["f16"], "GELU f16")
+    c2, s2 = orc.quantize_rows(y)  # codes decided from the GPU's own fp16 (R13)
+    assert np.array_equal(host(out["codes"]), c2)
+    assert np.array_equal(host(out["scales"]), s2)
+    # the codes also agree with the free-running oracle except where fp16 differs
+    mism = np.count_nonzero(host(out["codes"]) != ref["codes"]) / ref["codes"].size
+    assert mism < 1e-2
+
+
+# ------------------------------------------------------------------ a6 residual + LN + requant
+@pytest.mark.parametrize("M,N,K", [(128, 768, 768), (257, 1024, 1024), (300, 768, 3072), (64, 1024, 4096), (7, 256, 512)])
+def test_linear_resln_q4(q4, M, N, K):
+    x, wt, b = synth.hidden(M, K, f"lx{M}"), synth.weight(N, K, f"lw{N}_{K}"), synth.bias(N, f"lb{N}")
+    res = synth.hidden(M, N, f"lr{M}_{N}")
+    gam, bet = synth.ln_params(N, f"ln{N}")
+    a, sa = orc.quantize_rows(x)
+    w, sw = orc.quantize_rows(wt)
+    out = q4.w4a4_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_RESLN_Q4, bias=dev(b),
+                         residual=dev(res), gamma=dev(gam), beta=dev(bet), ln_eps=1e-12)
+    ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, orc.EPI_RESLN_Q4, bias=b, residual=res, gamma=gam,
+                          beta=bet, ln_eps=1e-12)
+    y = host(out["f16"])
+    assert_f16_close(y, ref["f16"], "RESLN f16")
+    c2, s2 = orc.quantize_rows(y)
+    assert np.array_equal(host(out["codes"]), c2)
+    assert np.array_equal(host(out["scales"]), s2)
+
+
+def test_resln_degenerate_rows(q4):
+    """constant row -> beta; gamma = 0 -> beta, through the fused kernel."""
+    M, N, K = 4, 768, 768
+    a = np.zeros((M, K // 2), np.uint8)
+    w = synth.random_packed(N, K, "ldeg")
+    sa, sw = np.ones(M, np.float32), synth.random_scales(N, "ldegs")
+    res = np.full((M, N), 3.25, np.float16)
+    res[2] = -1000.0
+    gam, bet = synth.ln_params(N, "ldegln")
+    out = q4.w4a4_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_RESLN_Q4, residual=dev(res),
+                         gamma=dev(gam), beta=dev(bet))
+    y = host(out["f16"])
+    assert np.array_equal(y, np.broadcast_to(bet, y.shape))
+    ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, orc.EPI_RESLN_Q4, residual=res, gamma=gam, beta=bet)
+    assert np.array_equal(host(out["codes"]), ref["codes"])
+
+
+def test_requant_clip(q4):
+    M, N, K = 64, 1024, 512
+    x, wt = synth.hidden(M, K, "cx"), synth.weight(N, K, "cw")
+    a, sa = orc.quantize_rows(x)
+    w, sw = orc.quantize_rows(wt)
+    sa = sa * 50
+    out = q4.w4a4_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_GELU_Q4, clip=5.0, f16_tap=True)
+    c2, s2 = orc.quantize_rows(host(out["f16"]), clip=5.0)
+    assert np.array_equal(host(out["codes"]), c2) and np.array_equal(host(out["scales"]), s2)
+
+
+# ------------------------------------------------------------------ a7 attention
+@pytest.mark.parametrize("B,S,H", [(2, 128, 12), (3, 128, 16), (2, 100, 4), (4, 1, 2), (1, 77, 16)])
+def test_attention(q4, B, S, H):
+    qkv = synth.hidden(B * S, 3 * H * 64, f"aq{B}_{S}_{H}")
+    codes, scales, ctx = q4.attention_f16_q4(dev(qkv), B, S, H, 64, f16_tap=True)
+    rctx, _, _ = orc.attention(qkv, B, S, H, 64)
+    c = host(ctx)
+    assert_f16_close(c, rctx, "ctx")
+    c2, s2 = orc.quantize_rows(c)
+    assert np.array_equal(host(codes), c2) and np.array_equal(host(scales), s2)
+
+
+# ------------------------------------------------------------------ a8 encoder layer
+def _layer_setup(cfg, B, S, seed="enc"):
+    p = synth.layer_params(cfg, 0, seed)
+    x = synth.hidden(B * S, cfg["hidden"], seed + "_x")
+    return p, x
+
+
+@pytest.mark.parametrize("size,B", [("base", 2), ("large", 1)])
+def test_encoder_layer_teacher_forced(q4, size, B):
+    cfg = synth.BERT[size]
+    S, M, h, f = 128, B * 128, cfg["hidden"], cfg["ffn"]
+    p, x = _layer_setup(cfg, B, S)
+    w = q4.quantize_layer(p)
+    # weight prep (a2) equals the oracle's O-3 bit for bit
+    for k in ("wqkv", "wo", "w1", "w2"):
+        rc, rs = orc.quantize_rows(p[k])
+        assert np.array_equal(host(w[k]), rc) and np.array_equal(host(w["s" + k[1:]]), rs), k
+    xq, xs = q4.quantize_rows(dev(x))
+    out = q4.encoder_layer(cfg, w, B, S, dev(x), xq, xs, taps=True)
+    T = {k: host(v) for k, v in out.items()}
+    W = {k: host(v) for k, v in w.items()}
+    xq_, xs_ = host(xq), host(xs)
+    # QKV: acc bit-exact, fp16 within tolerance
+    assert np.array_equal(T["acc_qkv"], orc.gemm_i32(xq_, W["wqkv"], M, 3 * h, h))
+    rq = orc.w4a4_linear(xq_, xs_, W["wqkv"], W["sqkv"], M, 3 * h, h, orc.EPI_F16, bias=p["bqkv"])
+    assert_f16_close(T["qkv"], rq["f16"], "qkv")
+    # attention on the GPU's qkv
+    rctx, _, _ = orc.attention(T["qkv"], B, S, cfg["heads"], 64)
+    assert_f16_close(T["ctx"], rctx, "ctx")
+    c2, s2 = orc.quantize_rows(T["ctx"])
+    assert np.array_equal(T["ctx_codes"], c2) and np.array_equal(T["ctx_scales"], s2)
+    # attn-out + residual + LN1 on the GPU's ctx codes
+    assert np.array_equal(T["acc_o"], orc.gemm_i32(T["ctx_codes"], W["wo"], M, h, h))
+    r1 = orc.w4a4_linear(T["ctx_codes"], T["ctx_scales"], W["wo"], W["so"], M, h, h, orc.EPI_RESLN_Q4,
+                         bias=p["bo"], residual=x, gamma=p["ln1_g"], beta=p["ln1_b"])
+    assert_f16_close(T["h1"], r1["f16"], "h1")
+    c2, s2 = orc.quantize_rows(T["h1"])
+    assert np.array_equal(T["h1_codes"], c2) and np.array_equal(T["h1_scales"], s2)
+    # FFN1 GELU on the GPU's h1 codes
+    assert np.array_equal(T["acc_1"], orc.gemm_i32(T["h1_codes"], W["w1"], M, f, h))
+    r2 = orc.w4a4_linear(T["h1_codes"], T["h1_scales"], W["w1"], W["s1"], M, f, h, orc.EPI_GELU_Q4, bias=p["b1"])
+    assert_f16_close(T["ffn1"], r2["f16"], "ffn1")
+    c2, s2 = orc.quantize_rows(T["ffn1"])
+    assert np.array_equal(T["f_codes"], c2) and np.array_equal(T["f_scales"], s2)
+    # FFN2 + residual + LN2
+    assert np.array_equal(T["acc_2"], orc.gemm_i32(T["f_codes"], W["w2"], M, h, f))
+    r3 = orc.w4a4_linear(T["f_codes"], T["f_scales"], W["w2"], W["s2"], M, h, f, orc.EPI_RESLN_Q4,
+                         bias=p["b2"], residual=T["h1"], gamma=p["ln2_g"], beta=p["ln2_b"])
+    assert_f16_close(T["h_out"], r3["f16"], "h_out")
+    c2, s2 = orc.quantize_rows(T["h_out"])
+    assert np.array_equal(T["hq_out"], c2) and np.array_equal(T["hs_out"], s2)
+
+
+def test_encoder_stack_host_device_graph(q4):
+    """q4_encoder_stack: device path, host (pinned) end-to-end path and CUDA-graph replay
+    agree bit for bit; layer-by-layer it equals repeated q4_encoder_layer."""
+    cfg = dict(synth.BERT["base"])
+    L, B, S = 3, 2, 128
+    layers = [synth.layer_params(cfg, l, "stk") for l in range(L)]
+    enc = q4.W4A4Encoder(cfg, layers)
+    x = synth.hidden(B * S, cfg["hidden"], "stk_x")
+    xd = dev(x)
+    out_d = torch.empty_like(xd)
+    enc.forward(xd, out_d, B, S)
+    xh = torch.from_numpy(x).pin_memory()
+    out_h = torch.empty(xh.shape, dtype=torch.float16).pin_memory()
+    enc.forward(xh, out_h, B, S)
+    torch.cuda.synchronize()
+    assert torch.equal(out_h, out_d.cpu())
+    out_g = torch.empty_like(xd)
+    enc.capture(xd, out_g, B, S)
+    out_g.zero_()
+    enc.replay()
+    assert torch.equal(out_g, out_d)
+    # reference: explicit per-layer calls
+    hq, hs = q4.quantize_rows(xd)
+    h = xd
+    for l in range(L):
+        o = q4.encoder_layer(cfg, enc.weights[l], B, S, h, hq, hs)
+        h, hq, hs = o["h_out"], o["hq_out"], o["hs_out"]
+    assert torch.equal(h, out_d)
+
+
+def test_full_size_layer_sampled(q4):
+    """BERT-large layer at the bench's launch configuration (M = 256 x 128 = 32768):
+    sampled sequences checked teacher-forced against the oracle (rows of a GEMM and
+    sequences of attention are independent, so a sample is an exact sub-problem)."""
+    cfg = synth.BERT["large"]
+    B, S = 256, 128
+    M, h, f = B * S, cfg["hidden"], cfg["ffn"]
+    p = synth.layer_params(cfg, 0, "full")
+    x = synth.hidden(M, h, "full_x")
+    w = q4.quantize_layer(p)
+    xq, xs = q4.quantize_rows(dev(x))
+    out = q4.encoder_layer(cfg, w, B, S, dev(x), xq, xs, taps=True)
+    torch.cuda.synchronize()
+    W = {k: host(v) for k, v in w.items()}
+    for bsel in (0, 137, 255):
+        rows = slice(bsel * S, (bsel + 1) * S)
+        T = {k: host(v[rows]) for k, v in out.items()}
+        xq_, xs_ = host(xq[rows]), host(xs[rows])
+        assert np.array_equal(T["acc_qkv"], orc.gemm_i32(xq_, W["wqkv"], S, 3 * h, h))
+        rq = orc.w4a4_linear(xq_, xs_, W["wqkv"], W["sqkv"], S, 3 * h, h, orc.EPI_F16, bias=p["bqkv"])
+        assert_f16_close(T["qkv"], rq["f16"], "qkv")
+        rctx, _, _ = orc.attention(T["qkv"], 1, S, cfg["heads"], 64)
+        assert_f16_close(T["ctx"], rctx, "ctx")
+        assert np.array_equal(T["acc_o"], orc.gemm_i32(T["ctx_codes"], W["wo"], S, h, h))
+        assert np.array_equal(T["acc_1"], orc.gemm_i32(T["h1_codes"], W["w1"], S, f, h))
+        assert np.array_equal(T["acc_2"], orc.gemm_i32(T["f_codes"], W["w2"], S, h, f))
+        r3 = orc.w4a4_linear(T["f_codes"], T["f_scales"], W["w2"], W["s2"], S, h, f, orc.EPI_RESLN_Q4,
+                             bias=p["b2"], residual=T["h1"], gamma=p["ln2_g"], beta=p["ln2_b"])
+        assert_f16_close(T["h_out"], r3["f16"], "h_out")
+        c2, s2 = orc.quantize_rows(T["h_out"])
+        assert np.array_equal(T["hq_out"], c2) and np.array_equal(T["hs_out"], s2)
+
+
+def test_launch_count_and_errors(q4):
+    n0 = q4.launch_count()
+    q4.quantize_rows(dev(synth.hidden(8, 64, "lc")))
+    assert q4.launch_count() == n0 + 1
+    with pytest.raises(q4.Q4Error, match="multiple of 32"):
+        a = torch.zeros(4, 16, dtype=torch.uint8, device="cuda")
+        w = torch.zeros(48, 16, dtype=torch.uint8, device="cuda")
+        s = torch.ones(64, device="cuda")
+        q4.w4a4_linear(a, s[:4], w, s[:48], q4.EPI_F16)

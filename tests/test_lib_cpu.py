@@ -1,0 +1,72 @@
+"""CPU-side checks of the C-ABI library: it loads without a GPU, exports every symbol
+include/q4.h declares, and validates arguments synchronously (no compute calls)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2301_12017_b200 import build
+    build.build()
+    from paper_2301_12017_b200 import _lib
+    return _lib.lib()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "q4.h")).read()
+    return sorted(set(re.findall(r"^Q4_API\s+[\w\s\*]+?\b(q4_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("q4_quantize_rows", "q4_w4a4_linear", "q4_attention_f16_q4", "q4_encoder_layer",
+              "q4_encoder_stack", "q4_last_error"):
+        assert s in syms
+    from paper_2301_12017_b200 import _lib
+    assert sorted(_lib.EXPORTS) == syms
+
+
+def test_library_exports_every_declared_symbol(L):
+    for s in declared_symbols():
+        assert hasattr(L, s), s
+
+
+def test_version(L):
+    assert b"sm_100a" in L.q4_version()
+
+
+def _dummy(n=64):
+    buf = (C.c_uint8 * (n + 64))()
+    a = C.addressof(buf)
+    return buf, C.c_void_p((a + 63) & ~63)
+
+
+def test_validation_errors_are_synchronous(L):
+    from paper_2301_12017_b200._lib import Epilogue, Q4_EALIGN, Q4_EINVAL, Q4_ESHAPE
+    keep, p = _dummy()
+    # quantize: cols not a multiple of 8
+    assert L.q4_quantize_rows(p, 4, 12, 12, 0.0, p, p, None) == Q4_ESHAPE
+    assert b"multiples of 8" in L.q4_last_error()
+    # quantize: clip not representable in fp16
+    assert L.q4_quantize_rows(p, 4, 16, 16, 0.1, p, p, None) == Q4_EINVAL
+    # quantize: misaligned x
+    assert L.q4_quantize_rows(C.c_void_p(p.value + 2), 4, 16, 16, 0.0, p, p, None) == Q4_EALIGN
+    e = Epilogue(kind=1)
+    assert L.q4_w4a4_linear(p, p, p, p, 4, 48, 64, C.byref(e), None, 0, None) == Q4_ESHAPE
+    assert b"N=48" in L.q4_last_error()
+    assert L.q4_w4a4_linear(p, p, p, p, 4, 64, 48, C.byref(e), None, 0, None) == Q4_ESHAPE
+    assert L.q4_w4a4_linear(p, p, p, p, 4, 64, 16384, C.byref(e), None, 0, None) == Q4_ESHAPE
+    e = Epilogue(kind=9)
+    assert L.q4_w4a4_linear(p, p, p, p, 4, 64, 64, C.byref(e), None, 0, None) == Q4_EINVAL
+    e = Epilogue(kind=3)  # RESLN without residual
+    assert L.q4_w4a4_linear(p, p, p, p, 4, 64, 64, C.byref(e), None, 0, None) == Q4_EINVAL
+    assert b"residual" in L.q4_last_error()
+    assert L.q4_attention_f16_q4(p, 2, 129, 12, 64, None, p, p, None) == Q4_ESHAPE
+    # M = 0 is a no-op that succeeds without touching the device
+    e = Epilogue(kind=1)
+    assert L.q4_w4a4_linear(p, p, p, p, 0, 64, 64, C.byref(e), None, 0, None) == 0
