@@ -131,8 +131,9 @@ Q4_API q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, /
  * per-token quantize of the context fused into the same kernel.
  *   qkv        [B*S, 3*heads*head_dim] fp16 (Q | K | V column blocks, head j at
  *              columns [j*head_dim, (j+1)*head_dim) of each block)
- *   ctx        = softmax(Q K^T / sqrt(head_dim)) V, no mask (R14), fp16
- *   ctx_f16    [B*S, heads*head_dim] optional tap (NULL = not written)
+ *   ctx        = softmax(Q K^T / sqrt(head_dim)) V, no mask (R14), rounded to fp16
+ *   ctx_f16    [B*S, heads*head_dim] fp16 output (required: the kernel streams the
+ *              context through it and re-reads it from L2 for the quantize)
  *   ctx_codes  [B*S, heads*head_dim/2], ctx_scales [B*S]: a1 applied per token over
  *              all heads of the fp16 ctx
  * Requirements: head_dim == 64, 1 <= S <= 128, heads*64 <= 1024. */

@@ -5,10 +5,11 @@
 // the op is HBM-bound (~64 flop/B vs an fp16 ridge of ~340), so it uses the
 // legacy mma.sync m16n8k16 tensor path, FlashAttention-2 style register reuse of P.
 //
-// CTA = 64 queries of one sequence, 4 warps x 16 rows, looping over all heads so
-// that the context row of every head lands in shared memory; the per-token max-abs
-// over all heads is then known and the codes are written directly (the fp16 ctx
-// never round-trips through HBM unless the tap is requested).
+// CTA = 64 queries of one sequence, 4 warps x 16 rows, looping over all heads with a
+// double-buffered cp.async Q/K/V ring (80 KB -> 2 CTAs per SM).  Each warp writes its
+// fp16 context rows (coalesced, via a 2 KB smem slab) and keeps the per-token running
+// max-abs in registers; after the last head it re-reads its own rows from L2 and writes
+// the INT4 codes + scales, so the per-token quantize is fused into the same kernel.
 #include "kernels.h"
 
 namespace q4 {
@@ -53,20 +54,21 @@ struct HeadBuf {
   __half k[SMAX * D];
   __half v[SMAX * D];
 };
+constexpr size_t kSmem = 2 * sizeof(HeadBuf) + 4 * 16 * 128;  // ring + 4 warp slabs (16 rows x 128 B)
 
 }  // namespace
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, 2)
     attention_q4_kernel(const __half* __restrict__ qkv, int S, int heads, __half* __restrict__ ctx_f16,
                         uint8_t* __restrict__ ctx_codes, float* __restrict__ ctx_scales) {
   extern __shared__ __align__(128) uint8_t smem[];
-  HeadBuf* hb = reinterpret_cast<HeadBuf*>(smem);                        // [2]
-  __half* ctx = reinterpret_cast<__half*>(smem + 2 * sizeof(HeadBuf));   // [QB][h]
+  HeadBuf* hb = reinterpret_cast<HeadBuf*>(smem);  // [2]
   const int h = heads * D, ld = 3 * h;
   const int b = blockIdx.y, q0 = blockIdx.x * QB;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const __half* base = qkv + (size_t)b * S * ld;
+  uint8_t* slab = smem + 2 * sizeof(HeadBuf) + warp * 16 * 128;  // this warp's 16 x 64 fp16 tile
 
   auto load_head = [&](int j, HeadBuf* dst) {
     for (int i = tid; i < QB * 8; i += THREADS) {
@@ -181,7 +183,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     const float inv0 = 1.0f / sum0, inv1 = 1.0f / sum1;
-    const int r0 = warp * 16 + g;
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
       const uint32_t h0 = pack_half2(oc[nt][0] * inv0, oc[nt][1] * inv0);
@@ -189,14 +190,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       const float2 f0 = unpack_half2(h0), f1 = unpack_half2(h1);
       am0 = fmaxf(am0, fmaxf(fabsf(f0.x), fabsf(f0.y)));
       am1 = fmaxf(am1, fmaxf(fabsf(f1.x), fabsf(f1.y)));
-      const int col = j * D + nt * 8 + 2 * t;
-      *reinterpret_cast<uint32_t*>(ctx + (size_t)r0 * h + col) = h0;
-      *reinterpret_cast<uint32_t*>(ctx + (size_t)(r0 + 8) * h + col) = h1;
+      // slab rows g / g+8; halves nt*8+2t, +1 sit in 16-byte chunk nt at byte 4t
+      *reinterpret_cast<uint32_t*>(slab + tile_off(g, nt) + 4 * t) = h0;
+      *reinterpret_cast<uint32_t*>(slab + tile_off(g + 8, nt) + 4 * t) = h1;
     }
+    __syncwarp();
+    // coalesced store of the warp's 16 x 64 ctx tile (4 rows x 128 B per instruction)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rr = i * 4 + (lane >> 3), ch = lane & 7;
+      const int tok = q0 + warp * 16 + rr;
+      const uint4 v = *reinterpret_cast<const uint4*>(slab + tile_off(rr, ch));
+      if (tok < S) *reinterpret_cast<uint4*>(ctx_f16 + ((size_t)b * S + tok) * h + j * D + ch * 8) = v;
+    }
+    __syncwarp();
     __syncthreads();  // cur buffer is refilled two heads later
   }
 
-  // per-token max-abs over all heads, then quantize + pack straight from smem
+  // per-token max-abs over all heads, then quantize + pack this warp's rows (L2-resident)
 #pragma unroll
   for (int o = 1; o <= 2; o <<= 1) {
     am0 = fmaxf(am0, __shfl_xor_sync(0xffffffffu, am0, o));
@@ -204,15 +215,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   for (int rr = 0; rr < 16; ++rr) {
     const float a = __shfl_sync(0xffffffffu, (rr & 8) ? am1 : am0, (rr & 7) * 4);
-    const int r = warp * 16 + rr;
-    const int tok = q0 + r;
+    const int tok = q0 + warp * 16 + rr;
     if (tok >= S) continue;
     const size_t grow = (size_t)b * S + tok;
-    const uint4* src = reinterpret_cast<const uint4*>(ctx + (size_t)r * h);
+    const uint4* src = reinterpret_cast<const uint4*>(ctx_f16 + grow * h);
     uint32_t* cw = reinterpret_cast<uint32_t*>(ctx_codes + grow * (h / 2));
     for (int v = lane; v < h / 8; v += 32) {
-      const uint4 x = src[v];
-      if (ctx_f16) reinterpret_cast<uint4*>(ctx_f16 + grow * h)[v] = x;
+      const uint4 x = __ldcg(src + v);
       const uint32_t* u = reinterpret_cast<const uint32_t*>(&x);
       int qv[8];
 #pragma unroll
@@ -230,17 +239,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 cudaError_t launch_attention(const __half* qkv, int B, int S, int heads, __half* ctx_f16,
                              uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s) {
   if (B == 0) return cudaSuccess;
-  const size_t smem = 2 * sizeof(HeadBuf) + (size_t)QB * heads * D * sizeof(__half);
-  static int configured = 0;
-  if (configured < (int)smem) {
-    cudaError_t e = cudaFuncSetAttribute(attention_q4_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(attention_q4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     if (e != cudaSuccess) return e;
-    configured = (int)smem;
+    configured = true;
   }
   const dim3 grid((unsigned)((S + QB - 1) / QB), (unsigned)B);
   note_launch();
-  attention_q4_kernel<<<grid, THREADS, smem, s>>>(qkv, S, heads, ctx_f16, ctx_codes, ctx_scales);
+  attention_q4_kernel<<<grid, THREADS, kSmem, s>>>(qkv, S, heads, ctx_f16, ctx_codes, ctx_scales);
   return cudaGetLastError();
 }
 

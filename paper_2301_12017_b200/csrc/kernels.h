@@ -33,7 +33,10 @@ struct GemmArgs {
 cudaError_t launch_quantize_rows(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
                                  uint8_t* codes, float* scales, cudaStream_t s);
 // Returns cudaErrorNotSupported for shapes the tcgen05 path cannot take (message in *why).
-cudaError_t launch_w4a4_tc(const GemmArgs& g, cudaStream_t s, const char** why);
+// Row epilogues (GELU_Q4 / RESLN_Q4) need `ws` of tc_workspace_bytes(M, N, tc_tile_n(...)).
+cudaError_t launch_w4a4_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why);
+int tc_tile_n(int M, int N, int kind);
+size_t tc_workspace_bytes(int M, int N, int TN);
 cudaError_t launch_w4a4_legacy(const GemmArgs& g, bool s4, cudaStream_t s, const char** why);
 cudaError_t launch_attention(const __half* qkv, int B, int S, int heads, __half* ctx_f16,
                              uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s);

@@ -66,13 +66,16 @@ q4_status q4_quantize_rows(const uint16_t* x, int64_t rows, int64_t cols, int64_
   return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_quantize_rows");
 }
 
-size_t q4_w4a4_linear_workspace(int64_t, int64_t, int64_t, int32_t) { return 0; }
+size_t q4_w4a4_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind) {
+  (void)K;
+  if (kind != Q4_EPI_GELU_Q4 && kind != Q4_EPI_RESLN_Q4) return 0;
+  if (M <= 0 || N <= 0 || M > (1ll << 31) - 1 || N > (1 << 24)) return 0;
+  return q4::tc_workspace_bytes((int)M, (int)N, q4::tc_tile_n((int)M, (int)N, kind));
+}
 
 q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const uint8_t* w_codes,
                          const float* w_scales, int64_t M, int64_t N, int64_t K, const q4_epilogue* epi,
                          void* workspace, size_t ws_bytes, void* stream) {
-  (void)workspace;
-  (void)ws_bytes;
   g_err[0] = 0;
   if (!epi) return fail(Q4_EINVAL, "q4_w4a4_linear: epi is NULL");
   if (M < 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1 << 24))
@@ -85,8 +88,10 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
   if (M == 0) return Q4_OK;
   if (!a_codes || !a_scales || !w_codes || !w_scales)
     return fail(Q4_EINVAL, "q4_w4a4_linear: NULL operand (a_codes/a_scales/w_codes/w_scales)");
-  if (!al16(a_codes) || !al16(w_codes) || !al4(a_scales) || !al4(w_scales))
-    return fail(Q4_EALIGN, "q4_w4a4_linear: codes must be 16-byte aligned, scales 4-byte aligned");
+  if (!al16(a_codes) || !al16(w_codes) || !al4(a_scales) || !al16(w_scales))
+    return fail(Q4_EALIGN, "q4_w4a4_linear: codes and w_scales must be 16-byte aligned, a_scales 4-byte aligned");
+  if ((epi->bias && !al4(epi->bias)) || (epi->gamma && !al4(epi->gamma)) || (epi->beta && !al4(epi->beta)))
+    return fail(Q4_EALIGN, "q4_w4a4_linear: bias/gamma/beta must be 4-byte aligned");
   switch (kind) {
     case Q4_EPI_I32:
       if (!epi->out_i32 || !al16(epi->out_i32)) return fail(Q4_EINVAL, "q4_w4a4_linear(I32): out_i32 NULL or not 16-byte aligned");
@@ -108,6 +113,13 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
       break;
   }
   if (!clip_ok(epi->requant_clip)) return fail(Q4_EINVAL, "q4_w4a4_linear: requant_clip=%g is not 0 or a positive fp16 value", epi->requant_clip);
+  if (kind == Q4_EPI_GELU_Q4 || kind == Q4_EPI_RESLN_Q4) {
+    if (N % 64) return fail(Q4_ESHAPE, "q4_w4a4_linear: N=%lld must be a multiple of 64 for row epilogues", (long long)N);
+    const size_t need = q4_w4a4_linear_workspace(M, N, K, kind);
+    if (!workspace || ws_bytes < need)
+      return fail(Q4_EINVAL, "q4_w4a4_linear: workspace %zu bytes < required %zu (q4_w4a4_linear_workspace)", ws_bytes, need);
+    if (!al16(workspace)) return fail(Q4_EALIGN, "q4_w4a4_linear: workspace must be 16-byte aligned");
+  }
   q4::GemmArgs g;
   g.a_codes = a_codes; g.a_scales = a_scales; g.w_codes = w_codes; g.w_scales = w_scales;
   g.M = (int)M; g.N = (int)N; g.K = (int)K; g.kind = kind; g.mainloop = epi->mainloop;
@@ -122,7 +134,7 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
   cudaError_t e;
   switch (epi->mainloop) {
     case Q4_MAINLOOP_AUTO:
-    case Q4_MAINLOOP_TCGEN05: e = q4::launch_w4a4_tc(g, (cudaStream_t)stream, &why); break;
+    case Q4_MAINLOOP_TCGEN05: e = q4::launch_w4a4_tc(g, workspace, ws_bytes, (cudaStream_t)stream, &why); break;
     case Q4_MAINLOOP_MMA_SYNC_S8: e = q4::launch_w4a4_legacy(g, false, (cudaStream_t)stream, &why); break;
     case Q4_MAINLOOP_MMA_SYNC_S4: e = q4::launch_w4a4_legacy(g, true, (cudaStream_t)stream, &why); break;
     default: return fail(Q4_EINVAL, "q4_w4a4_linear: unknown mainloop %d", epi->mainloop);
@@ -140,8 +152,9 @@ q4_status q4_attention_f16_q4(const uint16_t* qkv, int64_t B, int64_t S, int32_t
   if (heads < 1 || heads * 64 > 1024) return fail(Q4_ESHAPE, "q4_attention_f16_q4: heads=%d (need 1..16)", heads);
   if (B > 65535) return fail(Q4_ESHAPE, "q4_attention_f16_q4: B=%lld > 65535", (long long)B);
   if (B == 0) return Q4_OK;
-  if (!qkv || !ctx_codes || !ctx_scales) return fail(Q4_EINVAL, "q4_attention_f16_q4: NULL qkv/ctx_codes/ctx_scales");
-  if (!al16(qkv) || !al4(ctx_codes) || (ctx_f16 && !al16(ctx_f16)))
+  if (!qkv || !ctx_f16 || !ctx_codes || !ctx_scales)
+    return fail(Q4_EINVAL, "q4_attention_f16_q4: NULL qkv/ctx_f16/ctx_codes/ctx_scales");
+  if (!al16(qkv) || !al4(ctx_codes) || !al16(ctx_f16))
     return fail(Q4_EALIGN, "q4_attention_f16_q4: qkv/ctx_f16 must be 16-byte aligned, codes 4-byte");
   cudaError_t e = q4::launch_attention(reinterpret_cast<const __half*>(qkv), (int)B, (int)S, heads,
                                        reinterpret_cast<__half*>(ctx_f16), ctx_codes, ctx_scales, (cudaStream_t)stream);
@@ -152,7 +165,10 @@ q4_status q4_attention_f16_q4(const uint16_t* qkv, int64_t B, int64_t S, int32_t
 
 namespace {
 struct LayerWs {
+  uint8_t* gemm_ws;
+  size_t gemm_ws_bytes;
   uint16_t* qkv;
+  uint16_t* ctx;
   uint8_t* ctx_codes;
   float* ctx_scales;
   uint16_t* h1;
@@ -167,7 +183,16 @@ LayerWs layer_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base) {
   size_t o = 0;
   const int64_t h = c->hidden, f = c->ffn;
   auto take = [&](size_t n) { size_t r = o; o = align_up(o + n); return base ? base + r : nullptr; };
+  size_t gw = 0;
+  for (int64_t n : {h, f})
+    for (int kind : {Q4_EPI_GELU_Q4, Q4_EPI_RESLN_Q4}) {
+      size_t b = q4_w4a4_linear_workspace(M, n, 0, kind);
+      if (b > gw) gw = b;
+    }
+  w.gemm_ws_bytes = gw;
+  w.gemm_ws = take(gw);
   w.qkv = (uint16_t*)take((size_t)M * 3 * h * 2);
+  w.ctx = (uint16_t*)take((size_t)M * h * 2);
   w.ctx_codes = take((size_t)M * h / 2);
   w.ctx_scales = (float*)take((size_t)M * 4);
   w.h1 = (uint16_t*)take((size_t)M * h * 2);
@@ -221,7 +246,9 @@ q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, i
   float* f_scales = tp.f_scales ? tp.f_scales : ws.f_scales;
 
   auto lin = [&](const uint8_t* ac, const float* as, const uint8_t* wc, const float* wsc, int64_t N, int64_t K,
-                 q4_epilogue e) -> q4_status { return q4_w4a4_linear(ac, as, wc, wsc, M, N, K, &e, nullptr, 0, stream); };
+                 q4_epilogue e) -> q4_status {
+    return q4_w4a4_linear(ac, as, wc, wsc, M, N, K, &e, ws.gemm_ws, ws.gemm_ws_bytes, stream);
+  };
   auto acc_tap = [&](const uint8_t* ac, const float* as, const uint8_t* wc, const float* wsc, int64_t N, int64_t K,
                      int32_t* out) -> q4_status {
     if (!out) return Q4_OK;
@@ -238,7 +265,9 @@ q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, i
   if ((st = lin(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, e))) return st;
   if ((st = acc_tap(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, tp.acc_qkv))) return st;
   // FP16 attention + fused per-token ctx quantize
-  if ((st = q4_attention_f16_q4(qkv, B, S, cfg->heads, cfg->head_dim, tp.ctx, ctx_codes, ctx_scales, stream))) return st;
+  if ((st = q4_attention_f16_q4(qkv, B, S, cfg->heads, cfg->head_dim, tp.ctx ? tp.ctx : ws.ctx, ctx_codes,
+                                ctx_scales, stream)))
+    return st;
   // attention output: dequant + bias + residual(h_in) + LN1 + requant
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_RESLN_Q4; e.bias = w->bo; e.residual = h_in; e.gamma = w->ln1_g; e.beta = w->ln1_b;

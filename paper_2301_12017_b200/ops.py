@@ -48,7 +48,7 @@ def quantize_rows(x: torch.Tensor, clip: float = 0.0, codes=None, scales=None):
 
 def w4a4_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None, residual=None,
                 gamma=None, beta=None, ln_eps=1e-12, clip=0.0, mainloop=0, f16_tap=False,
-                out=None):
+                out=None, workspace=None):
     """a3-a6: INT4 x INT4 -> exact INT32 -> fused epilogue.  Returns a dict with the
     outputs of the epilogue kind: i32 | f16 | (codes, scales[, f16])."""
     _need(a_codes, torch.uint8, "a_codes", 2)
@@ -74,8 +74,12 @@ def w4a4_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None
                  gamma=_ptr(gamma), beta=_ptr(beta), ln_eps=ln_eps, requant_clip=clip,
                  out_i32=_ptr(o.get("i32")), out_f16=_ptr(o.get("f16")),
                  out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")))
+    ws_bytes = lib().q4_w4a4_linear_workspace(M, N, K, kind)
+    if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
+        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     check(lib().q4_w4a4_linear(_ptr(a_codes), _ptr(a_scales), _ptr(w_codes), _ptr(w_scales),
-                               M, N, K, C.byref(e), None, 0, _stream()))
+                               M, N, K, C.byref(e), _ptr(workspace),
+                               0 if workspace is None else workspace.numel(), _stream()))
     return o
 
 
@@ -86,7 +90,7 @@ def attention_f16_q4(qkv, B, S, heads, head_dim=64, f16_tap=False):
     dev = qkv.device
     codes = torch.empty(B * S, h // 2, dtype=torch.uint8, device=dev)
     scales = torch.empty(B * S, dtype=torch.float32, device=dev)
-    ctx = torch.empty(B * S, h, dtype=torch.float16, device=dev) if f16_tap else None
+    ctx = torch.empty(B * S, h, dtype=torch.float16, device=dev)
     check(lib().q4_attention_f16_q4(_ptr(qkv), B, S, heads, head_dim, _ptr(ctx), _ptr(codes),
                                     _ptr(scales), _stream()))
     return (codes, scales, ctx) if f16_tap else (codes, scales)

@@ -66,7 +66,8 @@ def test_validation_errors_are_synchronous(L):
     e = Epilogue(kind=3)  # RESLN without residual
     assert L.q4_w4a4_linear(p, p, p, p, 4, 64, 64, C.byref(e), None, 0, None) == Q4_EINVAL
     assert b"residual" in L.q4_last_error()
-    assert L.q4_attention_f16_q4(p, 2, 129, 12, 64, None, p, p, None) == Q4_ESHAPE
+    assert L.q4_attention_f16_q4(p, 2, 129, 12, 64, p, p, p, None) == Q4_ESHAPE
+    assert L.q4_attention_f16_q4(p, 2, 128, 12, 64, None, p, p, None) == Q4_EINVAL  # ctx_f16 required
     # M = 0 is a no-op that succeeds without touching the device
     e = Epilogue(kind=1)
     assert L.q4_w4a4_linear(p, p, p, p, 0, 64, 64, C.byref(e), None, 0, None) == 0
