@@ -299,16 +299,16 @@ def main():
       hcur = xd
       for l in range(L):
         w = w0[l]
-        qkv = timed("qkv_gemm_f16", lambda: q4.w4a4_linear(hq, hs, w["wqkv"], w["sqkv"], q4.EPI_F16, bias=w["bqkv"]),
+        qkv = timed("qkv_gemm_f16", lambda: q4.w4a4_linear(hq, hs, w["wqkv"], w["sqkv"], q4.EPI_F16, bias=w["bqkv"], w_i8=w.get("wqkv8")),
                     gemm_work(M, 3 * h, h, "f16"))["f16"]
         cq, cs = timed("attention_q4", lambda: q4.attention_f16_q4(qkv, B, S, cfg["heads"]),
                        attention_work(B, S, cfg["heads"]))
         o1 = timed("attn_out_gemm_resln_q4", lambda: q4.w4a4_linear(cq, cs, w["wo"], w["so"], q4.EPI_RESLN_Q4, bias=w["bo"],
-                   residual=hcur, gamma=w["ln1_g"], beta=w["ln1_b"]), gemm_work(M, h, h, "resln_q4"))
+                   residual=hcur, gamma=w["ln1_g"], beta=w["ln1_b"], w_i8=w.get("wo8")), gemm_work(M, h, h, "resln_q4"))
         o2 = timed("ffn1_gemm_gelu_q4", lambda: q4.w4a4_linear(o1["codes"], o1["scales"], w["w1"], w["s1"], q4.EPI_GELU_Q4,
-                   bias=w["b1"]), gemm_work(M, f, h, "gelu_q4"))
+                   bias=w["b1"], w_i8=w.get("w18")), gemm_work(M, f, h, "gelu_q4"))
         o3 = timed("ffn2_gemm_resln_q4", lambda: q4.w4a4_linear(o2["codes"], o2["scales"], w["w2"], w["s2"], q4.EPI_RESLN_Q4,
-                   bias=w["b2"], residual=o1["f16"], gamma=w["ln2_g"], beta=w["ln2_b"]), gemm_work(M, h, f, "resln_q4"))
+                   bias=w["b2"], residual=o1["f16"], gamma=w["ln2_g"], beta=w["ln2_b"], w_i8=w.get("w28")), gemm_work(M, h, f, "resln_q4"))
         hcur, hq, hs = o3["f16"], o3["codes"], o3["scales"]
       torch.cuda.synchronize()
     torch.cuda.synchronize()

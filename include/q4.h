@@ -97,9 +97,12 @@ typedef enum { Q4_EPI_I32 = 0, Q4_EPI_F16 = 1, Q4_EPI_GELU_Q4 = 2, Q4_EPI_RESLN_
  *   TCGEN05     TMA -> smem nibble->int8 unpack -> tcgen05.mma kind::i8 -> TMEM
  *   MMA_SYNC_S8 legacy: cp.async -> ldmatrix -> register unpack -> mma.sync s8
  *   MMA_SYNC_S4 legacy: cp.async -> ldmatrix -> mma.sync m16n8k64 .s4 (emulated on sm_100a)
+ *   TCGEN05_W8  as TCGEN05, but the weights come prepacked (epi->w_i8, q4_prepack_weights):
+ *               TMA'd straight into the swizzled operand stage; only A is unpacked on chip
+ * AUTO uses TCGEN05_W8 when epi->w_i8 is given and M > 256, else TCGEN05.
  * The legacy variants implement Q4_EPI_I32 and Q4_EPI_F16 only. */
 typedef enum { Q4_MAINLOOP_AUTO = 0, Q4_MAINLOOP_TCGEN05 = 1, Q4_MAINLOOP_MMA_SYNC_S8 = 2,
-               Q4_MAINLOOP_MMA_SYNC_S4 = 3 } q4_mainloop;
+               Q4_MAINLOOP_MMA_SYNC_S4 = 3, Q4_MAINLOOP_TCGEN05_W8 = 4 } q4_mainloop;
 
 typedef struct {
   int32_t kind;              /* q4_epi_kind                                              */
@@ -114,6 +117,8 @@ typedef struct {
   uint16_t* out_f16;         /* [M, N]   F16, RESLN (required); GELU_Q4 optional tap      */
   uint8_t* out_codes;        /* [M, N/2] *_Q4                                            */
   float* out_scales;         /* [M]      *_Q4                                            */
+  const int8_t* w_i8;        /* optional [N, K] prepacked weights (q4_prepack_weights) of the
+                                same codes as w_codes; NULL = unpack w_codes on chip       */
 } q4_epilogue;
 
 /* Requirements: M >= 0; N % 32 == 0; K % 32 == 0; K <= 8192 (the INT32 accumulator
@@ -124,6 +129,16 @@ Q4_API q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, /
                          const uint8_t* w_codes, const float* w_scales, /* [N,K/2], [N] */
                          int64_t M, int64_t N, int64_t K, const q4_epilogue* epi,
                          void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * a2' Offline weight prepack (once per weight, not on the forward path): packed INT4 codes
+ * w_codes [N, K/2] -> w_i8 [N, K] int8 holding 16*q in the K order of the on-chip
+ * activation unpack (per 32-element group: the 16 even-k values, then the 16 odd-k).
+ * The weights stay INT4-valued; only their on-device layout is
+ * MMA-ready, trading 2x weight bytes for 3x less on-chip unpack work.
+ * Requirements: K % 32 == 0, pointers 16-byte aligned. */
+Q4_API q4_status q4_prepack_weights(const uint8_t* w_codes, int64_t N, int64_t K, int8_t* w_i8,
+                                    void* stream);
 
 /* ---------------------------------------------------------------------------------
  * a7  FP16 attention between the quantized GEMMs (the
@@ -158,6 +173,7 @@ typedef struct {
 } q4_layer_cfg;
 typedef struct {
   const uint8_t *wqkv, *wo, *w1, *w2;   /* packed [3h,h/2], [h,h/2], [ffn,h/2], [h,ffn/2] */
+  const int8_t *wqkv8, *wo8, *w18, *w28; /* optional prepacked copies (q4_prepack_weights)  */
   const float *sqkv, *so, *s1, *s2;     /* per-output-channel scales                       */
   const uint16_t *bqkv, *bo, *b1, *b2;  /* fp16 biases                                      */
   const uint16_t *ln1_g, *ln1_b, *ln2_g, *ln2_b;

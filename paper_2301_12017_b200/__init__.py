@@ -6,15 +6,16 @@ The product is the C-ABI library libq4.so (include/q4.h, csrc/); this package is
 thin Python binding.  PyTorch provides device memory, streams, CUDA graphs and
 torch.distributed -- plumbing, not the product.  There is no CPU fallback."""
 from ._lib import (EPI_F16, EPI_GELU_Q4, EPI_I32, EPI_RESLN_Q4, MAINLOOP_AUTO,
-                   MAINLOOP_MMA_SYNC_S4, MAINLOOP_MMA_SYNC_S8, MAINLOOP_TCGEN05, Q4Error,
+                   MAINLOOP_MMA_SYNC_S4, MAINLOOP_MMA_SYNC_S8, MAINLOOP_TCGEN05, MAINLOOP_TCGEN05_W8,
+                   Q4Error,
                    launch_count, lib, version)
-from .ops import (attention_f16_q4, encoder_layer, quantize_layer, quantize_rows,
+from .ops import (attention_f16_q4, encoder_layer, prepack_weights, quantize_layer, quantize_rows,
                   w4a4_linear)
 from .encoder import W4A4Encoder
 
 __all__ = [
     "EPI_I32", "EPI_F16", "EPI_GELU_Q4", "EPI_RESLN_Q4", "MAINLOOP_AUTO", "MAINLOOP_TCGEN05",
-    "MAINLOOP_MMA_SYNC_S8", "MAINLOOP_MMA_SYNC_S4", "Q4Error", "lib", "version", "launch_count",
+    "MAINLOOP_MMA_SYNC_S8", "MAINLOOP_MMA_SYNC_S4", "MAINLOOP_TCGEN05_W8", "prepack_weights", "Q4Error", "lib", "version", "launch_count",
     "quantize_rows", "w4a4_linear", "attention_f16_q4", "encoder_layer", "quantize_layer",
     "W4A4Encoder",
 ]

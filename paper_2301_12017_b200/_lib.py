@@ -12,11 +12,11 @@ LIB_PATH = os.path.join(HERE, "libq4.so")
 
 Q4_OK, Q4_EINVAL, Q4_ESHAPE, Q4_EALIGN, Q4_EUNSUPPORTED, Q4_ECUDA = range(6)
 EPI_I32, EPI_F16, EPI_GELU_Q4, EPI_RESLN_Q4 = range(4)
-MAINLOOP_AUTO, MAINLOOP_TCGEN05, MAINLOOP_MMA_SYNC_S8, MAINLOOP_MMA_SYNC_S4 = range(4)
+MAINLOOP_AUTO, MAINLOOP_TCGEN05, MAINLOOP_MMA_SYNC_S8, MAINLOOP_MMA_SYNC_S4, MAINLOOP_TCGEN05_W8 = range(5)
 STATUS_NAMES = ["Q4_OK", "Q4_EINVAL", "Q4_ESHAPE", "Q4_EALIGN", "Q4_EUNSUPPORTED", "Q4_ECUDA"]
 
 EXPORTS = (
-    "q4_last_error", "q4_version", "q4_launch_count", "q4_quantize_rows",
+    "q4_last_error", "q4_version", "q4_launch_count", "q4_quantize_rows", "q4_prepack_weights",
     "q4_w4a4_linear_workspace", "q4_w4a4_linear", "q4_attention_f16_q4",
     "q4_encoder_layer_workspace", "q4_encoder_layer", "q4_encoder_stack_workspace",
     "q4_encoder_stack",
@@ -35,7 +35,7 @@ class Epilogue(C.Structure):
         ("bias", C.c_void_p), ("residual", C.c_void_p), ("gamma", C.c_void_p), ("beta", C.c_void_p),
         ("ln_eps", C.c_float), ("requant_clip", C.c_float),
         ("out_i32", C.c_void_p), ("out_f16", C.c_void_p), ("out_codes", C.c_void_p),
-        ("out_scales", C.c_void_p),
+        ("out_scales", C.c_void_p), ("w_i8", C.c_void_p),
     ]
 
 
@@ -44,8 +44,8 @@ class LayerCfg(C.Structure):
                 ("ffn", C.c_int32), ("ln_eps", C.c_float)]
 
 
-WEIGHT_FIELDS = ("wqkv", "wo", "w1", "w2", "sqkv", "so", "s1", "s2", "bqkv", "bo", "b1", "b2",
-                 "ln1_g", "ln1_b", "ln2_g", "ln2_b")
+WEIGHT_FIELDS = ("wqkv", "wo", "w1", "w2", "wqkv8", "wo8", "w18", "w28", "sqkv", "so", "s1", "s2",
+                 "bqkv", "bo", "b1", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")
 TAP_FIELDS = ("qkv", "ctx", "h1", "ffn1", "acc_qkv", "acc_o", "acc_1", "acc_2", "ctx_codes",
               "h1_codes", "f_codes", "ctx_scales", "h1_scales", "f_scales")
 
@@ -74,6 +74,7 @@ def lib():
         L.q4_version.restype = C.c_char_p
         L.q4_launch_count.restype = C.c_uint64
         L.q4_quantize_rows.argtypes = [P, I64, I64, I64, F, P, P, P]
+        L.q4_prepack_weights.argtypes = [P, I64, I64, P, P]
         L.q4_w4a4_linear_workspace.argtypes = [I64, I64, I64, I32]
         L.q4_w4a4_linear_workspace.restype = SZ
         L.q4_w4a4_linear.argtypes = [P, P, P, P, I64, I64, I64, C.POINTER(Epilogue), P, SZ, P]

@@ -217,21 +217,20 @@ __global__ void __launch_bounds__(THREADS, 2)
     const float a = __shfl_sync(0xffffffffu, (rr & 8) ? am1 : am0, (rr & 7) * 4);
     const int tok = q0 + warp * 16 + rr;
     if (tok >= S) continue;
+    const float r7 = a > 0.f ? __fdiv_rn(7.0f, a) : 0.f;
     const size_t grow = (size_t)b * S + tok;
     const uint4* src = reinterpret_cast<const uint4*>(ctx_f16 + grow * h);
     uint32_t* cw = reinterpret_cast<uint32_t*>(ctx_codes + grow * (h / 2));
-    for (int v = lane; v < h / 8; v += 32) {
-      const uint4 x = __ldcg(src + v);
-      const uint32_t* u = reinterpret_cast<const uint32_t*>(&x);
-      int qv[8];
+    uint4 x[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = unpack_half2(u[i]);
-        qv[2 * i] = a > 0.f ? q4_code(f.x, a) : 0;
-        qv[2 * i + 1] = a > 0.f ? q4_code(f.y, a) : 0;
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < h / 8) x[i] = __ldcg(src + lane + 32 * i);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < h / 8) {
+        const uint32_t hh[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
+        cw[lane + 32 * i] = requant8(hh, a, r7, 0.f);
       }
-      cw[v] = pack8(qv);
-    }
     if (lane == 0) ctx_scales[grow] = a > 0.f ? __fdiv_rn(a, 7.0f) : 1.0f;
   }
 }

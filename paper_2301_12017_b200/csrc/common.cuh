@@ -24,14 +24,16 @@ Q4_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the phase completes
+// (or the hint expires) instead of spinning and stealing issue slots from working warps.
 Q4_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(addr), "r"(parity)
+      : "r"(addr), "r"(parity), "r"(0x989680u)
       : "memory");
   return ok != 0;
 }
@@ -186,6 +188,64 @@ Q4_DEV float2 unpack_half2(uint32_t u) {
 // Exact symmetric INT4 code of fp16 value y (as float) given row amax a > 0:
 // rint(div.rn(7y, a)) == round-half-even of the exact rational 7y/a for all fp16 pairs.
 Q4_DEV int q4_code(float y, float a) { return __float2int_rn(__fdiv_rn(7.0f * y, a)); }
+
+// The same code, fast: with r7 = RN(7/a), p = y*r7 is within 1e-6 of 7y/a (|y| <= a), so
+// p's nearest integer is the answer unless p is within 2e-6 of a half-integer; there the
+// side is decided exactly by the sign of t - a*h (t = 7y, h = that half-integer; both are
+// short fp16 x small-integer products, so the FMA result is exact).  Half-even ties.
+Q4_DEV int requant_code(float y, float a, float r7) {
+  const float p = y * r7;
+  const float s = p + 12582912.0f;  // 1.5 * 2^23: rounds p to an integer, half to even
+  const float fn = s - 12582912.0f;
+  int n = __float_as_int(s) - 0x4B400000;
+  const float d0 = p - fn;
+  if (fabsf(d0) > 0.499998f) {
+    const float h = fn + copysignf(0.5f, d0);
+    const float e = fmaf(-a, h, 7.0f * y);
+    const int lo = (int)floorf(h), hi = lo + 1;
+    n = e > 0.f ? hi : (e < 0.f ? lo : ((lo & 1) ? hi : lo));
+  }
+  return n;
+}
+// Two INT4 codes -> low byte, previous word shifted left by 8 (I2IP, saturating).
+Q4_DEV uint32_t cvt_pack_s4(int hi, int lo, uint32_t prev) {
+  uint32_t d;
+  asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(hi), "r"(lo), "r"(prev));
+  return d;
+}
+// 8 fp16 values (4 packed words) -> 8 codes packed in one word (element i at bits 4i).
+// amax <= 0 gives all-zero codes (R5).  y is clamped to [-clip, clip] when clip > 0.
+Q4_DEV uint32_t requant8(const uint32_t (&h)[4], float amax, float r7, float clip) {
+  if (!(amax > 0.f)) return 0u;
+  float y[8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[j]));
+    y[2 * j] = f.x;
+    y[2 * j + 1] = f.y;
+  }
+  if (clip > 0.f) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) y[j] = fminf(fmaxf(y[j], -clip), clip);
+  }
+  int q[8];
+  float dmax = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float p = y[j] * r7;
+    const float sm = p + 12582912.0f;
+    dmax = fmaxf(dmax, fabsf(p - (sm - 12582912.0f)));
+    q[j] = __float_as_int(sm) - 0x4B400000;
+  }
+  if (dmax > 0.499998f) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) q[j] = requant_code(y[j], amax, r7);
+  }
+  uint32_t w = cvt_pack_s4(q[7], q[6], 0u);
+  w = cvt_pack_s4(q[5], q[4], w);
+  w = cvt_pack_s4(q[3], q[2], w);
+  return cvt_pack_s4(q[1], q[0], w);
+}
 // Pack 8 codes (each in [-8,7]) into a 32-bit word, element i in bits [4i, 4i+4).
 Q4_DEV uint32_t pack8(const int (&q)[8]) {
   uint32_t w = 0;

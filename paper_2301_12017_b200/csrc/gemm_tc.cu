@@ -22,6 +22,7 @@
 // step and exchange per-row partials (max-abs; shifted LayerNorm moments combined with
 // Chan's formula in rank order) through L2 with a per-m-block arrival counter.  The
 // grid is sized so all CTAs are co-resident (persistent, <= 1 CTA per SM).
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -49,23 +50,27 @@ struct TcParams {
   float2* xstat;      // [mblocks][ntn][128] (mean, M2) partials
   float* xamax;       // [mblocks][ntn][128] max-abs partials
   unsigned* xcnt;     // [2][mblocks] arrival counters (zeroed before launch)
+  int dbg;            // profiling only (env Q4_DEBUG_SKIP): 1 skip TMA, 2 skip unpack, 4 skip MMA, 8 skip epilogue math
 };
 
 constexpr int kThreads = 448;
 constexpr int kEpiWarp0 = 6;
 
-template <int TN>
+// BI8: B (weights) arrives prepacked as int8 "16*q" in the MMA's K order
+// (q4_prepack_weights) and is TMA'd straight into the swizzled operand stage; only the
+// activation operand A is unpacked on chip.
+template <int TN, bool BI8>
 struct TcCfg {
   static constexpr int BM = 128, BK = 128;  // BK in int8 elements = 64 packed bytes
-  static constexpr int SP = 3, SU = 2;      // packed / unpacked smem stages
-  static constexpr int A_PK = BM * 64, B_PK = TN * 64;
+  static constexpr int SP = BI8 ? 4 : 3, SU = BI8 ? 3 : 2;  // packed / unpacked smem stages
+  static constexpr int A_PK = BM * 64, B_PK = BI8 ? 0 : TN * 64;
   static constexpr int A_UN = BM * 128, B_UN = TN * 128;
   static constexpr int UN_STAGE = A_UN + B_UN, PK_STAGE = A_PK + B_PK;
   static constexpr int OFF_UN = 0;
   static constexpr int OFF_PK = SU * UN_STAGE;
   static constexpr int OFF_STG = OFF_PK + SP * PK_STAGE;  // 8 warps x 4 KB staging slabs
-  static constexpr int OFF_ROW = OFF_STG + 8 * 4096;      // [2][128] float4 row partials
-  static constexpr int OFF_BAR = OFF_ROW + 2 * 128 * 16;
+  static constexpr int OFF_PRM = OFF_STG + 8 * 4096;      // [4][TN] fp32 column params
+  static constexpr int OFF_BAR = OFF_PRM + 4 * TN * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int HW = TN / 2;  // columns per epilogue group
   static constexpr int TMEM_COLS = 2 * TN <= 64 ? 64 : 2 * TN <= 128 ? 128 : 2 * TN <= 256 ? 256 : 512;
@@ -75,29 +80,19 @@ struct TcCfg {
 
 // ------------------------------------------------------------------ tile iteration
 struct TileIter {
-  int cur, step, ntn, mblocks, rank;
-  bool row;
-  __device__ TileIter(const TcParams& p, bool row_) : ntn(p.ntn), mblocks(p.mblocks), row(row_) {
-    if (row) {
-      rank = blockIdx.x % p.ntn;
-      cur = blockIdx.x / p.ntn;
-      step = p.groups;
-    } else {
-      rank = 0;
-      cur = blockIdx.x;
-      step = gridDim.x;
-    }
+  // The grid is `groups` x `ntn` CTAs; CTA (g, rank) owns n-block `rank` for the whole
+  // kernel and walks m-blocks g, g + groups, ...  (fixed N-tile: column parameters are
+  // staged once; row epilogues find the ntn CTAs of an m-block at the same step).
+  int cur, step, mblocks, rank;
+  __device__ TileIter(const TcParams& p) : mblocks(p.mblocks) {
+    rank = blockIdx.x % p.ntn;
+    cur = blockIdx.x / p.ntn;
+    step = p.groups;
   }
   __device__ bool next(int& mb, int& nb) {
-    if (row) {
-      if (cur >= mblocks) return false;
-      mb = cur;
-      nb = rank;
-    } else {
-      if (cur >= mblocks * ntn) return false;
-      mb = cur / ntn;
-      nb = cur % ntn;
-    }
+    if (cur >= mblocks) return false;
+    mb = cur;
+    nb = rank;
     cur += step;
     return true;
   }
@@ -120,47 +115,32 @@ Q4_DEV void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
                "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                : "memory");
 }
-// Two INT4 codes -> low byte, previous word shifted left by 8 (I2IP, saturating).
-Q4_DEV uint32_t cvt_pack_s4(int hi, int lo, uint32_t prev) {
-  uint32_t d;
-  asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(hi), "r"(lo), "r"(prev));
-  return d;
-}
-
-// Exact symmetric INT4 code of y given the row's (clipped) max-abs a > 0 and r7 = RN(7/a):
-// round-half-even of the rational 7y/a (== rint(div.rn(7y, a)), R3).  The fast
-// estimate p = y*r7 is within 1e-6 of 7y/a; only when p is that close to a half-integer is
-// the side decided exactly by t - a*h with t = 7y, h = the half-integer (exact in fp32 there).
-Q4_DEV int requant_code(float y, float a, float r7) {
-  const float p = y * r7;
-  const float big = 12582912.0f;  // 1.5 * 2^23: (p + big) rounds p to an integer, half-even
-  const float s = p + big;
-  float fn = s - big;
-  int n = __float_as_int(s) - 0x4B400000;
-  const float d0 = p - fn;
-  if (fabsf(d0) > 0.499998f) {
-    const float h = fn + copysignf(0.5f, d0);
-    const float e = fmaf(-a, h, 7.0f * y);  // exact: t - a*h
-    const int lo = (int)floorf(h), hi = lo + 1;
-    n = e > 0.f ? hi : (e < 0.f ? lo : ((lo & 1) ? hi : lo));
-  }
-  return n;
-}
-
-template <int BK>
-Q4_DEV void unpack_tile(const uint8_t* __restrict__ pk, uint8_t* __restrict__ un, int rows, int t) {
-  constexpr int CPR = BK / 32;  // 16-byte packed chunks per row
-  const int n = rows * CPR;
-#pragma unroll 4
-  for (int i = t; i < n; i += 128) {
-    const uint32_t r = (uint32_t)i / CPR, c = (uint32_t)i % CPR;
-    const uint4 w = *reinterpret_cast<const uint4*>(pk + (size_t)i * 16);
-    uint4 lo, hi;
-    lo.x = nib_lo16(w.x); lo.y = nib_lo16(w.y); lo.z = nib_lo16(w.z); lo.w = nib_lo16(w.w);
-    hi.x = nib_hi16(w.x); hi.y = nib_hi16(w.y); hi.z = nib_hi16(w.z); hi.w = nib_hi16(w.w);
-    uint8_t* row = un + (size_t)r * BK;
-    *reinterpret_cast<uint4*>(row + (((2 * c) ^ (r & 7u)) << 4)) = lo;
-    *reinterpret_cast<uint4*>(row + (((2 * c + 1) ^ (r & 7u)) << 4)) = hi;
+// Unpack `ROWS` rows of one k-block (64 packed bytes -> 128 int8 per row) with 128
+// threads.  Chunk i (16 packed bytes = 32 nibbles of row i/4) -> two 16-byte int8 chunks
+// (even k, odd k) at swizzled positions.  All loads of a batch are issued before any
+// transform/store so each thread keeps NB shared-memory loads in flight.
+template <int ROWS>
+Q4_DEV void unpack_rows(const uint8_t* __restrict__ pk, uint8_t* __restrict__ un, int t) {
+  constexpr int NCH = ROWS * 4;                   // 16-byte packed chunks
+  constexpr int PER = NCH / 128;                  // chunks per thread
+  constexpr int NB = PER < 8 ? PER : 8;           // batch
+  static_assert(NCH % 128 == 0, "rows");
+#pragma unroll
+  for (int b0 = 0; b0 < PER; b0 += NB) {
+    uint4 w[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) w[j] = *reinterpret_cast<const uint4*>(pk + (size_t)(t + 128 * (b0 + j)) * 16);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const uint32_t i = (uint32_t)(t + 128 * (b0 + j));
+      const uint32_t r = i >> 2, c = i & 3u;
+      uint4 lo, hi;
+      lo.x = nib_lo16(w[j].x); lo.y = nib_lo16(w[j].y); lo.z = nib_lo16(w[j].z); lo.w = nib_lo16(w[j].w);
+      hi.x = nib_hi16(w[j].x); hi.y = nib_hi16(w[j].y); hi.z = nib_hi16(w[j].z); hi.w = nib_hi16(w[j].w);
+      uint8_t* row = un + (size_t)r * 128;
+      *reinterpret_cast<uint4*>(row + (((2 * c) ^ (r & 7u)) << 4)) = lo;
+      *reinterpret_cast<uint4*>(row + (((2 * c + 1) ^ (r & 7u)) << 4)) = hi;
+    }
   }
 }
 
@@ -232,6 +212,28 @@ Q4_DEV void requant16(const uint32_t (&h)[8], float amax, float r7, float clip, 
   }
 }
 
+// 32 accumulators (raw = 256*acc) of one row -> fp16 of t = acc*sa*sw + b (or GELU(t)),
+// packed in 16 words.  Column params come from the group's smem copy (broadcast LDS).
+Q4_DEV void dequant32(const uint32_t (&v)[32], float2 sa2, const float* sw, const float* bs, uint32_t (&h)[16],
+                      bool gelu = false) {
+  const float4* pw = reinterpret_cast<const float4*>(sw);
+  const float4* pb = reinterpret_cast<const float4*>(bs);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 w = pw[j], bb = pb[j];
+    float2 t0 = ffma2(fmul2(make_float2((float)(int)v[4 * j], (float)(int)v[4 * j + 1]), sa2), make_float2(w.x, w.y),
+                      make_float2(bb.x, bb.y));
+    float2 t1 = ffma2(fmul2(make_float2((float)(int)v[4 * j + 2], (float)(int)v[4 * j + 3]), sa2),
+                      make_float2(w.z, w.w), make_float2(bb.z, bb.w));
+    if (gelu) {
+      t0 = gelu2(t0);
+      t1 = gelu2(t1);
+    }
+    h[2 * j] = pack_half2(t0.x, t0.y);
+    h[2 * j + 1] = pack_half2(t1.x, t1.y);
+  }
+}
+
 // ------------------------------------------------------------------ epilogue pieces
 // Per-warp staging slab: 32 rows x 128 bytes, 16-byte chunks XOR-swizzled by row.
 Q4_DEV uint32_t slab_off(int row, int chunk) { return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4)); }
@@ -260,24 +262,25 @@ Q4_DEV void slab_load(uint8_t* stg, const uint8_t* gbase, int row0, int M, size_
   }
 }
 
-// Cross-CTA row exchange through L2: publish this CTA's partials, count arrivals of the
-// `ntn` CTAs sharing the m-block, wait, then every epilogue thread reads all partials.
-Q4_DEV void exchange_sync(unsigned* cnt, int ntn, int ew, int lane) {
-  __threadfence();
-  named_bar(1, 256);
-  if (ew == 0 && lane == 0) {
+// Cross-CTA row exchange through L2: every thread of the epilogue group has stored its
+// partial; one thread publishes the arrival (fence + atomic, cumulative over the group's
+// stores via bar.sync), waits for the `ntn` CTAs sharing the m-block, fences again, and
+// the group then reads all partials with L2 (.cg) loads.  Same pattern as a grid sync.
+Q4_DEV void exchange_sync(unsigned* cnt, int ntn, int bar_id, bool leader, int dbg = 0) {
+  named_bar(bar_id, 128);
+  if (leader && !(dbg & 32)) {
+    __threadfence();
     atomicAdd(cnt, 1u);
-    while (ld_acquire_gpu(cnt) < (unsigned)ntn) __nanosleep(64);
+    while (ld_acquire_gpu(cnt) < (unsigned)ntn) __nanosleep(32);
+    __threadfence();
   }
-  named_bar(1, 256);
-  __threadfence();
+  named_bar(bar_id, 128);
 }
 
-template <int TN, int KIND>
+template <int TN, int KIND, bool BI8>
 __global__ void __launch_bounds__(kThreads, 1)
     w4a4_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
-  using C = TcCfg<TN>;
-  constexpr bool ROW = (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4);
+  using C = TcCfg<TN, BI8>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full_p = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -295,8 +298,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int i = 0; i < C::SP; ++i) { mbar_init(&full_p[i], 1); mbar_init(&empty_p[i], 4); }
-    for (int i = 0; i < C::SU; ++i) { mbar_init(&full_u[i], 4); mbar_init(&empty_u[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    for (int i = 0; i < C::SU; ++i) { mbar_init(&full_u[i], BI8 ? 5 : 4); mbar_init(&empty_u[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  TileIter it(p, ROW);
+  TileIter it(p);
   int mb, nb;
 
   if (warp == 0) {
@@ -316,9 +319,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = g % C::SP;
           mbar_wait(&empty_p[s], ((g / C::SP) & 1u) ^ 1u);
           uint8_t* pk = smem + C::OFF_PK + s * C::PK_STAGE;
-          mbar_arrive_expect_tx(&full_p[s], (uint32_t)C::PK_STAGE);
-          tma_load_2d(pk, &tmA, &full_p[s], kb * 64, mb * C::BM);
-          tma_load_2d(pk + C::A_PK, &tmB, &full_p[s], kb * 64, nb * TN);
+          if (p.dbg & 1) {
+            mbar_arrive(&full_p[s]);
+          } else {
+            mbar_arrive_expect_tx(&full_p[s], (uint32_t)C::PK_STAGE);
+            tma_load_2d(pk, &tmA, &full_p[s], kb * 64, mb * C::BM);
+            if constexpr (!BI8) tma_load_2d(pk + C::A_PK, &tmB, &full_p[s], kb * 64, nb * TN);
+          }
+          if constexpr (BI8) {
+            // int8 weights straight into the (swizzled) operand stage of this k-block
+            const int su = g % C::SU;
+            mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
+            uint8_t* ub = smem + C::OFF_UN + su * C::UN_STAGE + C::A_UN;
+            mbar_arrive_expect_tx(&full_u[su], (uint32_t)C::B_UN);
+            tma_load_2d(ub, &tmB, &full_u[su], kb * 128, nb * TN);
+          }
         }
       }
     }
@@ -339,10 +354,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t ua = smem_u32(smem + C::OFF_UN + su * C::UN_STAGE);
           const uint32_t ub = ua + C::A_UN;
+          if (!(p.dbg & 4)) {
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            umma_i8(dt, umma_smem_desc(ua + ks * 32, 1024, 2), umma_smem_desc(ub + ks * 32, 1024, 2), idesc,
-                    (kb | ks) != 0);
+            for (int ks = 0; ks < 4; ++ks)
+              umma_i8(dt, umma_smem_desc(ua + ks * 32, 1024, 2), umma_smem_desc(ub + ks * 32, 1024, 2), idesc,
+                      (kb | ks) != 0);
+          }
           umma_commit(&empty_u[su]);
         }
         umma_commit(&tfull[b]);
@@ -361,8 +378,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
         const uint8_t* pk = smem + C::OFF_PK + s * C::PK_STAGE;
         uint8_t* un = smem + C::OFF_UN + su * C::UN_STAGE;
-        unpack_tile<128>(pk, un, C::BM, t);
-        unpack_tile<128>(pk + C::A_PK, un + C::A_UN, TN, t);
+        if (!(p.dbg & 2)) {
+          unpack_rows<C::BM>(pk, un, t);
+          if constexpr (!BI8) unpack_rows<TN>(pk + C::A_PK, un + C::A_UN, t);
+        }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -374,27 +393,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ---------------------------------------------------------------- epilogue
     const int ew = warp - kEpiWarp0;     // 0..7
-    const int grp = ew >> 2;             // column half
+    const int grp = ew >> 2;             // warpgroup: owns TMEM buffer grp (tiles tcount % 2 == grp)
+    const int bar_id = 1 + grp;
+    const bool leader = (ew & 3) == 0 && lane == 0;
     const int q = warp & 3;              // TMEM lane quarter
     const int r = q * 32 + lane;         // row within the tile
     uint8_t* stg = smem + C::OFF_STG + ew * 4096;
-    float4* rowp = reinterpret_cast<float4*>(smem + C::OFF_ROW);  // [2][128]
     const int N = p.N;
     const float clip = p.clip;
+    float* prm = reinterpret_cast<float*>(smem + C::OFF_PRM);  // sw | bias | gamma | beta of this CTA's n-block
+    constexpr int SW = TN < 64 ? TN : 64;  // staging slab width (columns)
+    {
+      const int c0 = (blockIdx.x % p.ntn) * TN;
+      for (int i = ew * 32 + lane; i < TN; i += 256) {
+        prm[i] = p.w_scales[c0 + i];
+        prm[TN + i] = p.bias ? __half2float(p.bias[c0 + i]) : 0.f;
+        if constexpr (KIND == EPI_RESLN_Q4) {
+          prm[2 * TN + i] = __half2float(p.gamma[c0 + i]);
+          prm[3 * TN + i] = __half2float(p.beta[c0 + i]);
+        }
+      }
+      asm volatile("bar.sync 3, 256;" ::: "memory");  // all 8 epilogue warps
+    }
     uint32_t tcount = 0;
     while (it.next(mb, nb)) {
       const uint32_t b = tcount & 1u;
+      if ((int)b != grp) { ++tcount; continue; }
       const int m0 = mb * C::BM;
       const int gm = m0 + r;
       const bool row_ok = gm < p.M;
-      const int c0 = nb * TN + grp * C::HW;  // first global column of this thread's half
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + b * TN + grp * C::HW;
+      const int c0 = nb * TN;  // first global column of the tile
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + b * TN;
       const float sa = row_ok ? p.a_scales[gm] * (1.0f / 256.0f) : 0.f;
+      const float2 sa2 = f2(sa);
       mbar_wait(&tfull[b], (tcount >> 1) & 1u);
       tc_fence_after();
 
       if constexpr (KIND == EPI_I32) {
-        for (int c = 0; c < C::HW; c += 8) {
+        for (int c = 0; c < TN; c += 8) {
           uint32_t v[8];
           tmem_ld8(tbase + c, v);
           tmem_wait_ld();
@@ -405,83 +441,79 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else if constexpr (KIND == EPI_F16) {
-        const float2 sa2 = f2(sa);
-        for (int s0 = 0; s0 < C::HW; s0 += 64) {
-          const int sw = C::HW - s0 < 64 ? C::HW - s0 : 64;
-          for (int c = 0; c < sw; c += 16) {
-            uint32_t v[16];
-            tmem_ld16(tbase + s0 + c, v);
-            const int n = c0 + s0 + c;
-            float2 ws[8], bb[8];
-            load_col_params(p.w_scales + n, p.bias ? p.bias + n : nullptr, ws, bb);
-            tmem_wait_ld();
-            uint32_t h[8];
+        for (int s0 = 0; s0 < ((p.dbg & 8) ? 0 : TN); s0 += SW) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float2 t = ffma2(fmul2(make_float2((float)(int)v[2 * j], (float)(int)v[2 * j + 1]), sa2), ws[j], bb[j]);
-              h[j] = pack_half2(t.x, t.y);
-            }
-            *reinterpret_cast<uint4*>(stg + slab_off(lane, c / 8)) = make_uint4(h[0], h[1], h[2], h[3]);
-            *reinterpret_cast<uint4*>(stg + slab_off(lane, c / 8 + 1)) = make_uint4(h[4], h[5], h[6], h[7]);
+          for (int c = 0; c < SW; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + s0 + c, v);
+            tmem_wait_ld();
+            uint32_t h[16];
+            dequant32(v, sa2, prm + s0 + c, prm + TN + s0 + c, h);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              *reinterpret_cast<uint4*>(stg + slab_off(lane, c / 8 + k)) =
+                  make_uint4(h[4 * k], h[4 * k + 1], h[4 * k + 2], h[4 * k + 3]);
           }
           __syncwarp();
           slab_store(stg, reinterpret_cast<uint8_t*>(p.out_f16), m0 + q * 32, p.M, (size_t)N * 2,
-                     (size_t)(c0 + s0) * 2, sw * 2, lane);
+                     (size_t)(c0 + s0) * 2, SW * 2, lane);
           __syncwarp();
         }
       } else {
         // ---------------------------------------------------------------- row epilogues
         const int ntn = p.ntn;
-        const float2 sa2 = f2(sa);
         float mean = 0.f, rstd = 0.f;
         if constexpr (KIND == EPI_RESLN_Q4) {
           // pass 1: z = acc*sa*sw + b + residual -> TMEM (in place); moments shifted by a pivot
           float2 s1 = f2(0.f), s2 = f2(0.f), npiv = f2(0.f);
-          for (int s0 = 0; s0 < C::HW; s0 += 64) {
-            const int sw = C::HW - s0 < 64 ? C::HW - s0 : 64;
+          for (int s0 = 0; s0 < TN; s0 += SW) {
             slab_load(stg, reinterpret_cast<const uint8_t*>(p.residual), m0 + q * 32, p.M, (size_t)N * 2,
                       (size_t)(c0 + s0) * 2, lane);
             __syncwarp();
-            for (int c = 0; c < sw; c += 16) {
-              uint32_t v[16];
-              tmem_ld16(tbase + s0 + c, v);
-              const uint4 ra = *reinterpret_cast<const uint4*>(stg + slab_off(lane, c / 8));
-              const uint4 rb = *reinterpret_cast<const uint4*>(stg + slab_off(lane, c / 8 + 1));
-              const uint32_t ru[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-              const int n = c0 + s0 + c;
-              float2 ws[8], bb[8];
-              load_col_params(p.w_scales + n, p.bias ? p.bias + n : nullptr, ws, bb);
+#pragma unroll
+            for (int c = 0; c < SW; c += 32) {
+              uint32_t v[32];
+              tmem_ld32(tbase + s0 + c, v);
+              uint32_t ru[16];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint4 x = *reinterpret_cast<const uint4*>(stg + slab_off(lane, c / 8 + k));
+                ru[4 * k] = x.x; ru[4 * k + 1] = x.y; ru[4 * k + 2] = x.z; ru[4 * k + 3] = x.w;
+              }
               tmem_wait_ld();
+              const float4* pw = reinterpret_cast<const float4*>(prm + s0 + c);
+              const float4* pb = reinterpret_cast<const float4*>(prm + TN + s0 + c);
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const float2 t = ffma2(fmul2(make_float2((float)(int)v[2 * j], (float)(int)v[2 * j + 1]), sa2), ws[j], bb[j]);
-                const float2 z = fadd2(t, unpack_half2(ru[j]));
-                if (s0 == 0 && c == 0 && j == 0) npiv = f2(-z.x);
-                const float2 d = fadd2(z, npiv);
-                s1 = fadd2(s1, d);
-                s2 = ffma2(d, d, s2);
-                v[2 * j] = __float_as_uint(z.x);
-                v[2 * j + 1] = __float_as_uint(z.y);
+                const float4 w = pw[j], bb = pb[j];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                  const int e = 4 * j + 2 * hh;
+                  const float2 t = ffma2(fmul2(make_float2((float)(int)v[e], (float)(int)v[e + 1]), sa2),
+                                         hh ? make_float2(w.z, w.w) : make_float2(w.x, w.y),
+                                         hh ? make_float2(bb.z, bb.w) : make_float2(bb.x, bb.y));
+                  const float2 z = fadd2(t, unpack_half2(ru[e / 2]));
+                  if (s0 == 0 && c == 0 && e == 0) npiv = f2(-z.x);
+                  const float2 d = fadd2(z, npiv);
+                  s1 = fadd2(s1, d);
+                  s2 = ffma2(d, d, s2);
+                  v[e] = __float_as_uint(z.x);
+                  v[e + 1] = __float_as_uint(z.y);
+                }
               }
-              tmem_st16(tbase + s0 + c, v);
+              tmem_st32(tbase + s0 + c, v);
             }
             __syncwarp();
           }
           tmem_wait_st();
-          // combine the two column halves (Chan), then the ntn CTAs of the row group
+          // publish this CTA's (mean, M2) over its TN columns; combine the ntn CTAs (Chan)
           {
-            const float nh = (float)C::HW;
+            const float nh = (float)TN;
             const float S1 = s1.x + s1.y, S2 = s2.x + s2.y;
             const float lmean = -npiv.x + S1 / nh;
             const float lm2 = fmaxf(S2 - S1 * S1 / nh, 0.f);
-            rowp[grp * 128 + r] = make_float4(lmean, lm2, 0.f, 0.f);
-            named_bar(1, 256);
-            const float4 a0 = rowp[r], a1 = rowp[128 + r];
-            const float d = a1.x - a0.x;
-            const float cm = a0.x + d * 0.5f;
-            const float cm2 = a0.y + a1.y + d * d * (nh * 0.5f);
-            if (grp == 0) p.xstat[((size_t)mb * ntn + nb) * 128 + r] = make_float2(cm, cm2);
-            exchange_sync(p.xcnt + mb, ntn, ew, lane);
+            p.xstat[((size_t)mb * ntn + nb) * 128 + r] = make_float2(lmean, lm2);
+            exchange_sync(p.xcnt + mb, ntn, bar_id, leader, p.dbg);
             float2 st = __ldcg(&p.xstat[((size_t)mb * ntn) * 128 + r]);
             float cnt = (float)TN;
             mean = st.x;
@@ -501,91 +533,84 @@ __global__ void __launch_bounds__(kThreads, 1)
         __half2 hmax = __float2half2_rn(0.f);
         const bool want_f16 = p.out_f16 != nullptr;
         const float2 nmean2 = f2(-mean), rstd2 = f2(rstd);
-        for (int s0 = 0; s0 < C::HW; s0 += 64) {
-          const int sw = C::HW - s0 < 64 ? C::HW - s0 : 64;
-          for (int c = 0; c < sw; c += 16) {
-            uint32_t v[16];
-            tmem_ld16(tbase + s0 + c, v);
-            const int n = c0 + s0 + c;
-            uint32_t h[8];
+        for (int s0 = 0; s0 < TN; s0 += SW) {
+#pragma unroll
+          for (int c = 0; c < SW; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + s0 + c, v);
+            tmem_wait_ld();
+            uint32_t h[16];
             if constexpr (KIND == EPI_RESLN_Q4) {
-              float2 gm[8], bt[8];
-              load_half_params(p.gamma + n, p.beta + n, gm, bt);
-              tmem_wait_ld();
+              const float4* pg = reinterpret_cast<const float4*>(prm + 2 * TN + s0 + c);
+              const float4* pe = reinterpret_cast<const float4*>(prm + 3 * TN + s0 + c);
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const float2 z = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-                const float2 y = ffma2(fmul2(fadd2(z, nmean2), rstd2), gm[j], bt[j]);
-                h[j] = pack_half2(y.x, y.y);
+                const float4 g4 = pg[j], e4 = pe[j];
+                const float2 z0 = make_float2(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]));
+                const float2 z1 = make_float2(__uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                const float2 y0 = ffma2(fmul2(fadd2(z0, nmean2), rstd2), make_float2(g4.x, g4.y), make_float2(e4.x, e4.y));
+                const float2 y1 = ffma2(fmul2(fadd2(z1, nmean2), rstd2), make_float2(g4.z, g4.w), make_float2(e4.z, e4.w));
+                h[2 * j] = pack_half2(y0.x, y0.y);
+                h[2 * j + 1] = pack_half2(y1.x, y1.y);
               }
             } else {
-              float2 ws[8], bb[8];
-              load_col_params(p.w_scales + n, p.bias ? p.bias + n : nullptr, ws, bb);
-              tmem_wait_ld();
+              uint32_t tq[16];
+              dequant32(v, sa2, prm + s0 + c, prm + TN + s0 + c, tq, true);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float2 t = ffma2(fmul2(make_float2((float)(int)v[2 * j], (float)(int)v[2 * j + 1]), sa2), ws[j], bb[j]);
-                const float2 y = gelu2(t);
-                h[j] = pack_half2(y.x, y.y);
-              }
+              for (int j = 0; j < 16; ++j) h[j] = tq[j];
             }
             if (clip > 0.f) {
               const __half2 cl = __float2half2_rn(clip);
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
+              for (int j = 0; j < 16; ++j)
                 hmax = __hmax2(hmax, __hmin2(__habs2(*reinterpret_cast<const __half2*>(&h[j])), cl));
             } else {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) hmax = __hmax2(hmax, __habs2(*reinterpret_cast<const __half2*>(&h[j])));
+              for (int j = 0; j < 16; ++j) hmax = __hmax2(hmax, __habs2(*reinterpret_cast<const __half2*>(&h[j])));
             }
-            tmem_st8(tbase + s0 + c, h);
+            tmem_st16(tbase + s0 + c, h);
             if (want_f16) {
-              *reinterpret_cast<uint4*>(stg + slab_off(lane, c / 8)) = make_uint4(h[0], h[1], h[2], h[3]);
-              *reinterpret_cast<uint4*>(stg + slab_off(lane, c / 8 + 1)) = make_uint4(h[4], h[5], h[6], h[7]);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                *reinterpret_cast<uint4*>(stg + slab_off(lane, c / 8 + k)) =
+                    make_uint4(h[4 * k], h[4 * k + 1], h[4 * k + 2], h[4 * k + 3]);
             }
           }
           if (want_f16) {
             __syncwarp();
             slab_store(stg, reinterpret_cast<uint8_t*>(p.out_f16), m0 + q * 32, p.M, (size_t)N * 2,
-                       (size_t)(c0 + s0) * 2, sw * 2, lane);
+                       (size_t)(c0 + s0) * 2, SW * 2, lane);
             __syncwarp();
           }
         }
         tmem_wait_st();
         float amax = fmaxf(__low2float(hmax), __high2float(hmax));
-        // row max-abs over the two halves and the ntn CTAs
-        rowp[grp * 128 + r].z = amax;
-        named_bar(1, 256);
-        amax = fmaxf(rowp[r].z, rowp[128 + r].z);
-        if (grp == 0) p.xamax[((size_t)mb * ntn + nb) * 128 + r] = amax;
-        exchange_sync(p.xcnt + p.mblocks + mb, ntn, ew, lane);
+        // row max-abs over the ntn CTAs
+        p.xamax[((size_t)mb * ntn + nb) * 128 + r] = amax;
+        exchange_sync(p.xcnt + p.mblocks + mb, ntn, bar_id, leader, p.dbg);
         for (int k = 0; k < ntn; ++k) amax = fmaxf(amax, __ldcg(&p.xamax[((size_t)mb * ntn + k) * 128 + r]));
         // pass B: codes (R1-R3), packed, staged, coalesced stores
         const float r7 = amax > 0.f ? __fdiv_rn(7.0f, amax) : 0.f;
-        for (int s0 = 0; s0 < C::HW; s0 += 64) {
-          const int sw = C::HW - s0 < 64 ? C::HW - s0 : 64;
-          for (int c = 0; c < sw; c += 16) {
-            uint32_t h[8];
-            tmem_ld8(tbase + s0 + c, h);
+        for (int s0 = 0; s0 < TN; s0 += SW) {
+#pragma unroll
+          for (int c = 0; c < SW; c += 32) {
+            uint32_t h[16];
+            tmem_ld16(tbase + s0 + c, h);
             tmem_wait_ld();
-            int qv[16];
-            requant16(h, amax, r7, clip, qv);
-            uint32_t w0 = cvt_pack_s4(qv[7], qv[6], 0u);
-            w0 = cvt_pack_s4(qv[5], qv[4], w0);
-            w0 = cvt_pack_s4(qv[3], qv[2], w0);
-            w0 = cvt_pack_s4(qv[1], qv[0], w0);
-            uint32_t w1 = cvt_pack_s4(qv[15], qv[14], 0u);
-            w1 = cvt_pack_s4(qv[13], qv[12], w1);
-            w1 = cvt_pack_s4(qv[11], qv[10], w1);
-            w1 = cvt_pack_s4(qv[9], qv[8], w1);
-            // 16 codes = 8 bytes; a 64-column slab row holds 32 code bytes in chunks 0-1
-            *reinterpret_cast<uint2*>(stg + slab_off(lane, c / 32) + ((c / 16) & 1) * 8) = make_uint2(w0, w1);
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t hk[4] = {h[4 * k], h[4 * k + 1], h[4 * k + 2], h[4 * k + 3]};
+              w[k] = requant8(hk, amax, r7, clip);
+            }
+            // 32 codes = 16 bytes = slab chunk c/32 of this row (a 64-column slab row holds 32 B)
+            *reinterpret_cast<uint4*>(stg + slab_off(lane, c / 32)) = make_uint4(w[0], w[1], w[2], w[3]);
           }
           __syncwarp();
-          slab_store(stg, p.out_codes, m0 + q * 32, p.M, (size_t)N / 2, (size_t)(c0 + s0) / 2, sw / 2, lane);
+          slab_store(stg, p.out_codes, m0 + q * 32, p.M, (size_t)N / 2, (size_t)(c0 + s0) / 2, SW / 2, lane);
           __syncwarp();
         }
-        if (row_ok && nb == 0 && grp == 0) p.out_scales[gm] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
+        if (row_ok && nb == 0) p.out_scales[gm] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
       }
       // accumulator buffer b may be overwritten by the MMA of tile tcount + 2
       tc_fence_before();
@@ -623,7 +648,7 @@ EncodeTiledFn get_encode() {
 
 // 2-D uint8 tensor map over a row-major [rows, row_bytes] buffer, box [box_rows, box_bytes].
 bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t row_bytes, uint32_t box_rows,
-               uint32_t box_bytes) {
+               uint32_t box_bytes, bool swizzle128 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {row_bytes, rows};
@@ -631,7 +656,8 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t row_byt
   cuuint32_t box[2] = {box_bytes, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -647,10 +673,10 @@ int num_sms() {
   return n;
 }
 
-template <int TN, int KIND>
+template <int TN, int KIND, bool BI8>
 cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {
-  using C = TcCfg<TN>;
-  auto kern = w4a4_tc_kernel<TN, KIND>;
+  using C = TcCfg<TN, BI8>;
+  auto kern = w4a4_tc_kernel<TN, KIND, BI8>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -659,7 +685,9 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   }
   CUtensorMap ta, tb;
   const uint64_t kb = (uint64_t)g.K / 2;
-  if (!make_tmap(&ta, g.a_codes, (uint64_t)g.M, kb, 128, 64) || !make_tmap(&tb, g.w_codes, (uint64_t)g.N, kb, TN, 64)) {
+  const bool okb = BI8 ? make_tmap(&tb, g.w_i8, (uint64_t)g.N, (uint64_t)g.K, TN, 128, true)
+                       : make_tmap(&tb, g.w_codes, (uint64_t)g.N, kb, TN, 64);
+  if (!make_tmap(&ta, g.a_codes, (uint64_t)g.M, kb, 128, 64) || !okb) {
     *why = "cuTensorMapEncodeTiled failed (driver entry point or alignment)";
     return cudaErrorInvalidValue;
   }
@@ -672,14 +700,15 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.ln_eps = g.ln_eps; p.clip = g.clip;
   p.out_i32 = g.out_i32; p.out_f16 = g.out_f16; p.out_codes = g.out_codes; p.out_scales = g.out_scales;
   p.xstat = nullptr; p.xamax = nullptr; p.xcnt = nullptr;
+  static const int dbg = [] { const char* e = getenv("Q4_DEBUG_SKIP"); return e ? atoi(e) : 0; }();
+  p.dbg = dbg;
   const int sms = num_sms();
-  int grid;
+  // groups of ntn co-resident CTAs (one per SM); a group walks the m-blocks
+  if (p.ntn > sms) { *why = "N/TN exceeds the number of SMs"; return cudaErrorNotSupported; }
+  p.groups = sms / p.ntn;
+  if (p.groups > p.mblocks) p.groups = p.mblocks;
+  const int grid = p.groups * p.ntn;
   if (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4) {
-    // co-residency: one CTA per SM, groups of ntn CTAs; every CTA of a group must be resident
-    if (p.ntn > sms) { *why = "row epilogue needs N/TN <= #SMs"; return cudaErrorNotSupported; }
-    p.groups = sms / p.ntn;
-    if (p.groups > p.mblocks) p.groups = p.mblocks;
-    grid = p.groups * p.ntn;
     const size_t need = tc_workspace_bytes(g.M, g.N, TN);
     if (!ws || ws_bytes < need) { *why = "workspace too small for the row-epilogue exchange"; return cudaErrorInvalidValue; }
     uint8_t* w = reinterpret_cast<uint8_t*>(ws);
@@ -689,26 +718,27 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     p.xcnt = reinterpret_cast<unsigned*>(w + nslot * 12);
     cudaError_t e = cudaMemsetAsync(p.xcnt, 0, sizeof(unsigned) * 2 * p.mblocks, s);
     if (e != cudaSuccess) return e;
-  } else {
-    p.groups = 0;
-    const int tiles = p.mblocks * p.ntn;
-    grid = tiles < sms ? tiles : sms;
   }
   note_launch();
   kern<<<grid, kThreads, C::SMEM, s>>>(ta, tb, p);
   return cudaGetLastError();
 }
 
-template <int TN>
-cudaError_t run_tc_kind(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s, const char** why) {
+template <int TN, bool BI8>
+cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s, const char** why) {
   switch (g.kind) {
-    case EPI_I32: return run_tc<TN, EPI_I32>(g, ws, wsb, s, why);
-    case EPI_F16: return run_tc<TN, EPI_F16>(g, ws, wsb, s, why);
-    case EPI_GELU_Q4: return run_tc<TN, EPI_GELU_Q4>(g, ws, wsb, s, why);
-    case EPI_RESLN_Q4: return run_tc<TN, EPI_RESLN_Q4>(g, ws, wsb, s, why);
+    case EPI_I32: return run_tc<TN, EPI_I32, BI8>(g, ws, wsb, s, why);
+    case EPI_F16: return run_tc<TN, EPI_F16, BI8>(g, ws, wsb, s, why);
+    case EPI_GELU_Q4: return run_tc<TN, EPI_GELU_Q4, BI8>(g, ws, wsb, s, why);
+    case EPI_RESLN_Q4: return run_tc<TN, EPI_RESLN_Q4, BI8>(g, ws, wsb, s, why);
   }
   *why = "unknown epilogue kind";
   return cudaErrorInvalidValue;
+}
+template <int TN>
+cudaError_t run_tc_kind(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s, const char** why) {
+  if (g.w_i8) return run_tc_kind2<TN, true>(g, ws, wsb, s, why);
+  return run_tc_kind2<TN, false>(g, ws, wsb, s, why);
 }
 
 }  // namespace

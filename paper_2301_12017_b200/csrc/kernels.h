@@ -15,6 +15,7 @@ struct GemmArgs {
   const uint8_t* a_codes;  // [M, K/2]
   const float* a_scales;   // [M]
   const uint8_t* w_codes;  // [N, K/2]
+  const int8_t* w_i8;      // [N, K] prepacked int8 (q4_prepack_weights) or nullptr
   const float* w_scales;   // [N]
   int M, N, K;
   int kind;      // q4_epi_kind
@@ -30,6 +31,7 @@ struct GemmArgs {
   float* out_scales;
 };
 
+cudaError_t launch_prepack_weights(const uint8_t* w_codes, int64_t N, int64_t K, int8_t* w_i8, cudaStream_t s);
 cudaError_t launch_quantize_rows(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
                                  uint8_t* codes, float* scales, cudaStream_t s);
 // Returns cudaErrorNotSupported for shapes the tcgen05 path cannot take (message in *why).

@@ -130,11 +130,18 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
   g.ln_eps = epi->ln_eps; g.clip = epi->requant_clip;
   g.out_i32 = epi->out_i32; g.out_f16 = reinterpret_cast<__half*>(epi->out_f16);
   g.out_codes = epi->out_codes; g.out_scales = epi->out_scales;
+  g.w_i8 = nullptr;
+  if (epi->mainloop == Q4_MAINLOOP_TCGEN05_W8 || (epi->mainloop == Q4_MAINLOOP_AUTO && epi->w_i8 && M > 256)) {
+    if (!epi->w_i8 || !al16(epi->w_i8))
+      return fail(Q4_EINVAL, "q4_w4a4_linear: TCGEN05_W8 needs 16-byte aligned epi->w_i8 (q4_prepack_weights)");
+    g.w_i8 = epi->w_i8;
+  }
   const char* why = "";
   cudaError_t e;
   switch (epi->mainloop) {
     case Q4_MAINLOOP_AUTO:
-    case Q4_MAINLOOP_TCGEN05: e = q4::launch_w4a4_tc(g, workspace, ws_bytes, (cudaStream_t)stream, &why); break;
+    case Q4_MAINLOOP_TCGEN05:
+    case Q4_MAINLOOP_TCGEN05_W8: e = q4::launch_w4a4_tc(g, workspace, ws_bytes, (cudaStream_t)stream, &why); break;
     case Q4_MAINLOOP_MMA_SYNC_S8: e = q4::launch_w4a4_legacy(g, false, (cudaStream_t)stream, &why); break;
     case Q4_MAINLOOP_MMA_SYNC_S4: e = q4::launch_w4a4_legacy(g, true, (cudaStream_t)stream, &why); break;
     default: return fail(Q4_EINVAL, "q4_w4a4_linear: unknown mainloop %d", epi->mainloop);
@@ -142,6 +149,16 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
   if (e == cudaErrorNotSupported) return fail(Q4_EUNSUPPORTED, "q4_w4a4_linear: %s (M=%lld N=%lld K=%lld)", why, (long long)M, (long long)N, (long long)K);
   if (e != cudaSuccess) return fail(Q4_ECUDA, "q4_w4a4_linear: %s %s", cudaGetErrorString(e), why);
   return Q4_OK;
+}
+
+q4_status q4_prepack_weights(const uint8_t* w_codes, int64_t N, int64_t K, int8_t* w_i8, void* stream) {
+  g_err[0] = 0;
+  if (N < 0 || K <= 0 || K % 32) return fail(Q4_ESHAPE, "q4_prepack_weights: N=%lld K=%lld (need K %% 32 == 0)", (long long)N, (long long)K);
+  if (N == 0) return Q4_OK;
+  if (!w_codes || !w_i8) return fail(Q4_EINVAL, "q4_prepack_weights: NULL w_codes/w_i8");
+  if (!al16(w_codes) || !al16(w_i8)) return fail(Q4_EALIGN, "q4_prepack_weights: pointers must be 16-byte aligned");
+  cudaError_t e = q4::launch_prepack_weights(w_codes, N, K, w_i8, (cudaStream_t)stream);
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_prepack_weights");
 }
 
 q4_status q4_attention_f16_q4(const uint16_t* qkv, int64_t B, int64_t S, int32_t heads, int32_t head_dim,
@@ -261,7 +278,7 @@ q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, i
   q4_epilogue e;
   // QKV projection: dequant + bias -> fp16
   memset(&e, 0, sizeof e);
-  e.kind = Q4_EPI_F16; e.bias = w->bqkv; e.out_f16 = qkv;
+  e.kind = Q4_EPI_F16; e.bias = w->bqkv; e.out_f16 = qkv; e.w_i8 = w->wqkv8;
   if ((st = lin(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, e))) return st;
   if ((st = acc_tap(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, tp.acc_qkv))) return st;
   // FP16 attention + fused per-token ctx quantize
@@ -271,18 +288,19 @@ q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, i
   // attention output: dequant + bias + residual(h_in) + LN1 + requant
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_RESLN_Q4; e.bias = w->bo; e.residual = h_in; e.gamma = w->ln1_g; e.beta = w->ln1_b;
-  e.ln_eps = cfg->ln_eps; e.out_f16 = h1; e.out_codes = h1_codes; e.out_scales = h1_scales;
+  e.ln_eps = cfg->ln_eps; e.out_f16 = h1; e.out_codes = h1_codes; e.out_scales = h1_scales; e.w_i8 = w->wo8;
   if ((st = lin(ctx_codes, ctx_scales, w->wo, w->so, h, h, e))) return st;
   if ((st = acc_tap(ctx_codes, ctx_scales, w->wo, w->so, h, h, tp.acc_o))) return st;
   // MLP intermediate: dequant + bias + GELU + requant
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_GELU_Q4; e.bias = w->b1; e.out_f16 = tp.ffn1; e.out_codes = f_codes; e.out_scales = f_scales;
+  e.w_i8 = w->w18;
   if ((st = lin(h1_codes, h1_scales, w->w1, w->s1, f, h, e))) return st;
   if ((st = acc_tap(h1_codes, h1_scales, w->w1, w->s1, f, h, tp.acc_1))) return st;
   // MLP output: dequant + bias + residual(h1) + LN2 + requant
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_RESLN_Q4; e.bias = w->b2; e.residual = h1; e.gamma = w->ln2_g; e.beta = w->ln2_b;
-  e.ln_eps = cfg->ln_eps; e.out_f16 = h_out; e.out_codes = hq_out; e.out_scales = hs_out;
+  e.ln_eps = cfg->ln_eps; e.out_f16 = h_out; e.out_codes = hq_out; e.out_scales = hs_out; e.w_i8 = w->w28;
   if ((st = lin(f_codes, f_scales, w->w2, w->s2, h, f, e))) return st;
   if ((st = acc_tap(f_codes, f_scales, w->w2, w->s2, h, f, tp.acc_2))) return st;
   return Q4_OK;

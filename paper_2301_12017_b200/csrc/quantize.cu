@@ -3,8 +3,9 @@
 //
 // One warp per row.  Each lane owns 16-byte vectors (8 halves) v = lane + 32*i, kept
 // in registers between the two passes (warp-shuffle max-abs, then codes), so x is read
-// from HBM exactly once.  Codes: rint(div.rn(7x, amax)) -- the IEEE-exact form that
-// equals round-half-even of the rational 7x/amax for every fp16 pair (R3).
+// from HBM exactly once.  Codes: round-half-even of the rational 7x/amax (R3),
+// computed as rint(x * RN(7/amax)) with an exact FMA tie-break near half-integers
+// (requant8 in common.cuh) -- bit-identical to rint(div.rn(7x, amax)).
 #include "kernels.h"
 
 namespace q4 {
@@ -41,23 +42,13 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(const __half* __rest
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   uint32_t* cr = reinterpret_cast<uint32_t*>(codes + row * (int64_t)(cols >> 1));
+  const float r7 = amax > 0.f ? __fdiv_rn(7.0f, amax) : 0.f;
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
     const int vi = lane + 32 * i;
     if (vi < nvec) {
-      const uint32_t* u = reinterpret_cast<const uint32_t*>(&v[i]);
-      int q[8];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float2 f = unpack_half2(u[j]);
-        if (clip > 0.f) {
-          f.x = fminf(fmaxf(f.x, -clip), clip);
-          f.y = fminf(fmaxf(f.y, -clip), clip);
-        }
-        q[2 * j] = amax > 0.f ? q4_code(f.x, amax) : 0;
-        q[2 * j + 1] = amax > 0.f ? q4_code(f.y, amax) : 0;
-      }
-      cr[vi] = pack8(q);
+      const uint32_t hh[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+      cr[vi] = requant8(hh, amax, r7, clip);
     }
   }
   if (lane == 0) scales[row] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
@@ -89,22 +80,34 @@ __global__ void __launch_bounds__(256) quantize_rows_long_kernel(const __half* _
   }
   for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   uint32_t* cr = reinterpret_cast<uint32_t*>(codes + row * (int64_t)(cols >> 1));
+  const float r7 = amax > 0.f ? __fdiv_rn(7.0f, amax) : 0.f;
   for (int vi = lane; vi < nvec; vi += 32) {
-    uint4 vv = __ldg(xr + vi);
-    const uint32_t* u = reinterpret_cast<const uint32_t*>(&vv);
-    int q[8];
-    for (int j = 0; j < 4; ++j) {
-      float2 f = unpack_half2(u[j]);
-      if (clip > 0.f) {
-        f.x = fminf(fmaxf(f.x, -clip), clip);
-        f.y = fminf(fmaxf(f.y, -clip), clip);
-      }
-      q[2 * j] = amax > 0.f ? q4_code(f.x, amax) : 0;
-      q[2 * j + 1] = amax > 0.f ? q4_code(f.y, amax) : 0;
-    }
-    cr[vi] = pack8(q);
+    const uint4 vv = __ldg(xr + vi);
+    const uint32_t hh[4] = {vv.x, vv.y, vv.z, vv.w};
+    cr[vi] = requant8(hh, amax, r7, clip);
   }
   if (lane == 0) scales[row] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
+}
+
+// Offline weight prep for the tcgen05 mainloop: packed INT4 [N, K/2] -> int8 [N, K] holding
+// 16*q in the operand K order the on-chip activation unpack produces: each 16-byte packed
+// chunk (32 consecutive k) -> 16 bytes of the even k, then 16 bytes of the odd k (the
+// K-permutation trick).  Same codes, same products.
+__global__ void prepack_weights_kernel(const uint4* __restrict__ w, int64_t nchunks, uint4* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nchunks) return;
+  const uint4 x = __ldg(w + i);
+  out[2 * i] = make_uint4(nib_lo16(x.x), nib_lo16(x.y), nib_lo16(x.z), nib_lo16(x.w));
+  out[2 * i + 1] = make_uint4(nib_hi16(x.x), nib_hi16(x.y), nib_hi16(x.z), nib_hi16(x.w));
+}
+
+cudaError_t launch_prepack_weights(const uint8_t* w_codes, int64_t N, int64_t K, int8_t* w_i8, cudaStream_t s) {
+  const int64_t nchunks = N * K / 32;
+  if (nchunks == 0) return cudaSuccess;
+  note_launch();
+  prepack_weights_kernel<<<(unsigned)((nchunks + 255) / 256), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(w_codes), nchunks, reinterpret_cast<uint4*>(w_i8));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_quantize_rows(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,

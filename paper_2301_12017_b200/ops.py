@@ -48,7 +48,7 @@ def quantize_rows(x: torch.Tensor, clip: float = 0.0, codes=None, scales=None):
 
 def w4a4_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None, residual=None,
                 gamma=None, beta=None, ln_eps=1e-12, clip=0.0, mainloop=0, f16_tap=False,
-                out=None, workspace=None):
+                out=None, workspace=None, w_i8=None):
     """a3-a6: INT4 x INT4 -> exact INT32 -> fused epilogue.  Returns a dict with the
     outputs of the epilogue kind: i32 | f16 | (codes, scales[, f16])."""
     _need(a_codes, torch.uint8, "a_codes", 2)
@@ -73,7 +73,7 @@ def w4a4_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None
     e = Epilogue(kind=kind, mainloop=mainloop, bias=_ptr(bias), residual=_ptr(residual),
                  gamma=_ptr(gamma), beta=_ptr(beta), ln_eps=ln_eps, requant_clip=clip,
                  out_i32=_ptr(o.get("i32")), out_f16=_ptr(o.get("f16")),
-                 out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")))
+                 out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")), w_i8=_ptr(w_i8))
     ws_bytes = lib().q4_w4a4_linear_workspace(M, N, K, kind)
     if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
         workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
@@ -100,18 +100,32 @@ def layer_cfg(cfg: dict) -> LayerCfg:
     return LayerCfg(cfg["hidden"], cfg["heads"], cfg["head_dim"], cfg["ffn"], cfg.get("ln_eps", 1e-12))
 
 
+def prepack_weights(w_codes: torch.Tensor) -> torch.Tensor:
+    """a2': packed INT4 [N, K/2] -> MMA-ready int8 [N, K] (q4_prepack_weights)."""
+    _need(w_codes, torch.uint8, "w_codes", 2)
+    N, K = w_codes.shape[0], w_codes.shape[1] * 2
+    out = torch.empty(N, K, dtype=torch.int8, device=w_codes.device)
+    check(lib().q4_prepack_weights(_ptr(w_codes), N, K, _ptr(out), _stream()))
+    return out
+
+
 def layer_weights(w: dict) -> LayerWeights:
-    """w: dict of CUDA tensors (codes uint8, scales fp32, biases / LN params fp16)."""
-    return LayerWeights(**{k: w[k].data_ptr() for k in _lib.WEIGHT_FIELDS})
+    """w: dict of CUDA tensors (codes uint8, scales fp32, biases / LN params fp16; the
+    optional prepacked int8 copies wqkv8 / wo8 / w18 / w28)."""
+    return LayerWeights(**{k: (w[k].data_ptr() if w.get(k) is not None else None)
+                           for k in _lib.WEIGHT_FIELDS})
 
 
-def quantize_layer(params: dict, device="cuda") -> dict:
+def quantize_layer(params: dict, device="cuda", prepack: bool = True) -> dict:
     """Offline weight prep (a2, not timed): fp16 [out, in] weights -> per-output-channel
-    INT4 codes + scales on the device; biases and LN parameters copied as fp16."""
+    INT4 codes + scales on the device (and, with prepack, the MMA-ready int8 copy);
+    biases and LN parameters copied as fp16."""
     w = {}
     for k in ("wqkv", "wo", "w1", "w2"):
         t = torch.as_tensor(params[k]).to(device=device, dtype=torch.float16).contiguous()
         w[k], w["s" + k[1:]] = quantize_rows(t)
+        if prepack:
+            w[k + "8"] = prepack_weights(w[k])
     for k in ("bqkv", "bo", "b1", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b"):
         w[k] = torch.as_tensor(params[k]).to(device=device, dtype=torch.float16).contiguous()
     return w

@@ -76,12 +76,14 @@ SHAPES = [(1, 256, 256), (127, 768, 768), (129, 3072, 768), (300, 768, 3072), (2
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
-@pytest.mark.parametrize("mainloop", [1, 2, 3], ids=["tcgen05", "mma_s8", "mma_s4"])
+@pytest.mark.parametrize("mainloop", [1, 4, 2, 3], ids=["tcgen05", "tcgen05_w8", "mma_s8", "mma_s4"])
 def test_gemm_i32_bit_exact(q4, M, N, K, mainloop):
     a = synth.random_packed(M, K, f"ga{M}_{K}", full_range=True)
     w = synth.random_packed(N, K, f"gw{N}_{K}", full_range=True)
     sa, sw = synth.random_scales(M, "gsa"), synth.random_scales(N, "gsw")
-    out = q4.w4a4_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_I32, mainloop=mainloop)
+    wd = dev(w)
+    w8 = q4.prepack_weights(wd) if mainloop == 4 else None
+    out = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_I32, mainloop=mainloop, w_i8=w8)
     ref = orc.gemm_i32(a, w, M, N, K)
     got = host(out["i32"])
     assert np.array_equal(got, ref), f"{np.count_nonzero(got != ref)} mismatches"
@@ -99,23 +101,29 @@ def test_gemm_extreme_codes(q4):
 
 # ------------------------------------------------------------------ a4 dequant epilogue
 @pytest.mark.parametrize("M,N,K", [(1, 768, 768), (129, 2304, 768), (300, 3072, 1024), (77, 1024, 4096)])
-@pytest.mark.parametrize("mainloop", [1, 2], ids=["tcgen05", "mma_s8"])
+@pytest.mark.parametrize("mainloop", [1, 4, 2], ids=["tcgen05", "tcgen05_w8", "mma_s8"])
 def test_linear_f16(q4, M, N, K, mainloop):
     x, wt, b = synth.hidden(M, K, f"fx{M}"), synth.weight(N, K, f"fw{N}_{K}"), synth.bias(N, f"fb{N}")
     a, sa = orc.quantize_rows(x)
     w, sw = orc.quantize_rows(wt)
-    out = q4.w4a4_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_F16, bias=dev(b), mainloop=mainloop)
+    wd = dev(w)
+    w8 = q4.prepack_weights(wd) if mainloop == 4 else None
+    out = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_F16, bias=dev(b), mainloop=mainloop, w_i8=w8)
     ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, orc.EPI_F16, bias=b)["f16"]
     assert_f16_close(host(out["f16"]), ref, "F16")
 
 
 # ------------------------------------------------------------------ a5 GELU + requant
 @pytest.mark.parametrize("M,N,K", [(128, 3072, 768), (257, 4096, 1024), (33, 768, 768), (5, 256, 256), (100, 2048, 512)])
-def test_linear_gelu_q4(q4, M, N, K):
+@pytest.mark.parametrize("mainloop", [1, 4], ids=["tcgen05", "tcgen05_w8"])
+def test_linear_gelu_q4(q4, M, N, K, mainloop):
     x, wt, b = synth.hidden(M, K, f"gx{M}"), synth.weight(N, K, f"gw{N}_{K}"), synth.bias(N, f"gb{N}")
     a, sa = orc.quantize_rows(x)
     w, sw = orc.quantize_rows(wt)
-    out = q4.w4a4_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_GELU_Q4, bias=dev(b), f16_tap=True)
+    wd = dev(w)
+    w8 = q4.prepack_weights(wd) if mainloop == 4 else None
+    out = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_GELU_Q4, bias=dev(b), f16_tap=True,
+                         mainloop=mainloop, w_i8=w8)
     ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, orc.EPI_GELU_Q4, bias=b)
     y = host(out["f16"])
     assert_f16_close(y, ref["f16"], "GELU f16")
@@ -129,14 +137,18 @@ def test_linear_gelu_q4(q4, M, N, K):
 
 # ------------------------------------------------------------------ a6 residual + LN + requant
 @pytest.mark.parametrize("M,N,K", [(128, 768, 768), (257, 1024, 1024), (300, 768, 3072), (64, 1024, 4096), (7, 256, 512)])
-def test_linear_resln_q4(q4, M, N, K):
+@pytest.mark.parametrize("mainloop", [1, 4], ids=["tcgen05", "tcgen05_w8"])
+def test_linear_resln_q4(q4, M, N, K, mainloop):
     x, wt, b = synth.hidden(M, K, f"lx{M}"), synth.weight(N, K, f"lw{N}_{K}"), synth.bias(N, f"lb{N}")
     res = synth.hidden(M, N, f"lr{M}_{N}")
     gam, bet = synth.ln_params(N, f"ln{N}")
     a, sa = orc.quantize_rows(x)
     w, sw = orc.quantize_rows(wt)
-    out = q4.w4a4_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_RESLN_Q4, bias=dev(b),
-                         residual=dev(res), gamma=dev(gam), beta=dev(bet), ln_eps=1e-12)
+    wd = dev(w)
+    w8 = q4.prepack_weights(wd) if mainloop == 4 else None
+    out = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_RESLN_Q4, bias=dev(b),
+                         residual=dev(res), gamma=dev(gam), beta=dev(bet), ln_eps=1e-12,
+                         mainloop=mainloop, w_i8=w8)
     ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, orc.EPI_RESLN_Q4, bias=b, residual=res, gamma=gam,
                           beta=bet, ln_eps=1e-12)
     y = host(out["f16"])
@@ -311,3 +323,39 @@ def test_launch_count_and_errors(q4):
         w = torch.zeros(48, 16, dtype=torch.uint8, device="cuda")
         s = torch.ones(64, device="cuda")
         q4.w4a4_linear(a, s[:4], w, s[:48], q4.EPI_F16)
+
+
+@pytest.mark.slow
+def test_quantize_exhaustive_fp16_pairs(q4):
+    """Every (x, amax) fp16 pair, 0 <= x <= amax, through the CUDA quantize kernel (whose
+    fast path is rint(x * RN(7/amax)) with an exact FMA tie-break) equals the IEEE
+    division form rint(fl32(7x) / amax) -- which the oracle's exact rational rounding
+    equals over the same sweep (tests/test_oracle_quant.py)."""
+    allpos = np.arange(1, 0x7C00, dtype=np.uint16).view(np.float16)
+    n = allpos.size
+    chunk = 512
+    for s in range(0, n, chunk):
+        idx = np.arange(s, min(n, s + chunk))
+        width = ((idx[-1] + 1 + 7) // 8) * 8
+        X = np.zeros((idx.size, width), np.float16)
+        for r, i in enumerate(idx):
+            X[r, : i + 1] = allpos[: i + 1]
+        c, sc = q4.quantize_rows(dev(X))
+        q = orc.unpack_int4(host(c), width).astype(np.int64)
+        a = allpos[idx].astype(np.float32)[:, None]
+        ref = np.rint((np.float32(7.0) * X.astype(np.float32)) / a).astype(np.int64)
+        mask = np.arange(width)[None, :] <= idx[:, None]
+        assert np.array_equal(q[mask], ref[mask]), f"chunk {s}"
+        assert np.array_equal(host(sc), allpos[idx].astype(np.float32) / np.float32(7))
+
+
+def test_prepack_weights_layout(q4):
+    """q4_prepack_weights: int8 row n holds 16*q[n, k] for k in the on-chip unpack order
+    (per 32-k group: the 16 even k, then the 16 odd k) -- checked against the oracle's
+    unpacked codes."""
+    N, K = 96, 512
+    w = synth.random_packed(N, K, "pp", full_range=True)
+    got = host(q4.prepack_weights(dev(w))).astype(np.int64)
+    q = orc.unpack_int4(w, K).astype(np.int64).reshape(N, K // 32, 32)
+    ref = np.concatenate([q[:, :, 0::2], q[:, :, 1::2]], axis=2).reshape(N, K) * 16
+    assert np.array_equal(got, ref)
