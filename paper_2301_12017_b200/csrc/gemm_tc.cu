@@ -22,6 +22,7 @@
 // step and exchange per-row partials (max-abs; shifted LayerNorm moments combined with
 // Chan's formula in rank order) through L2 with a per-m-block arrival counter.  The
 // grid is sized so all CTAs are co-resident (persistent, <= 1 CTA per SM).
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -51,10 +52,20 @@ struct TcParams {
   float* xamax;       // [mblocks][ntn][128] max-abs partials
   unsigned* xcnt;     // [2][mblocks] arrival counters (zeroed before launch)
   int dbg;            // profiling only (env Q4_DEBUG_SKIP): 1 skip TMA, 2 skip unpack, 4 skip MMA, 8 skip epilogue math
+  unsigned long long* trace;  // profiling only (env Q4_TRACE): [grid][64 tiles][8] %globaltimer stamps
 };
+Q4_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
-constexpr int kThreads = 448;
-constexpr int kEpiWarp0 = 6;
+// Epilogue warps per TMEM buffer group: 8 for GELU_Q4 (ALU-heavy), 4 otherwise (more
+// registers per thread for the LayerNorm passes).  Two groups + 6 mainloop warps.
+template <int KIND> struct EpiCfg {
+  static constexpr int EPW = KIND == 2 ? 8 : 4;
+  static constexpr int THREADS = (6 + 2 * EPW) * 32;
+};
 
 // BI8: B (weights) arrives prepacked as int8 "16*q" in the MMA's K order
 // (q4_prepack_weights) and is TMA'd straight into the swizzled operand stage; only the
@@ -68,9 +79,10 @@ struct TcCfg {
   static constexpr int UN_STAGE = A_UN + B_UN, PK_STAGE = A_PK + B_PK;
   static constexpr int OFF_UN = 0;
   static constexpr int OFF_PK = SU * UN_STAGE;
-  static constexpr int OFF_STG = OFF_PK + SP * PK_STAGE;  // 8 warps x 4 KB staging slabs
+  static constexpr int OFF_STG = OFF_PK + SP * PK_STAGE;  // 8 warp pairs x 4 KB staging slabs
   static constexpr int OFF_PRM = OFF_STG + 8 * 4096;      // [4][TN] fp32 column params
-  static constexpr int OFF_BAR = OFF_PRM + 4 * TN * 4;
+  static constexpr int OFF_ROW = OFF_PRM + 4 * TN * 4;    // [2 groups][2 sides][128] float4 row partials
+  static constexpr int OFF_BAR = OFF_ROW + 2 * 2 * 128 * 16;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int HW = TN / 2;  // columns per epilogue group
   static constexpr int TMEM_COLS = 2 * TN <= 64 ? 64 : 2 * TN <= 128 ? 128 : 2 * TN <= 256 ? 256 : 512;
@@ -121,25 +133,26 @@ Q4_DEV void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
 // transform/store so each thread keeps NB shared-memory loads in flight.
 template <int ROWS>
 Q4_DEV void unpack_rows(const uint8_t* __restrict__ pk, uint8_t* __restrict__ un, int t) {
-  constexpr int NCH = ROWS * 4;                   // 16-byte packed chunks
-  constexpr int PER = NCH / 128;                  // chunks per thread
-  constexpr int NB = PER < 8 ? PER : 8;           // batch
-  static_assert(NCH % 128 == 0, "rows");
+  constexpr int PER = ROWS * 4 / 128;  // 16-byte packed chunks per thread
+  static_assert(ROWS * 4 % 128 == 0, "rows");
+  // chunk j of thread t: packed row (t >> 2) + 32 j, 16-byte column c = t & 3.  The swizzle
+  // key (row & 7) does not depend on j, so both destination offsets are loop-invariant.
+  const uint32_t r = (uint32_t)t >> 2, c = (uint32_t)t & 3u, key = r & 7u;
+  const uint32_t src = (uint32_t)t * 16;
+  const uint32_t d0 = r * 128 + (((2 * c) ^ key) << 4), d1 = r * 128 + (((2 * c + 1) ^ key) << 4);
+  constexpr int NB = PER < 8 ? PER : 8;
 #pragma unroll
   for (int b0 = 0; b0 < PER; b0 += NB) {
     uint4 w[NB];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) w[j] = *reinterpret_cast<const uint4*>(pk + (size_t)(t + 128 * (b0 + j)) * 16);
+    for (int j = 0; j < NB; ++j) w[j] = *reinterpret_cast<const uint4*>(pk + src + (b0 + j) * 2048);
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      const uint32_t i = (uint32_t)(t + 128 * (b0 + j));
-      const uint32_t r = i >> 2, c = i & 3u;
       uint4 lo, hi;
       lo.x = nib_lo16(w[j].x); lo.y = nib_lo16(w[j].y); lo.z = nib_lo16(w[j].z); lo.w = nib_lo16(w[j].w);
       hi.x = nib_hi16(w[j].x); hi.y = nib_hi16(w[j].y); hi.z = nib_hi16(w[j].z); hi.w = nib_hi16(w[j].w);
-      uint8_t* row = un + (size_t)r * 128;
-      *reinterpret_cast<uint4*>(row + (((2 * c) ^ (r & 7u)) << 4)) = lo;
-      *reinterpret_cast<uint4*>(row + (((2 * c + 1) ^ (r & 7u)) << 4)) = hi;
+      *reinterpret_cast<uint4*>(un + d0 + (b0 + j) * 4096) = lo;
+      *reinterpret_cast<uint4*>(un + d1 + (b0 + j) * 4096) = hi;
     }
   }
 }
@@ -266,19 +279,43 @@ Q4_DEV void slab_load(uint8_t* stg, const uint8_t* gbase, int row0, int M, size_
 // partial; one thread publishes the arrival (fence + atomic, cumulative over the group's
 // stores via bar.sync), waits for the `ntn` CTAs sharing the m-block, fences again, and
 // the group then reads all partials with L2 (.cg) loads.  Same pattern as a grid sync.
-Q4_DEV void exchange_sync(unsigned* cnt, int ntn, int bar_id, bool leader, int dbg = 0) {
-  named_bar(bar_id, 128);
+Q4_DEV void exchange_sync(unsigned* cnt, int ntn, int bar_id, int nthreads, bool leader, int dbg = 0) {
+  named_bar(bar_id, nthreads);
   if (leader && !(dbg & 32)) {
     __threadfence();
     atomicAdd(cnt, 1u);
     while (ld_acquire_gpu(cnt) < (unsigned)ntn) __nanosleep(32);
     __threadfence();
   }
-  named_bar(bar_id, 128);
+  named_bar(bar_id, nthreads);
+}
+// Partial-slab variant for warps sharing one slab: rows [r0, r0 + nrows).
+Q4_DEV void slab_store16(const uint8_t* stg, uint8_t* gbase, int row0, int r0, int nrows, int M, size_t ldb,
+                         size_t colb, int bytes_per_row, int lane) {
+  const int cpr = bytes_per_row >> 4;
+  const int rows_per_it = 32 / cpr;
+  for (int r = r0 + lane / cpr; r < r0 + nrows; r += rows_per_it) {
+    const int c = lane % cpr;
+    if (row0 + r < M) {
+      const uint4 v = *reinterpret_cast<const uint4*>(stg + slab_off(r, c));
+      *reinterpret_cast<uint4*>(gbase + (size_t)(row0 + r) * ldb + colb + c * 16) = v;
+    }
+  }
+}
+Q4_DEV void slab_load16(uint8_t* stg, const uint8_t* gbase, int row0, int r0, int M, size_t ldb, size_t colb,
+                        int bytes_per_row, int lane) {
+  const int cpr = bytes_per_row >> 4;
+  const int rows_per_it = 32 / cpr;
+  for (int r = r0 + lane / cpr; r < r0 + 16; r += rows_per_it) {
+    const int c = lane % cpr;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row0 + r < M) v = __ldg(reinterpret_cast<const uint4*>(gbase + (size_t)(row0 + r) * ldb + colb + c * 16));
+    *reinterpret_cast<uint4*>(stg + slab_off(r, c)) = v;
+  }
 }
 
 template <int TN, int KIND, bool BI8>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     w4a4_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
   using C = TcCfg<TN, BI8>;
   extern __shared__ uint8_t smem_raw[];
@@ -293,16 +330,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (p.K + C::BK - 1) / C::BK;
+  // Warp roles.  The issue arbiter favours higher warp ids, so the mainloop's critical
+  // path (unpack, TMA producer, MMA issuer) sits above the epilogue warps.
+  constexpr int NE = 2 * EpiCfg<KIND>::EPW;  // epilogue warps 0 .. NE-1
+  constexpr int WU = NE;                     // unpack warps WU .. WU+3
+  constexpr int WP = NE + 4;                 // TMA producer
+  constexpr int WM = NE + 5;                 // MMA issuer (+ TMEM alloc / dealloc)
 
-  if (warp == 0 && lane == 0) {
+  if (warp == WP && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int i = 0; i < C::SP; ++i) { mbar_init(&full_p[i], 1); mbar_init(&empty_p[i], 4); }
     for (int i = 0; i < C::SU; ++i) { mbar_init(&full_u[i], BI8 ? 5 : 4); mbar_init(&empty_u[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EpiCfg<KIND>::EPW); }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == WM) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -310,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   TileIter it(p);
   int mb, nb;
 
-  if (warp == 0) {
+  if (warp == WP) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
       uint32_t g = 0;
@@ -338,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == WM) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_i8(128, TN);
@@ -367,45 +410,65 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp < kEpiWarp0) {
+  } else if (warp >= WU) {
     // ---------------------------------------------------------------- unpack
-    const int t = threadIdx.x - 64;
+    const int t = threadIdx.x - 32 * WU;
     uint32_t g = 0;
+    // profiling only (Q4_TRACE): k-block phase durations of thread 64, trace slot 63 of this CTA
+    unsigned long long* utr = (p.trace && t == 0) ? p.trace + ((size_t)blockIdx.x * 64 + 63) * 8 : nullptr;
     while (it.next(mb, nb)) {
       for (int kb = 0; kb < KB; ++kb, ++g) {
         const int s = g % C::SP, su = g % C::SU;
+        const unsigned long long u0 = utr ? gtimer() : 0;
         mbar_wait(&full_p[s], (g / C::SP) & 1u);
+        const unsigned long long u1 = utr ? gtimer() : 0;
         mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
+        const unsigned long long u2 = utr ? gtimer() : 0;
         const uint8_t* pk = smem + C::OFF_PK + s * C::PK_STAGE;
         uint8_t* un = smem + C::OFF_UN + su * C::UN_STAGE;
         if (!(p.dbg & 2)) {
           unpack_rows<C::BM>(pk, un, t);
           if constexpr (!BI8) unpack_rows<TN>(pk + C::A_PK, un + C::A_UN, t);
         }
+        const unsigned long long u3 = utr ? gtimer() : 0;
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&full_u[su]);
           mbar_arrive(&empty_p[s]);
         }
+        if (utr && g >= 16 && g < 16 + 256) {  // (wait_full, wait_empty, unpack, fence+arrive), 256 k-blocks
+          const unsigned long long u4 = gtimer();
+          utr[0] += u1 - u0; utr[1] += u2 - u1; utr[2] += u3 - u2; utr[3] += u4 - u3; utr[4] += 1;
+        }
       }
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int ew = warp - kEpiWarp0;     // 0..7
-    const int grp = ew >> 2;             // warpgroup: owns TMEM buffer grp (tiles tcount % 2 == grp)
-    const int bar_id = 1 + grp;
-    const bool leader = (ew & 3) == 0 && lane == 0;
-    const int q = warp & 3;              // TMEM lane quarter
-    const int r = q * 32 + lane;         // row within the tile
-    uint8_t* stg = smem + C::OFF_STG + ew * 4096;
+    // 2 groups (group g drains TMEM buffer g: tiles with tcount % 2 == g) x EPW warps.  In
+    // a group, the warp with lane quarter q and side `sub` (EPW = 8: two sides) handles rows
+    // 32q..32q+31 and the 32-column chunks j with j % NS == sub.  The NS warps of a
+    // (group, q) set share a 32-row x 128-byte staging slab, so every 64-column slab leaves as
+    // full 128-byte row segments.
+    constexpr int EPW = EpiCfg<KIND>::EPW;
+    constexpr int NS = EPW / 4;            // sides per lane quarter
+    constexpr int GT = EPW * 32;           // threads per group
+    const int ew = warp;                   // 0 .. 2*EPW-1
+    const int grp = ew / EPW;
+    const int sub = (ew >> 2) % NS;
+    const int q = warp & 3;                // TMEM lane quarter
+    const int r = q * 32 + lane;           // row within the tile
+    const int pair = grp * 4 + q;
+    const int gbar = 1 + grp, pbar = 4 + pair;
+    const bool leader = (ew % EPW) == 0 && lane == 0;
+    uint8_t* stg = smem + C::OFF_STG + pair * 4096;
+    float4* rowp = reinterpret_cast<float4*>(smem + C::OFF_ROW) + grp * 256;  // [2 sides][128]
     const int N = p.N;
     const float clip = p.clip;
-    float* prm = reinterpret_cast<float*>(smem + C::OFF_PRM);  // sw | bias | gamma | beta of this CTA's n-block
-    constexpr int SW = TN < 64 ? TN : 64;  // staging slab width (columns)
+    float* prm = reinterpret_cast<float*>(smem + C::OFF_PRM);  // sw | bias | gamma | beta of this n-block
     {
       const int c0 = (blockIdx.x % p.ntn) * TN;
-      for (int i = ew * 32 + lane; i < TN; i += 256) {
+      for (int i = ew * 32 + lane; i < TN; i += 2 * GT) {
         prm[i] = p.w_scales[c0 + i];
         prm[TN + i] = p.bias ? __half2float(p.bias[c0 + i]) : 0.f;
         if constexpr (KIND == EPI_RESLN_Q4) {
@@ -413,113 +476,149 @@ __global__ void __launch_bounds__(kThreads, 1)
           prm[3 * TN + i] = __half2float(p.beta[c0 + i]);
         }
       }
-      asm volatile("bar.sync 3, 256;" ::: "memory");  // all 8 epilogue warps
+      asm volatile("bar.sync 3, %0;" ::"r"(2 * GT) : "memory");  // all epilogue warps
     }
+    // sync of the NS warps sharing a slab (a warp alone needs only __syncwarp)
+    auto slab_sync = [&]() {
+      if constexpr (NS > 1) named_bar(pbar, 32 * NS); else __syncwarp();
+    };
+    constexpr int NCH = TN / 32;          // 32-column chunks per tile
+    constexpr int NSL = (NCH + 1) / 2;    // 64-column slabs
+    constexpr int RS = 32 / NS;           // slab rows stored by each warp of the set
     uint32_t tcount = 0;
+    unsigned long long* tr = nullptr;
+    auto stamp = [&](int k) {
+      if (tr && leader) tr[k] = gtimer();
+    };
     while (it.next(mb, nb)) {
       const uint32_t b = tcount & 1u;
       if ((int)b != grp) { ++tcount; continue; }
+      tr = (p.trace && tcount < 64) ? p.trace + ((size_t)blockIdx.x * 64 + tcount) * 8 : nullptr;
+      stamp(0);
       const int m0 = mb * C::BM;
       const int gm = m0 + r;
       const bool row_ok = gm < p.M;
-      const int c0 = nb * TN;  // first global column of the tile
+      const int c0 = nb * TN;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + b * TN;
       const float sa = row_ok ? p.a_scales[gm] * (1.0f / 256.0f) : 0.f;
       const float2 sa2 = f2(sa);
+      const uint4* resp = nullptr;
+      if constexpr (KIND == EPI_RESLN_Q4) {
+        // this row's residual chunks: pull them into L2 while the mainloop runs
+        resp = reinterpret_cast<const uint4*>(p.residual + (size_t)(row_ok ? gm : 0) * N + c0);
+        if (row_ok)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(resp), "r"((uint32_t)TN * 2) : "memory");
+      }
       mbar_wait(&tfull[b], (tcount >> 1) & 1u);
       tc_fence_after();
+      stamp(1);
 
       if constexpr (KIND == EPI_I32) {
-        for (int c = 0; c < TN; c += 8) {
-          uint32_t v[8];
-          tmem_ld8(tbase + c, v);
-          tmem_wait_ld();
-          if (row_ok) {
-            int4* o = reinterpret_cast<int4*>(p.out_i32 + (size_t)gm * N + c0 + c);
-            o[0] = make_int4((int)v[0] >> 8, (int)v[1] >> 8, (int)v[2] >> 8, (int)v[3] >> 8);
-            o[1] = make_int4((int)v[4] >> 8, (int)v[5] >> 8, (int)v[6] >> 8, (int)v[7] >> 8);
+        for (int j = sub; j < NCH; j += NS) {
+          for (int c = 32 * j; c < 32 * j + 32; c += 8) {
+            uint32_t v[8];
+            tmem_ld8(tbase + c, v);
+            tmem_wait_ld();
+            if (row_ok) {
+              int4* o = reinterpret_cast<int4*>(p.out_i32 + (size_t)gm * N + c0 + c);
+              o[0] = make_int4((int)v[0] >> 8, (int)v[1] >> 8, (int)v[2] >> 8, (int)v[3] >> 8);
+              o[1] = make_int4((int)v[4] >> 8, (int)v[5] >> 8, (int)v[6] >> 8, (int)v[7] >> 8);
+            }
           }
         }
       } else if constexpr (KIND == EPI_F16) {
-        for (int s0 = 0; s0 < ((p.dbg & 8) ? 0 : TN); s0 += SW) {
+        for (int k = 0; k < ((p.dbg & 8) ? 0 : NSL); ++k) {
 #pragma unroll
-          for (int c = 0; c < SW; c += 32) {
-            uint32_t v[32];
-            tmem_ld32(tbase + s0 + c, v);
-            tmem_wait_ld();
-            uint32_t h[16];
-            dequant32(v, sa2, prm + s0 + c, prm + TN + s0 + c, h);
+          for (int jj = 0; jj < 2; jj += NS) {
+            const int j = 2 * k + jj + sub;
+            if (j < NCH) {
+              uint32_t v[32];
+              tmem_ld32(tbase + 32 * j, v);
+              tmem_wait_ld();
+              uint32_t h[16];
+              dequant32(v, sa2, prm + 32 * j, prm + TN + 32 * j, h);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              *reinterpret_cast<uint4*>(stg + slab_off(lane, c / 8 + k)) =
-                  make_uint4(h[4 * k], h[4 * k + 1], h[4 * k + 2], h[4 * k + 3]);
+              for (int u = 0; u < 4; ++u)
+                *reinterpret_cast<uint4*>(stg + slab_off(lane, (j & 1) * 4 + u)) =
+                    make_uint4(h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
+            }
           }
-          __syncwarp();
-          slab_store(stg, reinterpret_cast<uint8_t*>(p.out_f16), m0 + q * 32, p.M, (size_t)N * 2,
-                     (size_t)(c0 + s0) * 2, SW * 2, lane);
-          __syncwarp();
+          slab_sync();
+          const int cols = TN - 64 * k < 64 ? TN - 64 * k : 64;
+          slab_store16(stg, reinterpret_cast<uint8_t*>(p.out_f16), m0 + q * 32, RS * sub, RS, p.M, (size_t)N * 2,
+                       (size_t)(c0 + 64 * k) * 2, cols * 2, lane);
+          slab_sync();
         }
       } else {
         // ---------------------------------------------------------------- row epilogues
         const int ntn = p.ntn;
         float mean = 0.f, rstd = 0.f;
         if constexpr (KIND == EPI_RESLN_Q4) {
-          // pass 1: z = acc*sa*sw + b + residual -> TMEM (in place); moments shifted by a pivot
+          // pass 1: z = acc*sa*sw + b + residual -> TMEM (in place); moments shifted by a pivot.
+          // The residual goes straight to registers, one chunk ahead of its use.
           float2 s1 = f2(0.f), s2 = f2(0.f), npiv = f2(0.f);
-          for (int s0 = 0; s0 < TN; s0 += SW) {
-            slab_load(stg, reinterpret_cast<const uint8_t*>(p.residual), m0 + q * 32, p.M, (size_t)N * 2,
-                      (size_t)(c0 + s0) * 2, lane);
-            __syncwarp();
+          uint4 rr[4];
 #pragma unroll
-            for (int c = 0; c < SW; c += 32) {
-              uint32_t v[32];
-              tmem_ld32(tbase + s0 + c, v);
-              uint32_t ru[16];
+          for (int u = 0; u < 4; ++u) rr[u] = row_ok ? __ldg(resp + 4 * sub + u) : make_uint4(0, 0, 0, 0);
+          for (int j = sub; j < NCH; j += NS) {
+            uint32_t v[32];
+            tmem_ld32(tbase + 32 * j, v);
+            uint4 rn[4];
+            const bool more = j + NS < NCH;
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint4 x = *reinterpret_cast<const uint4*>(stg + slab_off(lane, c / 8 + k));
-                ru[4 * k] = x.x; ru[4 * k + 1] = x.y; ru[4 * k + 2] = x.z; ru[4 * k + 3] = x.w;
+            for (int u = 0; u < 4; ++u)
+              rn[u] = (more && row_ok) ? __ldg(resp + 4 * (j + NS) + u) : make_uint4(0, 0, 0, 0);
+            const uint32_t ru[16] = {rr[0].x, rr[0].y, rr[0].z, rr[0].w, rr[1].x, rr[1].y, rr[1].z, rr[1].w,
+                                     rr[2].x, rr[2].y, rr[2].z, rr[2].w, rr[3].x, rr[3].y, rr[3].z, rr[3].w};
+            tmem_wait_ld();
+            const float4* pw = reinterpret_cast<const float4*>(prm + 32 * j);
+            const float4* pb = reinterpret_cast<const float4*>(prm + TN + 32 * j);
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const float4 w = pw[jj], bb = pb[jj];
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int e = 4 * jj + 2 * hh;
+                const float2 t = ffma2(fmul2(make_float2((float)(int)v[e], (float)(int)v[e + 1]), sa2),
+                                       hh ? make_float2(w.z, w.w) : make_float2(w.x, w.y),
+                                       hh ? make_float2(bb.z, bb.w) : make_float2(bb.x, bb.y));
+                const float2 z = fadd2(t, unpack_half2(ru[e / 2]));
+                if (j == sub && e == 0) npiv = f2(-z.x);
+                const float2 d = fadd2(z, npiv);
+                s1 = fadd2(s1, d);
+                s2 = ffma2(d, d, s2);
+                v[e] = __float_as_uint(z.x);
+                v[e + 1] = __float_as_uint(z.y);
               }
-              tmem_wait_ld();
-              const float4* pw = reinterpret_cast<const float4*>(prm + s0 + c);
-              const float4* pb = reinterpret_cast<const float4*>(prm + TN + s0 + c);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 w = pw[j], bb = pb[j];
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                  const int e = 4 * j + 2 * hh;
-                  const float2 t = ffma2(fmul2(make_float2((float)(int)v[e], (float)(int)v[e + 1]), sa2),
-                                         hh ? make_float2(w.z, w.w) : make_float2(w.x, w.y),
-                                         hh ? make_float2(bb.z, bb.w) : make_float2(bb.x, bb.y));
-                  const float2 z = fadd2(t, unpack_half2(ru[e / 2]));
-                  if (s0 == 0 && c == 0 && e == 0) npiv = f2(-z.x);
-                  const float2 d = fadd2(z, npiv);
-                  s1 = fadd2(s1, d);
-                  s2 = ffma2(d, d, s2);
-                  v[e] = __float_as_uint(z.x);
-                  v[e + 1] = __float_as_uint(z.y);
-                }
-              }
-              tmem_st32(tbase + s0 + c, v);
             }
-            __syncwarp();
+            tmem_st32(tbase + 32 * j, v);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) rr[u] = rn[u];
           }
           tmem_wait_st();
-          // publish this CTA's (mean, M2) over its TN columns; combine the ntn CTAs (Chan)
+          stamp(2);
           {
-            const float nh = (float)TN;
+            // this side's (mean, M2); combine the sides (Chan), then the ntn CTAs (Chan, rank order)
+            const float nh = (float)(TN / NS);
             const float S1 = s1.x + s1.y, S2 = s2.x + s2.y;
-            const float lmean = -npiv.x + S1 / nh;
-            const float lm2 = fmaxf(S2 - S1 * S1 / nh, 0.f);
-            p.xstat[((size_t)mb * ntn + nb) * 128 + r] = make_float2(lmean, lm2);
-            exchange_sync(p.xcnt + mb, ntn, bar_id, leader, p.dbg);
+            float cm = -npiv.x + S1 / nh, cm2 = fmaxf(S2 - S1 * S1 / nh, 0.f);
+            if constexpr (NS > 1) {
+              rowp[sub * 128 + r] = make_float4(cm, cm2, 0.f, 0.f);
+              named_bar(gbar, GT);
+              const float4 a0 = rowp[r], a1 = rowp[128 + r];
+              const float d = a1.x - a0.x;
+              cm = a0.x + 0.5f * d;
+              cm2 = a0.y + a1.y + d * d * (nh * 0.5f);
+            }
+            if (sub == 0) p.xstat[((size_t)mb * ntn + nb) * 128 + r] = make_float2(cm, cm2);
+            exchange_sync(p.xcnt + mb, ntn, gbar, GT, leader, p.dbg);
+            stamp(3);
             float2 st = __ldcg(&p.xstat[((size_t)mb * ntn) * 128 + r]);
             float cnt = (float)TN;
             mean = st.x;
             float m2 = st.y;
-            for (int k = 1; k < ntn; ++k) {
-              const float2 o = __ldcg(&p.xstat[((size_t)mb * ntn + k) * 128 + r]);
+            for (int kk = 1; kk < ntn; ++kk) {
+              const float2 o = __ldcg(&p.xstat[((size_t)mb * ntn + kk) * 128 + r]);
               const float tot = cnt + (float)TN;
               const float dd = o.x - mean;
               mean = fmaf(dd, (float)TN / tot, mean);
@@ -533,85 +632,93 @@ __global__ void __launch_bounds__(kThreads, 1)
         __half2 hmax = __float2half2_rn(0.f);
         const bool want_f16 = p.out_f16 != nullptr;
         const float2 nmean2 = f2(-mean), rstd2 = f2(rstd);
-        for (int s0 = 0; s0 < TN; s0 += SW) {
+        for (int k = 0; k < NSL; ++k) {
 #pragma unroll
-          for (int c = 0; c < SW; c += 32) {
+          for (int jj = 0; jj < 2; jj += NS) {
+            const int j = 2 * k + jj + sub;
             uint32_t v[32];
-            tmem_ld32(tbase + s0 + c, v);
+            tmem_ld32(tbase + 32 * j, v);
             tmem_wait_ld();
             uint32_t h[16];
             if constexpr (KIND == EPI_RESLN_Q4) {
-              const float4* pg = reinterpret_cast<const float4*>(prm + 2 * TN + s0 + c);
-              const float4* pe = reinterpret_cast<const float4*>(prm + 3 * TN + s0 + c);
+              const float4* pg = reinterpret_cast<const float4*>(prm + 2 * TN + 32 * j);
+              const float4* pe = reinterpret_cast<const float4*>(prm + 3 * TN + 32 * j);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 g4 = pg[j], e4 = pe[j];
-                const float2 z0 = make_float2(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]));
-                const float2 z1 = make_float2(__uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+              for (int i4 = 0; i4 < 8; ++i4) {
+                const float4 g4 = pg[i4], e4 = pe[i4];
+                const float2 z0 = make_float2(__uint_as_float(v[4 * i4]), __uint_as_float(v[4 * i4 + 1]));
+                const float2 z1 = make_float2(__uint_as_float(v[4 * i4 + 2]), __uint_as_float(v[4 * i4 + 3]));
                 const float2 y0 = ffma2(fmul2(fadd2(z0, nmean2), rstd2), make_float2(g4.x, g4.y), make_float2(e4.x, e4.y));
                 const float2 y1 = ffma2(fmul2(fadd2(z1, nmean2), rstd2), make_float2(g4.z, g4.w), make_float2(e4.z, e4.w));
-                h[2 * j] = pack_half2(y0.x, y0.y);
-                h[2 * j + 1] = pack_half2(y1.x, y1.y);
+                h[2 * i4] = pack_half2(y0.x, y0.y);
+                h[2 * i4 + 1] = pack_half2(y1.x, y1.y);
               }
             } else {
-              uint32_t tq[16];
-              dequant32(v, sa2, prm + s0 + c, prm + TN + s0 + c, tq, true);
-#pragma unroll
-              for (int j = 0; j < 16; ++j) h[j] = tq[j];
+              dequant32(v, sa2, prm + 32 * j, prm + TN + 32 * j, h, true);
             }
             if (clip > 0.f) {
               const __half2 cl = __float2half2_rn(clip);
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                hmax = __hmax2(hmax, __hmin2(__habs2(*reinterpret_cast<const __half2*>(&h[j])), cl));
+              for (int u = 0; u < 16; ++u)
+                hmax = __hmax2(hmax, __hmin2(__habs2(*reinterpret_cast<const __half2*>(&h[u])), cl));
             } else {
 #pragma unroll
-              for (int j = 0; j < 16; ++j) hmax = __hmax2(hmax, __habs2(*reinterpret_cast<const __half2*>(&h[j])));
+              for (int u = 0; u < 16; ++u) hmax = __hmax2(hmax, __habs2(*reinterpret_cast<const __half2*>(&h[u])));
             }
-            tmem_st16(tbase + s0 + c, h);
+            tmem_st16(tbase + 32 * j, h);
             if (want_f16) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                *reinterpret_cast<uint4*>(stg + slab_off(lane, c / 8 + k)) =
-                    make_uint4(h[4 * k], h[4 * k + 1], h[4 * k + 2], h[4 * k + 3]);
+              for (int u = 0; u < 4; ++u)
+                *reinterpret_cast<uint4*>(stg + slab_off(lane, (j & 1) * 4 + u)) =
+                    make_uint4(h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
             }
           }
           if (want_f16) {
-            __syncwarp();
-            slab_store(stg, reinterpret_cast<uint8_t*>(p.out_f16), m0 + q * 32, p.M, (size_t)N * 2,
-                       (size_t)(c0 + s0) * 2, SW * 2, lane);
-            __syncwarp();
+            slab_sync();
+            slab_store16(stg, reinterpret_cast<uint8_t*>(p.out_f16), m0 + q * 32, RS * sub, RS, p.M, (size_t)N * 2,
+                         (size_t)(c0 + 64 * k) * 2, 128, lane);
+            slab_sync();
           }
         }
         tmem_wait_st();
+        stamp(4);
         float amax = fmaxf(__low2float(hmax), __high2float(hmax));
-        // row max-abs over the ntn CTAs
-        p.xamax[((size_t)mb * ntn + nb) * 128 + r] = amax;
-        exchange_sync(p.xcnt + p.mblocks + mb, ntn, bar_id, leader, p.dbg);
-        for (int k = 0; k < ntn; ++k) amax = fmaxf(amax, __ldcg(&p.xamax[((size_t)mb * ntn + k) * 128 + r]));
+        // row max-abs over the sides, then the ntn CTAs
+        if constexpr (NS > 1) {
+          rowp[sub * 128 + r].z = amax;
+          named_bar(gbar, GT);
+          amax = fmaxf(rowp[r].z, rowp[128 + r].z);
+        }
+        if (sub == 0) p.xamax[((size_t)mb * ntn + nb) * 128 + r] = amax;
+        exchange_sync(p.xcnt + p.mblocks + mb, ntn, gbar, GT, leader, p.dbg);
+        stamp(5);
+        for (int kk = 0; kk < ntn; ++kk) amax = fmaxf(amax, __ldcg(&p.xamax[((size_t)mb * ntn + kk) * 128 + r]));
         // pass B: codes (R1-R3), packed, staged, coalesced stores
         const float r7 = amax > 0.f ? __fdiv_rn(7.0f, amax) : 0.f;
-        for (int s0 = 0; s0 < TN; s0 += SW) {
+        for (int k = 0; k < NSL; ++k) {
 #pragma unroll
-          for (int c = 0; c < SW; c += 32) {
+          for (int jj = 0; jj < 2; jj += NS) {
+            const int j = 2 * k + jj + sub;
             uint32_t h[16];
-            tmem_ld16(tbase + s0 + c, h);
+            tmem_ld16(tbase + 32 * j, h);
             tmem_wait_ld();
             uint32_t w[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t hk[4] = {h[4 * k], h[4 * k + 1], h[4 * k + 2], h[4 * k + 3]};
-              w[k] = requant8(hk, amax, r7, clip);
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t hk[4] = {h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]};
+              w[u] = requant8(hk, amax, r7, clip);
             }
-            // 32 codes = 16 bytes = slab chunk c/32 of this row (a 64-column slab row holds 32 B)
-            *reinterpret_cast<uint4*>(stg + slab_off(lane, c / 32)) = make_uint4(w[0], w[1], w[2], w[3]);
+            // 32 codes = 16 bytes: chunk (j & 1) of the slab row (a 64-column slab row = 32 code bytes)
+            *reinterpret_cast<uint4*>(stg + slab_off(lane, j & 1)) = make_uint4(w[0], w[1], w[2], w[3]);
           }
-          __syncwarp();
-          slab_store(stg, p.out_codes, m0 + q * 32, p.M, (size_t)N / 2, (size_t)(c0 + s0) / 2, SW / 2, lane);
-          __syncwarp();
+          slab_sync();
+          slab_store16(stg, p.out_codes, m0 + q * 32, RS * sub, RS, p.M, (size_t)N / 2, (size_t)(c0 + 64 * k) / 2, 32,
+                       lane);
+          slab_sync();
         }
-        if (row_ok && nb == 0) p.out_scales[gm] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
+        if (row_ok && nb == 0 && sub == 0) p.out_scales[gm] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
       }
+      stamp(6);
       // accumulator buffer b may be overwritten by the MMA of tile tcount + 2
       tc_fence_before();
       __syncwarp();
@@ -622,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (warp == WM) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
 // ====================================================================== host side
@@ -702,6 +809,14 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.xstat = nullptr; p.xamax = nullptr; p.xcnt = nullptr;
   static const int dbg = [] { const char* e = getenv("Q4_DEBUG_SKIP"); return e ? atoi(e) : 0; }();
   p.dbg = dbg;
+  p.trace = nullptr;
+  static const char* trace_path = getenv("Q4_TRACE");
+  static unsigned long long* trace_buf = nullptr;
+  if (trace_path) {
+    if (!trace_buf) cudaMalloc(&trace_buf, sizeof(unsigned long long) * 148 * 64 * 8);
+    cudaMemsetAsync(trace_buf, 0, sizeof(unsigned long long) * 148 * 64 * 8, s);
+    p.trace = trace_buf;
+  }
   const int sms = num_sms();
   // groups of ntn co-resident CTAs (one per SM); a group walks the m-blocks
   if (p.ntn > sms) { *why = "N/TN exceeds the number of SMs"; return cudaErrorNotSupported; }
@@ -720,7 +835,18 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     if (e != cudaSuccess) return e;
   }
   note_launch();
-  kern<<<grid, kThreads, C::SMEM, s>>>(ta, tb, p);
+  kern<<<grid, EpiCfg<KIND>::THREADS, C::SMEM, s>>>(ta, tb, p);
+  if (trace_path) {  // profiling only: dump the stamps of this launch (synchronous)
+    static unsigned long long host[148 * 64 * 8];
+    cudaMemcpy(host, trace_buf, sizeof(host), cudaMemcpyDeviceToHost);
+    FILE* f = fopen(trace_path, "ab");
+    if (f) {
+      const int hdr[4] = {grid, KIND, TN, g.M};
+      fwrite(hdr, sizeof(hdr), 1, f);
+      fwrite(host, sizeof(host), 1, f);
+      fclose(f);
+    }
+  }
   return cudaGetLastError();
 }
 

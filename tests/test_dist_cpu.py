@@ -1,0 +1,64 @@
+"""Multi-process host logic of the batch-sharded path (gloo, world_size 2, CPU)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2301_12017_b200 import dist as qd
+from paper_2301_12017_b200 import synth
+
+
+def test_shard_partitions_the_batch():
+    for gb in (1, 7, 256, 1000):
+        for w in (1, 2, 3, 4, 8):
+            got = [qd.shard(gb, r, w) for r in range(w)]
+            assert sum(c for _, c in got) == gb
+            assert all(got[i][0] + got[i][1] == got[i + 1][0] for i in range(w - 1))
+            assert max(c for _, c in got) - min(c for _, c in got) <= 1
+    with pytest.raises(ValueError):
+        qd.shard(8, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r, w, _ = qd.env_ranks()
+        start, count = qd.shard(6, r, w)
+        # each rank generates only its own sequences; seeds are per sequence
+        x = np.concatenate([synth.hidden(16, 64, "input", b) for b in range(start, start + count)])
+        qd.barrier()
+        m = qd.max_over_ranks(10.0 * (r + 1))
+        q.put((r, start, count, x, m))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_shards_and_max():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = np.concatenate([synth.hidden(16, 64, "input", b) for b in range(6)])
+    got = np.concatenate([x for _, _, _, x, _ in res])
+    assert np.array_equal(got, full)  # shards reassemble the single-rank global batch
+    assert all(m == 20.0 for *_, m in res)  # max over ranks seen by every rank
+    assert [(s, c) for _, s, c, _, _ in res] == [(0, 3), (3, 3)]
