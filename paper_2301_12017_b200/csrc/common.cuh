@@ -59,6 +59,31 @@ Q4_DEV void tma_load_2d(void* smem_dst, const void* tmap, uint64_t* bar, int32_t
       : "memory");
 }
 
+// Same, with an L2 cache-policy hint (policy from l2_policy_evict_*).
+Q4_DEV void tma_load_2d_hint(void* smem_dst, const void* tmap, uint64_t* bar, int32_t c0, int32_t c1,
+                             uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+Q4_DEV uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+Q4_DEV uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+Q4_DEV void st_global_hint(void* ptr, uint4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w), "l"(policy)
+               : "memory");
+}
+
 // ------------------------------------------------------------------ cluster
 Q4_DEV uint32_t cluster_ctarank() {
   uint32_t r;
@@ -293,6 +318,42 @@ Q4_DEV float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// (p.x - h.lo, p.y - h.hi) with the fp16 halves of h taken as exact f32 (FHFMA: f16*f16+f32,
+// one rounding -> exact when h = fp16(p)).
+Q4_DEV float2 sub_half2_f32(uint32_t h, float2 p) {
+  float2 d;
+  asm("{.reg .f16 a, b, m;\n\tmov.b32 {a, b}, %2;\n\tmov.b16 m, 0xBC00;\n\t"
+      "fma.rn.f32.f16 %0, a, m, %3;\n\tfma.rn.f32.f16 %1, b, m, %4;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "r"(h), "f"(p.x), "f"(p.y));
+  return d;
+}
+Q4_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+// requant8(h, amax, r7, 0) with packed fp32x2 arithmetic, for amax > 0 and |y| <= amax,
+// split into a branch-free stage and a rare fix-up so several words can be in flight.
+// s = p + 1.5*2^23 holds round-half-even(p) = n in [-7, 7] as bits 0x4B400000 + n, so the
+// low byte of s is n in two's complement: gather the 8 low bytes with PRMT and merge the
+// nibbles (even elements low, odd high) instead of subtracting and packing per element.
+// Returns the packed word; dmax collects max |p - rint(p)| (> 0.499998: use requant8).
+Q4_DEV uint32_t requant8_nofix(const uint32_t (&h)[4], float r7, float& dmax) {
+  uint32_t sb[8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 p = fmul2(unpack_half2(h[j]), f2(r7));
+    const float2 sm = fadd2(p, f2(12582912.0f));
+    const float2 d = ffma2(fadd2(sm, f2(-12582912.0f)), f2(-1.f), p);  // exact p - rint(p)
+    dmax = fmaxf(dmax, fmaxf(fabsf(d.x), fabsf(d.y)));
+    sb[2 * j] = __float_as_uint(sm.x);
+    sb[2 * j + 1] = __float_as_uint(sm.y);
+  }
+  const uint32_t ev = prmt(prmt(sb[0], sb[2], 0x40u), prmt(sb[4], sb[6], 0x40u), 0x5410u);
+  const uint32_t od = prmt(prmt(sb[1], sb[3], 0x40u), prmt(sb[5], sb[7], 0x40u), 0x5410u);
+  return (ev & 0x0F0F0F0Fu) | ((od << 4) & 0xF0F0F0F0u);
 }
 
 // GELU (erf form, reading R11) for two values, ~13 ops/element, |err| <= 3e-6 vs fp64:

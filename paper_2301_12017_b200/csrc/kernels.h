@@ -42,5 +42,7 @@ size_t tc_workspace_bytes(int M, int N, int TN);
 cudaError_t launch_w4a4_legacy(const GemmArgs& g, bool s4, cudaStream_t s, const char** why);
 cudaError_t launch_attention(const __half* qkv, int B, int S, int heads, __half* ctx_f16,
                              uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s);
+cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __half* ctx_f16,
+                                uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s);
 
 }  // namespace q4

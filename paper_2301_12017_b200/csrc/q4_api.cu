@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/q4.h"
@@ -173,8 +174,11 @@ q4_status q4_attention_f16_q4(const uint16_t* qkv, int64_t B, int64_t S, int32_t
     return fail(Q4_EINVAL, "q4_attention_f16_q4: NULL qkv/ctx_f16/ctx_codes/ctx_scales");
   if (!al16(qkv) || !al4(ctx_codes) || !al16(ctx_f16))
     return fail(Q4_EALIGN, "q4_attention_f16_q4: qkv/ctx_f16 must be 16-byte aligned, codes 4-byte");
-  cudaError_t e = q4::launch_attention(reinterpret_cast<const __half*>(qkv), (int)B, (int)S, heads,
-                                       reinterpret_cast<__half*>(ctx_f16), ctx_codes, ctx_scales, (cudaStream_t)stream);
+  // tcgen05 kernel by default; the mma.sync kernel stays as the measured baseline (Q4_ATTN_LEGACY=1)
+  static const bool legacy = [] { const char* e = getenv("Q4_ATTN_LEGACY"); return e && atoi(e) != 0; }();
+  cudaError_t e = (legacy ? q4::launch_attention : q4::launch_attention_tc)(
+      reinterpret_cast<const __half*>(qkv), (int)B, (int)S, heads, reinterpret_cast<__half*>(ctx_f16), ctx_codes,
+      ctx_scales, (cudaStream_t)stream);
   return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_attention_f16_q4");
 }
 
