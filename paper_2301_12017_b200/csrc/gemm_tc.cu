@@ -157,6 +157,30 @@ Q4_DEV void unpack_rows(const uint8_t* __restrict__ pk, uint8_t* __restrict__ un
   }
 }
 
+// 32 codes (4 packed words) from 16 words of halves.  Unclipped rows take the batched
+// fast path (one tie check for all 32 values); clipped rows or near-ties use requant8.
+Q4_DEV uint4 requant32(const uint32_t (&h)[16], float amax, float r7, float clip) {
+  uint32_t w[4];
+  bool exact = clip > 0.f || !(amax > 0.f);
+  if (!exact) {
+    float dmax = 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t hk[4] = {h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]};
+      w[u] = requant8_nofix(hk, r7, dmax);
+    }
+    exact = dmax > 0.499998f;
+  }
+  if (exact) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t hk[4] = {h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]};
+      w[u] = requant8(hk, amax, r7, clip);
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 // Per-column epilogue parameters for 16 consecutive columns (broadcast loads: every lane
 // of the warp reads the same addresses).
 Q4_DEV void load_col_params(const float* ws, const __half* bias, float2 (&w)[8], float2 (&b)[8]) {
@@ -702,14 +726,9 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
             uint32_t h[16];
             tmem_ld16(tbase + 32 * j, h);
             tmem_wait_ld();
-            uint32_t w[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const uint32_t hk[4] = {h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]};
-              w[u] = requant8(hk, amax, r7, clip);
-            }
+            const uint4 wq = requant32(h, amax, r7, clip);
             // 32 codes = 16 bytes: chunk (j & 1) of the slab row (a 64-column slab row = 32 code bytes)
-            *reinterpret_cast<uint4*>(stg + slab_off(lane, j & 1)) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4*>(stg + slab_off(lane, j & 1)) = wq;
           }
           slab_sync();
           slab_store16(stg, p.out_codes, m0 + q * 32, RS * sub, RS, p.M, (size_t)N / 2, (size_t)(c0 + 64 * k) / 2, 32,
@@ -873,7 +892,8 @@ int tc_tile_n(int M, int N, int kind) {
   // Small M (latency configs): narrower tiles spread the work over more SMs.  Row
   // epilogues need >= 64 columns per tile (>= 16 code bytes per row per half).
   const bool row = kind == EPI_GELU_Q4 || kind == EPI_RESLN_Q4;
-  const int pref = M <= 512 ? 64 : 256;
+  static const int env_tn = getenv("Q4_TN") ? atoi(getenv("Q4_TN")) : 0;  // profiling only
+  const int pref = env_tn ? env_tn : M <= 512 ? 64 : 256;
   static const int cand[] = {256, 128, 64, 32};
   for (int c : cand)
     if (c <= pref && N % c == 0 && !(row && c < 64)) return c;

@@ -1,0 +1,31 @@
+"""Fit of the GELU tail polynomial used by gelu2() in csrc/common.cuh (offline tooling;
+not part of the product path).  GELU(x) = max(x,0) - |x| Q(|x|), Q(t) = exp(-t^2/2) R(t),
+R(v) a degree-8 polynomial in v = 2.75 - min(t, 5.5).  Weighted least squares on the GELU
+error, reweighted towards minimax; prints the coefficients and the max |error| of the
+float32 evaluation order the kernel uses against the fp64 erf form."""
+import numpy as np
+from scipy.special import erfc
+
+HI, DEG = 5.5, 8
+t = np.linspace(0, HI, 200001)
+R = 0.5 * erfc(t / np.sqrt(2)) * np.exp(t * t / 2)
+V = np.vander(HI / 2 - t, DEG + 1)
+w = t * np.exp(-t * t / 2) + 2e-3
+c, *_ = np.linalg.lstsq(V * w[:, None], R * w, rcond=None)
+for _ in range(30):
+    e = np.abs((V @ c - R) * t * np.exp(-t * t / 2))
+    w2 = w * (1 + 50 * e / e.max())
+    c, *_ = np.linalg.lstsq(V * w2[:, None], R * w2, rcond=None)
+c32 = c.astype(np.float32)
+x = np.linspace(-8, 8, 400001).astype(np.float32)
+tn = np.maximum(-np.abs(x), np.float32(-HI))
+v = (tn + np.float32(HI / 2)).astype(np.float32)
+r = np.full_like(v, c32[0])
+for ci in c32[1:]:
+    r = (r * v + ci).astype(np.float32)
+ea = ((tn * tn).astype(np.float32) * np.float32(-0.72134752044448170)).astype(np.float32)
+q = (np.exp2(ea.astype(np.float64)).astype(np.float32) * r).astype(np.float32)
+y = (tn * q + np.maximum(x, 0)).astype(np.float32)
+xd = x.astype(np.float64)
+print("coefficients (highest degree first):", ", ".join(f"{float(ci):.9e}f" for ci in c32))
+print("max |GELU error| (float32 evaluation):", float(np.max(np.abs(y - xd * 0.5 * erfc(-xd / np.sqrt(2))))))
