@@ -329,6 +329,16 @@ Q4_DEV float2 sub_half2_f32(uint32_t h, float2 p) {
       : "r"(h), "f"(p.x), "f"(p.y));
   return d;
 }
+// (p.x + h.lo, p.y + h.hi) with the fp16 halves of h taken as exact f32 (FHFMA h*1+p:
+// one rounding, the same result as converting h and adding).
+Q4_DEV float2 add_half2_f32(uint32_t h, float2 p) {
+  float2 d;
+  asm("{.reg .f16 a, b, m;\n\tmov.b32 {a, b}, %2;\n\tmov.b16 m, 0x3C00;\n\t"
+      "fma.rn.f32.f16 %0, a, m, %3;\n\tfma.rn.f32.f16 %1, b, m, %4;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "r"(h), "f"(p.x), "f"(p.y));
+  return d;
+}
 Q4_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t d;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));

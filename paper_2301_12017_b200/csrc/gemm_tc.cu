@@ -60,11 +60,18 @@ Q4_DEV unsigned long long gtimer() {
   return t;
 }
 
-// Epilogue warps per TMEM buffer group: 8 for GELU_Q4 (ALU-heavy), 4 otherwise (more
-// registers per thread for the LayerNorm passes).  Two groups + 6 mainloop warps.
+// Epilogue warps per TMEM buffer group: 4 for I32 / F16 (two groups + 6 mainloop warps).
+// Row epilogues (GELU_Q4 / RESLN_Q4) run 8 warps per group.  RESLN_Q4 (register-heavy
+// LayerNorm passes) rebalances registers with setmaxnreg: the 6 mainloop warps (+2 idle,
+// so they form two aligned warpgroups) drop to
+// MAINLOOP_REGS and the 16 epilogue warps rise to EPI_REGS.  The pool is what the CTA was
+// launched with (768 threads x 80 = 61440): 8 x 48 + 16 x 96 = 1920 warp-registers x 32.
 template <int KIND> struct EpiCfg {
-  static constexpr int EPW = KIND == 2 ? 8 : 4;
-  static constexpr int THREADS = (6 + 2 * EPW) * 32;
+  static constexpr bool ROW = KIND == 2 || KIND == 3;
+  static constexpr int EPW = ROW ? 8 : 4;
+  static constexpr int PAD = KIND == 3 ? 2 : 0;  // idle warps completing the mainloop warpgroup
+  static constexpr int THREADS = (6 + PAD + 2 * EPW) * 32;
+  static constexpr int MAINLOOP_REGS = 48, EPI_REGS = 96;
 };
 
 // BI8: B (weights) arrives prepacked as int8 "16*q" in the MMA's K order
@@ -377,6 +384,11 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
   TileIter it(p);
   int mb, nb;
 
+  // Register rebalancing (row epilogues): one setmaxnreg per side, executed by whole
+  // warpgroups at a single call site that dominates that side's code.
+  if (warp >= NE) {
+  if constexpr (EpiCfg<KIND>::PAD > 0)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(EpiCfg<KIND>::MAINLOOP_REGS));
   if (warp == WP) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
@@ -410,14 +422,21 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_i8(128, TN);
       uint32_t g = 0, tcount = 0;
+      // profiling only (Q4_TRACE): per-tile (wait tempty, wait full_u total, issue span), slot 62
+      unsigned long long* mtr = p.trace ? p.trace + ((size_t)blockIdx.x * 64 + 62) * 8 : nullptr;
       while (it.next(mb, nb)) {
         const uint32_t b = tcount & 1u;
+        const unsigned long long m0 = mtr ? gtimer() : 0;
         mbar_wait(&tempty[b], ((tcount >> 1) & 1u) ^ 1u);
         tc_fence_after();
+        const unsigned long long m1 = mtr ? gtimer() : 0;
+        unsigned long long mw = 0;
         const uint32_t dt = tmem + b * TN;
         for (int kb = 0; kb < KB; ++kb, ++g) {
           const int su = g % C::SU;
+          const unsigned long long w0 = mtr ? gtimer() : 0;
           mbar_wait(&full_u[su], (g / C::SU) & 1u);
+          if (mtr) mw += gtimer() - w0;
           tc_fence_after();
           const uint32_t ua = smem_u32(smem + C::OFF_UN + su * C::UN_STAGE);
           const uint32_t ub = ua + C::A_UN;
@@ -430,11 +449,17 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
           umma_commit(&empty_u[su]);
         }
         umma_commit(&tfull[b]);
+        if (mtr && tcount >= 2) {
+          const unsigned long long m2 = gtimer();
+          mtr[0] += m1 - m0; mtr[1] += mw; mtr[2] += m2 - m1; mtr[3] += 1;
+        }
         ++tcount;
       }
     }
     __syncwarp();
-  } else if (warp >= WU) {
+  } else if (warp > WM) {
+    // idle (register donors completing the mainloop warpgroup)
+  } else {
     // ---------------------------------------------------------------- unpack
     const int t = threadIdx.x - 32 * WU;
     uint32_t g = 0;
@@ -467,8 +492,11 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
         }
       }
     }
+  }
   } else {
     // ---------------------------------------------------------------- epilogue
+    if constexpr (EpiCfg<KIND>::PAD > 0)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EpiCfg<KIND>::EPI_REGS));
     // 2 groups (group g drains TMEM buffer g: tiles with tcount % 2 == g) x EPW warps.  In
     // a group, the warp with lane quarter q and side `sub` (EPW = 8: two sides) handles rows
     // 32q..32q+31 and the 32-column chunks j with j % NS == sub.  The NS warps of a
@@ -527,11 +555,14 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
       const float sa = row_ok ? p.a_scales[gm] * (1.0f / 256.0f) : 0.f;
       const float2 sa2 = f2(sa);
       const uint4* resp = nullptr;
+      uint4 rr[4];  // RESLN: residual of this thread's current chunk (first one loaded before the wait)
       if constexpr (KIND == EPI_RESLN_Q4) {
         // this row's residual chunks: pull them into L2 while the mainloop runs
         resp = reinterpret_cast<const uint4*>(p.residual + (size_t)(row_ok ? gm : 0) * N + c0);
         if (row_ok)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(resp), "r"((uint32_t)TN * 2) : "memory");
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rr[u] = (row_ok && !(p.dbg & 64)) ? __ldg(resp + 4 * sub + u) : make_uint4(0, 0, 0, 0);
       }
       mbar_wait(&tfull[b], (tcount >> 1) & 1u);
       tc_fence_after();
@@ -576,14 +607,12 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
       } else {
         // ---------------------------------------------------------------- row epilogues
         const int ntn = p.ntn;
+        const float inv_ntn = 1.0f / (float)ntn;
         float mean = 0.f, rstd = 0.f;
         if constexpr (KIND == EPI_RESLN_Q4) {
           // pass 1: z = acc*sa*sw + b + residual -> TMEM (in place); moments shifted by a pivot.
           // The residual goes straight to registers, one chunk ahead of its use.
           float2 s1 = f2(0.f), s2 = f2(0.f), npiv = f2(0.f);
-          uint4 rr[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) rr[u] = row_ok ? __ldg(resp + 4 * sub + u) : make_uint4(0, 0, 0, 0);
           for (int j = sub; j < NCH; j += NS) {
             uint32_t v[32];
             tmem_ld32(tbase + 32 * j, v);
@@ -591,7 +620,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
             const bool more = j + NS < NCH;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              rn[u] = (more && row_ok) ? __ldg(resp + 4 * (j + NS) + u) : make_uint4(0, 0, 0, 0);
+              rn[u] = (more && row_ok && !(p.dbg & 64)) ? __ldg(resp + 4 * (j + NS) + u) : make_uint4(0, 0, 0, 0);
             const uint32_t ru[16] = {rr[0].x, rr[0].y, rr[0].z, rr[0].w, rr[1].x, rr[1].y, rr[1].z, rr[1].w,
                                      rr[2].x, rr[2].y, rr[2].z, rr[2].w, rr[3].x, rr[3].y, rr[3].z, rr[3].w};
             tmem_wait_ld();
@@ -606,7 +635,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
                 const float2 t = ffma2(fmul2(make_float2((float)(int)v[e], (float)(int)v[e + 1]), sa2),
                                        hh ? make_float2(w.z, w.w) : make_float2(w.x, w.y),
                                        hh ? make_float2(bb.z, bb.w) : make_float2(bb.x, bb.y));
-                const float2 z = fadd2(t, unpack_half2(ru[e / 2]));
+                const float2 z = add_half2_f32(ru[e / 2], t);
                 if (j == sub && e == 0) npiv = f2(-z.x);
                 const float2 d = fadd2(z, npiv);
                 s1 = fadd2(s1, d);
@@ -637,18 +666,23 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
             if (sub == 0) p.xstat[((size_t)mb * ntn + nb) * 128 + r] = make_float2(cm, cm2);
             exchange_sync(p.xcnt + mb, ntn, gbar, GT, leader, p.dbg);
             stamp(3);
-            float2 st = __ldcg(&p.xstat[((size_t)mb * ntn) * 128 + r]);
-            float cnt = (float)TN;
-            mean = st.x;
-            float m2 = st.y;
-            for (int kk = 1; kk < ntn; ++kk) {
-              const float2 o = __ldcg(&p.xstat[((size_t)mb * ntn + kk) * 128 + r]);
-              const float tot = cnt + (float)TN;
-              const float dd = o.x - mean;
-              mean = fmaf(dd, (float)TN / tot, mean);
-              m2 = m2 + o.y + dd * dd * (cnt * (float)TN / tot);
-              cnt = tot;
+            // every partial covers TN columns: mean = average of the means, M2 = sum of the M2s
+            // + TN * sum of squared deviations of the means
+            const float2* xs = p.xstat + ((size_t)mb * ntn) * 128 + r;
+            float msum = 0.f, m2 = 0.f;
+            for (int kk = 0; kk < ntn; ++kk) {
+              const float2 o = __ldcg(xs + (size_t)kk * 128);
+              msum += o.x;
+              m2 += o.y;
             }
+            mean = msum * inv_ntn;
+            float dev = 0.f;
+            for (int kk = 0; kk < ntn; ++kk) {
+              const float dd = __ldcg(xs + (size_t)kk * 128).x - mean;
+              dev = fmaf(dd, dd, dev);
+            }
+            m2 = fmaf((float)TN, dev, m2);
+            const float cnt = (float)(TN * ntn);
             rstd = 1.0f / sqrtf(m2 / cnt + p.ln_eps);
           }
         }

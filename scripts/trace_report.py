@@ -36,3 +36,12 @@ for i in range(len(raw) // rec):
     if ok.sum():
         m = (u[ok, :4] / n[ok, None]).mean(0)
         print(f"  unpack per k-block (ns): wait_full_p={m[0]:.0f} wait_empty_u={m[1]:.0f} unpack={m[2]:.0f} fence+arrive={m[3]:.0f}")
+
+# MMA issuer stamps (slot 62): per tile means (us)
+for i in range(len(raw) // rec):
+    t = np.frombuffer(raw[i * rec + 16:(i + 1) * rec], np.uint64).reshape(148, 64, 8).astype(np.float64)
+    u = t[:, 62, :]
+    ok = u[:, 3] > 0
+    if ok.sum():
+        m = (u[ok, :3] / u[ok, 3:4]).mean(0) / 1e3
+        print(f"  mma per tile (us): wait_tempty={m[0]:.2f} wait_full_u={m[1]:.2f} issue_span={m[2]:.2f}")
