@@ -67,7 +67,7 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
 __global__ void __launch_bounds__(AT_THREADS, 2)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tq, int S, int heads, __half* __restrict__ ctx_f16,
                         uint8_t* __restrict__ ctx_codes, float* __restrict__ ctx_scales,
-                        unsigned long long* __restrict__ trace, int dbg) {
+                        unsigned long long* __restrict__ trace, int dbg, int G) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* kv_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -79,7 +79,9 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = heads * 64;
-  const int b = blockIdx.x;
+  // G CTAs (one cluster) per sequence, each running hpc = heads / G consecutive heads
+  const int b = blockIdx.x / G, g = blockIdx.x % G;
+  const int hpc = heads / G, j0 = g * hpc;
   const int row0 = b * S;  // first token of this sequence
 
   if (warp == 8 && lane == 0) {
@@ -101,9 +103,9 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
     // ---------------------------------------------------------------- producer
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
-      for (int j = 0; j < heads; ++j) {
-        const int st = j % NST;
-        mbar_wait(&kv_empty[st], ((j / NST) & 1u) ^ 1u);
+      for (int jj = 0; jj < hpc; ++jj) {
+        const int st = jj % NST, j = j0 + jj;
+        mbar_wait(&kv_empty[st], ((jj / NST) & 1u) ^ 1u);
         uint8_t* base = smem + st * STAGE;
         mbar_arrive_expect_tx(&kv_full[st], (uint32_t)STAGE);
         // QKV is read once: evict-first keeps L2 for the ctx rows re-read by the quantize
@@ -117,10 +119,10 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idS = idesc_f16(128, 128, 0), idO = idesc_f16(128, 64, 1);
-      for (int j = 0; j < heads; ++j) {
-        const int st = j % NST;
-        const uint32_t ph = (uint32_t)j & 1u;
-        mbar_wait(&kv_full[st], (j / NST) & 1u);
+      for (int jj = 0; jj < hpc; ++jj) {
+        const int st = jj % NST;
+        const uint32_t ph = (uint32_t)jj & 1u;
+        mbar_wait(&kv_full[st], (jj / NST) & 1u);
         tc_fence_after();
         const uint32_t q = smem_u32(smem + st * STAGE), k = q + TILE, v = k + TILE;
         // S = Q K^T (in-order after PV of the previous head, which read P from these columns)
@@ -279,7 +281,8 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
           const int rr = it * 8 + (lane >> 2), ch = lane & 3;
           const int tok = q * 32 + ps * 16 + rr;
           const uint4 x = *reinterpret_cast<const uint4*>(slab + (uint32_t)(rr * 64 + ((ch ^ ((rr >> 1) & 3)) << 4)));
-          if (tok < S) st_global_hint(ctx_f16 + (size_t)(row0 + tok) * h + j * 64 + 32 * hf + ch * 8, x, pol_keep);
+          if (tok < S)
+            st_global_hint(ctx_f16 + (size_t)(row0 + tok) * h + (j0 + j) * 64 + 32 * hf + ch * 8, x, pol_keep);
         }
         __syncwarp();
       }
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
     };
     stamp(0, 6);
     const bool full = S - 64 * hf >= 64;  // warp-uniform
-    for (int j = 0; j < heads; ++j) {
+    for (int j = 0; j < hpc; ++j) {  // j: this CTA's head index (absolute head j0 + j)
       if (full)
         softmax(j, std::false_type{});
       else
@@ -299,6 +302,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
     red[hf * 128 + r] = __half2float(__float2half_rn(amax));
     __threadfence_block();  // ctx rows written by the other half's warps are re-read below
     asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (G > 1) goto cluster_tail;  // the row max-abs spans the cluster: combined below
     // The Q/K/V stages are idle now (every MMA completed before the last o_full): warp w
     // stages 6 of its rows at a time (12 KB) with cp.async so ~200 KB per SM is in flight.
     uint8_t* qb = smem + warp * 12288;
@@ -368,6 +372,45 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
     }
     stamp(0, 7);
   }
+cluster_tail:
+  if (G > 1) {
+    // Row max-abs over the G CTAs of this sequence through distributed shared memory; each
+    // CTA then codes its own hpc * 64 columns (a code depends only on its element and the
+    // row scale).  All threads of all CTAs take part in both cluster barriers; the second
+    // keeps every CTA's red[] alive until the others have read it.
+    float* red = reinterpret_cast<float*>(smem + OFF_RED);        // [2][128] this CTA's partials
+    float* amx = reinterpret_cast<float*>(smem + OFF_SLAB);       // [128] combined max-abs
+    float* rr7 = amx + 128;                                       // [128] 7 / amax
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (threadIdx.x < 128) {
+      const int r = threadIdx.x;
+      float a = 0.f;
+      for (int c = 0; c < G; ++c) {
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(red + r)), "r"(c));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(red + 128 + r)), "r"(c));
+        float x, y;
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(ra) : "memory");
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(y) : "r"(rb) : "memory");
+        a = fmaxf(a, fmaxf(x, y));
+      }
+      amx[r] = a;
+      rr7[r] = a > 0.f ? __fdiv_rn(7.0f, a) : 0.f;
+      if (g == 0 && r < S) ctx_scales[row0 + r] = a > 0.f ? __fdiv_rn(a, 7.0f) : 1.0f;
+    }
+    __syncthreads();
+    // this CTA's columns [64 j0, 64 (j0 + hpc)): cpr 16-byte chunks (8 values) per row
+    const int cpr = hpc * 8;
+    for (int idx = threadIdx.x; idx < S * cpr; idx += AT_THREADS) {
+      const int rw = idx / cpr, c = idx - rw * cpr;
+      const float a = amx[rw];
+      const uint4 x = __ldcg(reinterpret_cast<const uint4*>(ctx_f16 + (size_t)(row0 + rw) * h + j0 * 64 + c * 8));
+      const uint32_t hh[4] = {x.x, x.y, x.z, x.w};
+      reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] =
+          a > 0.f ? requant8(hh, a, rr7[rw], 0.f) : 0u;
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc(tmem, 256);
@@ -405,9 +448,28 @@ cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __ha
   static const int dbg = getenv("Q4_ATTN_DBG") ? atoi(getenv("Q4_ATTN_DBG")) : 0;  // profiling only
   static unsigned long long* trace_buf = nullptr;
   if (trace_path && !trace_buf) cudaMalloc(&trace_buf, sizeof(unsigned long long) * 512 * 16 * 16);
+  // Small batches: split each sequence's heads over a cluster of G CTAs so the grid fills
+  // the GPU (about two CTAs per SM); G divides heads and is at most 8 (portable cluster).
+  int G = 1;
+  if (B < 148)
+    for (int d = 8; d >= 2; --d)
+      if (heads % d == 0 && B * d <= 296) { G = d; break; }
   note_launch();
-  attention_tc_kernel<<<B, AT_THREADS, SMEM_AT, s>>>(tq, S, heads, ctx_f16, ctx_codes, ctx_scales,
-                                                     trace_path ? trace_buf : nullptr, dbg);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(B * G));
+  cfg.blockDim = dim3(AT_THREADS);
+  cfg.dynamicSmemBytes = SMEM_AT;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t le = cudaLaunchKernelEx(&cfg, attention_tc_kernel, tq, S, heads, ctx_f16, ctx_codes, ctx_scales,
+                                      trace_path ? trace_buf : nullptr, dbg, G);
+  if (le != cudaSuccess) return le;
   if (trace_path) {  // profiling only: dump this launch's stamps
     static unsigned long long host[512 * 16 * 16];
     cudaMemcpy(host, trace_buf, sizeof(host), cudaMemcpyDeviceToHost);
