@@ -16,6 +16,11 @@
  *   - Pointers are caller-owned DEVICE memory unless stated (q4_encoder_stack also
  *     accepts host memory for its input/output).  The library never allocates in
  *     these calls; scratch comes in through `workspace`, sized by *_workspace().
+ *     A workspace must be ZERO-FILLED before its first use (cudaMemset): the row
+ *     epilogues keep self-resetting cross-CTA rendezvous counters in it, and every
+ *     completed call leaves them zero again, so no per-call reset (and no memset node
+ *     in a captured graph) is needed.  A counter left non-zero (e.g. by a kernel fault)
+ *     makes the next row-epilogue call trap with Q4_ECUDA instead of hanging.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *     Calls are stream-ordered and asynchronous: no host synchronisation, no
  *     allocation, no host-side state change, so they can be captured in CUDA graphs

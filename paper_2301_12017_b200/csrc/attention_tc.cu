@@ -98,6 +98,8 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();  // everything below may read the previous kernel's outputs
   // TMEM columns: S / P at [0, 128), O at [128, 192) (single-buffered; two CTAs per SM overlap)
   if (warp == 8) {
     // ---------------------------------------------------------------- producer
@@ -460,13 +462,16 @@ cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __ha
   cfg.blockDim = dim3(AT_THREADS);
   cfg.dynamicSmemBytes = SMEM_AT;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)G;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see launch_pdl)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool no_pdl = getenv("Q4_NO_PDL") != nullptr;  // profiling only
+  cfg.numAttrs = (no_pdl || (int64_t)B * S > kPdlMaxRows) ? 1 : 2;
   cudaError_t le = cudaLaunchKernelEx(&cfg, attention_tc_kernel, tq, S, heads, ctx_f16, ctx_codes, ctx_scales,
                                       trace_path ? trace_buf : nullptr, dbg, G);
   if (le != cudaSuccess) return le;

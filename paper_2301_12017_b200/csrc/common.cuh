@@ -43,6 +43,13 @@ Q4_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Kernels launched with launch_pdl() start their prologue (barrier init, TMEM alloc,
+// descriptor prefetch) while the previous kernel in the stream drains, and must execute
+// pdl_wait() before touching any global memory another kernel produces or consumes.
+Q4_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+Q4_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ proxies / fences
 Q4_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

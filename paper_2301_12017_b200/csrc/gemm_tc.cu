@@ -50,7 +50,7 @@ struct TcParams {
   float* out_scales;
   float2* xstat;      // [mblocks][ntn][128] (mean, M2) partials
   float* xamax;       // [mblocks][ntn][128] max-abs partials
-  unsigned* xcnt;     // [2][mblocks] arrival counters (zeroed before launch)
+  unsigned* xcnt;     // [4][mblocks] arrival / departure counters (self-resetting; zero on entry)
   int dbg;            // profiling only (env Q4_DEBUG_SKIP): 1 skip TMA, 2 skip unpack, 4 skip MMA, 8 skip epilogue math
   unsigned long long* trace;  // profiling only (env Q4_TRACE): [grid][64 tiles][8] %globaltimer stamps
 };
@@ -310,13 +310,26 @@ Q4_DEV void slab_load(uint8_t* stg, const uint8_t* gbase, int row0, int M, size_
 // partial; one thread publishes the arrival (fence + atomic, cumulative over the group's
 // stores via bar.sync), waits for the `ntn` CTAs sharing the m-block, fences again, and
 // the group then reads all partials with L2 (.cg) loads.  Same pattern as a grid sync.
-Q4_DEV void exchange_sync(unsigned* cnt, int ntn, int bar_id, int nthreads, bool leader, int dbg = 0) {
+// Cross-CTA rendezvous of the ntn CTAs of one m-block (co-resident by construction).
+// cnt[0] counts arrivals, cnt[dep] departures; the last CTA to leave resets both, so the
+// counters are zero again when the kernel ends (the workspace must be zeroed once before
+// its first use; kernels leave it zeroed).  A rendezvous that cannot complete (corrupt
+// workspace) traps after ~2^26 polls instead of hanging the GPU.
+Q4_DEV void exchange_sync(unsigned* cnt, size_t dep, int ntn, int bar_id, int nthreads, bool leader, int dbg = 0) {
   named_bar(bar_id, nthreads);
   if (leader && !(dbg & 32)) {
     __threadfence();
     atomicAdd(cnt, 1u);
-    while (ld_acquire_gpu(cnt) < (unsigned)ntn) __nanosleep(32);
+    unsigned polls = 0;
+    while (ld_acquire_gpu(cnt) < (unsigned)ntn) {
+      __nanosleep(32);
+      if (++polls > (1u << 26)) __trap();
+    }
     __threadfence();
+    if (atomicAdd(cnt + dep, 1u) == (unsigned)ntn - 1) {  // everyone has seen the full count
+      cnt[0] = 0u;
+      cnt[dep] = 0u;
+    }
   }
   named_bar(bar_id, nthreads);
 }
@@ -383,6 +396,8 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   TileIter it(p);
   int mb, nb;
+  pdl_launch_dependents();
+  pdl_wait();  // everything below may read the previous kernel's outputs
 
   // Register rebalancing (row epilogues): one setmaxnreg per side, executed by whole
   // warpgroups at a single call site that dominates that side's code.
@@ -664,24 +679,24 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
               cm2 = a0.y + a1.y + d * d * (nh * 0.5f);
             }
             if (sub == 0) p.xstat[((size_t)mb * ntn + nb) * 128 + r] = make_float2(cm, cm2);
-            exchange_sync(p.xcnt + mb, ntn, gbar, GT, leader, p.dbg);
+            exchange_sync(p.xcnt + mb, 2 * (size_t)p.mblocks, ntn, gbar, GT, leader, p.dbg);
             stamp(3);
             // every partial covers TN columns: mean = average of the means, M2 = sum of the M2s
-            // + TN * sum of squared deviations of the means
+            // + TN * sum of squared deviations of the means.  One pass, deviations taken
+            // from partial 0's mean (the partial means are close, so no cancellation).
             const float2* xs = p.xstat + ((size_t)mb * ntn) * 128 + r;
-            float msum = 0.f, m2 = 0.f;
-            for (int kk = 0; kk < ntn; ++kk) {
+            const float2 o0 = __ldcg(xs);
+            float dsum = 0.f, dsq = 0.f, m2 = o0.y;
+            for (int kk = 1; kk < ntn; ++kk) {
               const float2 o = __ldcg(xs + (size_t)kk * 128);
-              msum += o.x;
+              const float dd = o.x - o0.x;
+              dsum += dd;
+              dsq = fmaf(dd, dd, dsq);
               m2 += o.y;
             }
-            mean = msum * inv_ntn;
-            float dev = 0.f;
-            for (int kk = 0; kk < ntn; ++kk) {
-              const float dd = __ldcg(xs + (size_t)kk * 128).x - mean;
-              dev = fmaf(dd, dd, dev);
-            }
-            m2 = fmaf((float)TN, dev, m2);
+            const float dm = dsum * inv_ntn;  // mean - mean_0
+            mean = o0.x + dm;
+            m2 = fmaf((float)TN, fmaf(-(float)ntn * dm, dm, dsq), m2);
             const float cnt = (float)(TN * ntn);
             rstd = 1.0f / sqrtf(m2 / cnt + p.ln_eps);
           }
@@ -748,7 +763,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
           amax = fmaxf(rowp[r].z, rowp[128 + r].z);
         }
         if (sub == 0) p.xamax[((size_t)mb * ntn + nb) * 128 + r] = amax;
-        exchange_sync(p.xcnt + p.mblocks + mb, ntn, gbar, GT, leader, p.dbg);
+        exchange_sync(p.xcnt + p.mblocks + mb, 2 * (size_t)p.mblocks, ntn, gbar, GT, leader, p.dbg);
         stamp(5);
         for (int kk = 0; kk < ntn; ++kk) amax = fmaxf(amax, __ldcg(&p.xamax[((size_t)mb * ntn + kk) * 128 + r]));
         // pass B: codes (R1-R3), packed, staged, coalesced stores
@@ -884,11 +899,12 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     p.xstat = reinterpret_cast<float2*>(w);
     p.xamax = reinterpret_cast<float*>(w + nslot * 8);
     p.xcnt = reinterpret_cast<unsigned*>(w + nslot * 12);
-    cudaError_t e = cudaMemsetAsync(p.xcnt, 0, sizeof(unsigned) * 2 * p.mblocks, s);
-    if (e != cudaSuccess) return e;
   }
   note_launch();
-  kern<<<grid, EpiCfg<KIND>::THREADS, C::SMEM, s>>>(ta, tb, p);
+  {
+    const cudaError_t le = launch_pdl(g.M <= kPdlMaxRows, kern, dim3(grid), dim3(EpiCfg<KIND>::THREADS), C::SMEM, s, ta, tb, p);
+    if (le != cudaSuccess) return le;
+  }
   if (trace_path) {  // profiling only: dump the stamps of this launch (synchronous)
     static unsigned long long host[148 * 64 * 8];
     cudaMemcpy(host, trace_buf, sizeof(host), cudaMemcpyDeviceToHost);
@@ -939,7 +955,7 @@ int tc_tile_n(int M, int N, int kind) {
 size_t tc_workspace_bytes(int M, int N, int TN) {
   if (TN <= 0) return 0;
   const size_t mblocks = (size_t)(M + 127) / 128, ntn = (size_t)N / TN;
-  return mblocks * ntn * 128 * 12 + 2 * mblocks * sizeof(unsigned) + 256;
+  return mblocks * ntn * 128 * 12 + 4 * mblocks * sizeof(unsigned) + 256;
 }
 
 cudaError_t launch_w4a4_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {

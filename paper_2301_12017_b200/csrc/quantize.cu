@@ -15,6 +15,8 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(const __half* __rest
                                                             int64_t rows, int cols, int64_t ld_x,
                                                             float clip, uint8_t* __restrict__ codes,
                                                             float* __restrict__ scales) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -117,9 +119,9 @@ cudaError_t launch_quantize_rows(const __half* x, int64_t rows, int cols, int64_
   const dim3 grid((unsigned)((rows + warps - 1) / warps)), block(32 * warps);
   const int nvec = cols / 8;
   note_launch();
-  if (nvec <= 32) quantize_rows_kernel<1><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
-  else if (nvec <= 64) quantize_rows_kernel<2><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
-  else if (nvec <= 128) quantize_rows_kernel<4><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
+  if (nvec <= 32) return launch_pdl(rows <= kPdlMaxRows, quantize_rows_kernel<1>, grid, block, 0, s, x, rows, cols, ld_x, clip, codes, scales);
+  else if (nvec <= 64) return launch_pdl(rows <= kPdlMaxRows, quantize_rows_kernel<2>, grid, block, 0, s, x, rows, cols, ld_x, clip, codes, scales);
+  else if (nvec <= 128) return launch_pdl(rows <= kPdlMaxRows, quantize_rows_kernel<4>, grid, block, 0, s, x, rows, cols, ld_x, clip, codes, scales);
   else if (nvec <= 256) quantize_rows_kernel<8><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
   else if (nvec <= 512) quantize_rows_kernel<16><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
   else quantize_rows_long_kernel<<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);

@@ -29,7 +29,7 @@ class W4A4Encoder:
     def workspace(self, B: int, S: int) -> torch.Tensor:
         if self._ws_shape != (B, S):
             n = lib().q4_encoder_stack_workspace(C.byref(self._lc), B, S)
-            self._ws = torch.empty(max(n, 1), dtype=torch.uint8, device=self.device)
+            self._ws = torch.zeros(max(n, 1), dtype=torch.uint8, device=self.device)
             self._ws_shape = (B, S)
         return self._ws
 

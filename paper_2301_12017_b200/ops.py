@@ -76,7 +76,7 @@ def w4a4_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None
                  out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")), w_i8=_ptr(w_i8))
     ws_bytes = lib().q4_w4a4_linear_workspace(M, N, K, kind)
     if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
-        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
     check(lib().q4_w4a4_linear(_ptr(a_codes), _ptr(a_scales), _ptr(w_codes), _ptr(w_scales),
                                M, N, K, C.byref(e), _ptr(workspace),
                                0 if workspace is None else workspace.numel(), _stream()))
@@ -139,7 +139,7 @@ def encoder_layer(cfg: dict, w: dict, B: int, S: int, h_in, hq_in, hs_in, taps: 
     lc = layer_cfg(cfg)
     ws_bytes = lib().q4_encoder_layer_workspace(C.byref(lc), B, S)
     if workspace is None:
-        workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+        workspace = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     out = {"h_out": torch.empty(M, h, dtype=torch.float16, device=dev),
            "hq_out": torch.empty(M, h // 2, dtype=torch.uint8, device=dev),
            "hs_out": torch.empty(M, dtype=torch.float32, device=dev)}
