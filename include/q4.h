@@ -104,7 +104,8 @@ typedef enum { Q4_EPI_I32 = 0, Q4_EPI_F16 = 1, Q4_EPI_GELU_Q4 = 2, Q4_EPI_RESLN_
  *   MMA_SYNC_S4 legacy: cp.async -> ldmatrix -> mma.sync m16n8k64 .s4 (emulated on sm_100a)
  *   TCGEN05_W8  as TCGEN05, but the weights come prepacked (epi->w_i8, q4_prepack_weights):
  *               TMA'd straight into the swizzled operand stage; only A is unpacked on chip
- * AUTO uses TCGEN05_W8 when epi->w_i8 is given and M > 256, else TCGEN05.
+ * AUTO uses TCGEN05_W8 when epi->w_i8 is given (faster at every measured M, 128..32768:
+ * profiles/r1_gemm_sweep.jsonl), else TCGEN05.
  * The legacy variants implement Q4_EPI_I32 and Q4_EPI_F16 only. */
 typedef enum { Q4_MAINLOOP_AUTO = 0, Q4_MAINLOOP_TCGEN05 = 1, Q4_MAINLOOP_MMA_SYNC_S8 = 2,
                Q4_MAINLOOP_MMA_SYNC_S4 = 3, Q4_MAINLOOP_TCGEN05_W8 = 4 } q4_mainloop;

@@ -132,7 +132,7 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
   g.out_i32 = epi->out_i32; g.out_f16 = reinterpret_cast<__half*>(epi->out_f16);
   g.out_codes = epi->out_codes; g.out_scales = epi->out_scales;
   g.w_i8 = nullptr;
-  if (epi->mainloop == Q4_MAINLOOP_TCGEN05_W8 || (epi->mainloop == Q4_MAINLOOP_AUTO && epi->w_i8 && M > 256)) {
+  if (epi->mainloop == Q4_MAINLOOP_TCGEN05_W8 || (epi->mainloop == Q4_MAINLOOP_AUTO && epi->w_i8)) {
     if (!epi->w_i8 || !al16(epi->w_i8))
       return fail(Q4_EINVAL, "q4_w4a4_linear: TCGEN05_W8 needs 16-byte aligned epi->w_i8 (q4_prepack_weights)");
     g.w_i8 = epi->w_i8;

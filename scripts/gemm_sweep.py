@@ -1,0 +1,52 @@
+"""BASELINE configs[4]: W4A4 GEMM shape sweep, M in {128..32768} x (K, N) in
+{(768,3072), (3072,768), (1024,4096), (4096,1024)}, F16 (dequant + bias) epilogue, CUDA-event
+timing of a CUDA graph of 20 back-to-back launches (inputs resident; the graph removes the
+host launch cost that would otherwise dominate at small M), for the tcgen05 mainloop with packed
+weights, with prepacked int8 weights (W8) and the legacy mma.sync s8 baseline.  TOPS =
+2*M*N*K / t; roofline = min(INT8 peak, HBM * ops/bytes) with the peaks of bench.peaks().
+Writes one JSON object per line (profiles/r1_gemm_sweep.jsonl when run by the round script)."""
+import os, sys, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2301_12017_b200 as q4
+from paper_2301_12017_b200 import synth
+from bench import peaks
+
+pk = peaks()
+int8_peak, hbm = pk["int8_tops"], pk["hbm_gbs"]
+dev = torch.device("cuda")
+for (K, N) in ((768, 3072), (3072, 768), (1024, 4096), (4096, 1024)):
+    w = torch.from_numpy(synth.random_packed(N, K, "sw%d" % N)).to(dev)
+    sw = torch.from_numpy(synth.random_scales(N, "ssw%d" % N)).to(dev)
+    w8 = q4.prepack_weights(w)
+    for M in (128, 512, 2048, 8192, 32768):
+        a = torch.from_numpy(synth.random_packed(M, K, "sa%d" % M)).to(dev)
+        sa = torch.from_numpy(synth.random_scales(M, "ssa%d" % M)).to(dev)
+        ops = 2.0 * M * N * K
+        for name, ml, kw in (("tcgen05", 1, {}), ("tcgen05_w8", 4, {"w_i8": w8}), ("mma_sync_s8", 2, {})):
+            ws = torch.zeros(max(1, q4.lib().q4_w4a4_linear_workspace(M, N, K, q4.EPI_F16)), dtype=torch.uint8,
+                             device=dev)
+            o = q4.w4a4_linear(a, sa, w, sw, q4.EPI_F16, mainloop=ml, workspace=ws, **kw)
+            for _ in range(3):
+                q4.w4a4_linear(a, sa, w, sw, q4.EPI_F16, mainloop=ml, out=o, workspace=ws, **kw)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(20):
+                    q4.w4a4_linear(a, sa, w, sw, q4.EPI_F16, mainloop=ml, out=o, workspace=ws, **kw)
+            g.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(5):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 100 * 1e-3
+            wbytes = N * K if ml == 4 else N * K / 2
+            byt = M * K / 2 + wbytes + 4 * M + 6 * N + 2 * M * N
+            roof = min(int8_peak, hbm * 1e9 * ops / byt / 1e12)
+            print(json.dumps({"M": M, "N": N, "K": K, "mainloop": name, "us": round(t * 1e6, 2),
+                              "TOPS": round(ops / t / 1e12, 1), "frac_int8_peak": round(ops / t / 1e12 / int8_peak, 3),
+                              "roofline_TOPS": round(roof, 1), "frac_roofline": round(ops / t / 1e12 / roof, 3)}),
+                  flush=True)
