@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip latency / GEMM side measurements")
+    ap.add_argument("--gather", default="cls", choices=["cls", "full", "none"],
+                    help="N>1: NCCL all-gather of the outputs inside every timed step (SURVEY 8(e))")
     return ap.parse_args()
 
 
@@ -235,8 +237,16 @@ def main():
 
     enc.capture(xd, out, B, S)
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+    # the one data collective (N > 1): gather the outputs of every rank after the last layer
+    gather = qd.OutputGather(B, S, h, args.gather, dev) if (world > 1 and args.gather != "none") else None
+
+    def step():
         enc.replay()
+        if gather is not None:
+            gather(out)
+
+    for _ in range(args.warmup):
+        step()
     torch.cuda.synchronize()
 
     # ------------------------------------------------------------------ timed region
@@ -246,7 +256,7 @@ def main():
     with ClockSampler(list(range(N)) if rank == 0 else [local]) as clk:
         ev[0].record(stream)
         for i in range(args.steps):
-            enc.replay()
+            step()
             ev[i + 1].record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -256,6 +266,24 @@ def main():
     p50 = max_over_ranks(statistics.median(step_ms))
     value = N * B / (ms_per_step / 1e3)
     clocks = clk.summary()
+    gather_info = None
+    if gather is not None:
+        # both gather modes timed alone on the same stream (device time, max over ranks)
+        gather_info = {"in_step": args.gather, "bytes_per_rank": gather.bytes_per_rank}
+        for mode in ("cls", "full"):
+            g = qd.OutputGather(B, S, h, mode, dev)
+            g(out)
+            torch.cuda.synchronize()
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(10):
+                g(out)
+            b.record(stream)
+            torch.cuda.synchronize()
+            gather_info[f"{mode}_ms"] = max_over_ranks(a.elapsed_time(b) / 10)
+            gather_info[f"{mode}_bytes_per_rank"] = g.bytes_per_rank
+            del g
 
     # ------------------------------------------------------------------ end to end (host buffers)
     e2e = None
@@ -368,12 +396,13 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "int4 (W4A4, s8 tensor-core MMA, s32 acc)",
             "data": "synthetic (seeded, random-init weights)",
             "config": {"workload": WORKLOAD, "model": f"bert-{args.model}", "layers": L, "batch_per_gpu": B,
-                       "global_batch": B * N, "seq_len": S, "parallelism": f"dp{N} (batch-sharded replicas, no collective)",
+                       "global_batch": B * N, "seq_len": S, "parallelism": f"dp{N} (batch-sharded replicas" + (
+                           f", NCCL all-gather of the {args.gather} outputs per step)" if gather is not None else ", no collective)"),
                        "l2": f"no flush: per-step working set {(M * h * 2 * 6 + M * cfg['ffn'] / 2) / 1e9:.2f} GB "
                              f"of activations + {sum(v.numel() for w in enc.weights for v in w.values()) / 1e6:.0f} MB "
                              f"weights >> 126 MB L2", "cuda_graph": True},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks, "kernels": breakdown, "extras": extras, "lib": q4.version(),
+            "clocks": clocks, "gather": gather_info, "kernels": breakdown, "extras": extras, "lib": q4.version(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -2,10 +2,11 @@
 
 Sequences are independent, so the path shards by batch with no collective in the data
 path: rank r of W takes its contiguous slice of the global batch, holds full weight
-replicas, and runs the same CUDA graph.  The only cross-rank operations are host-side
-plumbing: a barrier around the timed region and a max-reduction of the per-rank device
-time (the job finishes when the slowest rank does).  torch.distributed supplies the
-process group (NCCL on GPUs, gloo in the CPU tests)."""
+replicas, and runs the same CUDA graph.  The one data collective is the gather of the
+outputs after the last layer (`OutputGather`); the rest is host-side plumbing: a barrier
+around the timed region and a max-reduction of the per-rank device time (the job
+finishes when the slowest rank does).  torch.distributed supplies the process group
+(NCCL over NVLink/NVSwitch on GPUs, gloo in the CPU tests)."""
 from __future__ import annotations
 
 import os
@@ -42,3 +43,42 @@ def max_over_ranks(x: float, device=None) -> float:
 def barrier():
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.barrier()
+
+
+class OutputGather:
+    """The one collective of the batch-sharded path (north_star: "no collective in the hot
+    path beyond an NCCL gather of outputs"): every rank's final hidden states
+    [B_r * S, h] are gathered, in rank order, into the global [B * S, h] -- mode "full" --
+    or only the [CLS] row (token 0) of each sequence, [B, h] -- mode "cls", the input of a
+    BERT classification head.  Rank r's rows land at [r * B_r, (r+1) * B_r): the gathered
+    tensor is the single-GPU output of the same global batch (shards are equal-sized here).
+
+    Buffers are allocated once (graph- and replay-friendly); `__call__` is stream-ordered
+    and does not synchronize.  World size 1: the local tensor itself (no collective)."""
+
+    def __init__(self, B: int, S: int, h: int, mode: str = "cls", device=None, dtype=torch.float16):
+        if mode not in ("cls", "full"):
+            raise ValueError(f"gather mode {mode!r} (expected 'cls' or 'full')")
+        self.B, self.S, self.h, self.mode = B, S, h, mode
+        self.world = dist.get_world_size() if (dist.is_available() and dist.is_initialized()) else 1
+        rows = B if mode == "cls" else B * S
+        self.local = torch.empty(rows, h, dtype=dtype, device=device) if mode == "cls" else None
+        self.out = torch.empty(self.world * rows, h, dtype=dtype, device=device) if self.world > 1 else None
+
+    @property
+    def bytes_per_rank(self) -> int:
+        rows = self.B if self.mode == "cls" else self.B * self.S
+        return rows * self.h * 2
+
+    def __call__(self, hidden: torch.Tensor) -> torch.Tensor:
+        if tuple(hidden.shape) != (self.B * self.S, self.h):
+            raise ValueError(f"gather: hidden {tuple(hidden.shape)} != ({self.B * self.S}, {self.h})")
+        if self.mode == "cls":
+            self.local.copy_(hidden.view(self.B, self.S, self.h)[:, 0])
+            src = self.local
+        else:
+            src = hidden
+        if self.world == 1:
+            return src
+        dist.all_gather_into_tensor(self.out, src.contiguous())
+        return self.out

@@ -62,3 +62,45 @@ def test_two_rank_gloo_shards_and_max():
     assert np.array_equal(got, full)  # shards reassemble the single-rank global batch
     assert all(m == 20.0 for *_, m in res)  # max over ranks seen by every rank
     assert [(s, c) for _, s, c, _, _ in res] == [(0, 3), (3, 3)]
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B, S, h = 3, 4, 8
+        start, count = qd.shard(B * world, rank, world)
+        loc = torch.from_numpy(np.concatenate([synth.hidden(S, h, "input", b) for b in range(start, start + count)]))
+        got = {m: qd.OutputGather(B, S, h, m)(loc).clone().numpy() for m in ("cls", "full")}
+        with pytest.raises(ValueError):
+            qd.OutputGather(B, S, h, "full")(loc[:-1])
+        q.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_output_gather():
+    """The gathered outputs equal the single-rank global batch (full) and its [CLS] rows."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = np.concatenate([synth.hidden(4, 8, "input", b) for b in range(6)])
+    for _, got in res:  # every rank holds the whole gathered output
+        assert np.array_equal(got["full"], full)
+        assert np.array_equal(got["cls"], full[::4])
+
+
+def test_output_gather_single_process():
+    B, S, h = 2, 3, 4
+    x = torch.arange(B * S * h, dtype=torch.float16).view(B * S, h)
+    assert torch.equal(qd.OutputGather(B, S, h, "full")(x), x)
+    assert torch.equal(qd.OutputGather(B, S, h, "cls")(x), x[::S])
+    with pytest.raises(ValueError):
+        qd.OutputGather(B, S, h, "rows")
