@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libq4.so")
+# Q4_LIB_PATH: profiling only (A/B timing of two builds); the default is the in-tree build
+LIB_PATH = os.environ.get("Q4_LIB_PATH") or os.path.join(HERE, "libq4.so")
 
 Q4_OK, Q4_EINVAL, Q4_ESHAPE, Q4_EALIGN, Q4_EUNSUPPORTED, Q4_ECUDA = range(6)
 EPI_I32, EPI_F16, EPI_GELU_Q4, EPI_RESLN_Q4 = range(4)

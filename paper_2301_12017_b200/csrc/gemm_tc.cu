@@ -118,6 +118,7 @@ struct TileIter {
 };
 
 // ------------------------------------------------------------------ small helpers
+constexpr int kUnpackBar = 12;  // named barrier of the 4 unpack warps (ids 1-11: epilogue)
 Q4_DEV void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 Q4_DEV unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
@@ -165,22 +166,22 @@ Q4_DEV void unpack_rows(const uint8_t* __restrict__ pk, uint8_t* __restrict__ un
 }
 
 // 32 codes (4 packed words) from 16 words of halves.  Unclipped rows take the batched
-// fast path (one tie check for all 32 values); clipped rows or near-ties use requant8.
+// fast path (one tie check per 8 values); clipped rows or near-ties use requant8.
 Q4_DEV uint4 requant32(const uint32_t (&h)[16], float amax, float r7, float clip) {
+  // The fix-up is taken per 8 codes: a warp holds 32 rows, so a per-32 check sends the whole
+  // warp down the exact path for ~20% of its chunks (GELU rows, measured); per 8 it is ~6%.
   uint32_t w[4];
-  bool exact = clip > 0.f || !(amax > 0.f);
-  if (!exact) {
-    float dmax = 0.f;
+  const bool exact = clip > 0.f || !(amax > 0.f);
+  float dm[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t hk[4] = {h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]};
-      w[u] = requant8_nofix(hk, r7, dmax);
-    }
-    exact = dmax > 0.499998f;
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t hk[4] = {h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]};
+    dm[u] = 0.f;
+    w[u] = requant8_nofix(hk, r7, dm[u]);
   }
-  if (exact) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < 4; ++u) {
+    if (exact || dm[u] > 0.499998f) {
       const uint32_t hk[4] = {h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]};
       w[u] = requant8(hk, amax, r7, clip);
     }
@@ -484,9 +485,15 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
       for (int kb = 0; kb < KB; ++kb, ++g) {
         const int s = g % C::SP, su = g % C::SU;
         const unsigned long long u0 = utr ? gtimer() : 0;
-        mbar_wait(&full_p[s], (g / C::SP) & 1u);
+        // Row epilogues: the first unpack warp polls both barriers and the other three block
+        // in bar.sync (their spin would take issue slots from 16 busy epilogue warps).  With
+        // the light F16 / I32 epilogues every warp polls (measured faster: no barrier hop).
+        if (!EpiCfg<KIND>::ROW || warp == WU) {
+          mbar_wait(&full_p[s], (g / C::SP) & 1u);
+          mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
+        }
         const unsigned long long u1 = utr ? gtimer() : 0;
-        mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
+        if constexpr (EpiCfg<KIND>::ROW) named_bar(kUnpackBar, 128);
         const unsigned long long u2 = utr ? gtimer() : 0;
         const uint8_t* pk = smem + C::OFF_PK + s * C::PK_STAGE;
         uint8_t* un = smem + C::OFF_UN + su * C::UN_STAGE;
@@ -579,7 +586,10 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) rr[u] = (row_ok && !(p.dbg & 64)) ? __ldg(resp + 4 * sub + u) : make_uint4(0, 0, 0, 0);
       }
-      mbar_wait(&tfull[b], (tcount >> 1) & 1u);
+      // one warp of the group polls the accumulator barrier; the others block in bar.sync
+      // (a try_wait spin in all EPW warps costs issue slots the working group needs)
+      if (ew % EPW == 0) mbar_wait(&tfull[b], (tcount >> 1) & 1u);
+      named_bar(gbar, GT);
       tc_fence_after();
       stamp(1);
 

@@ -135,6 +135,28 @@ def test_linear_gelu_q4(q4, M, N, K, mainloop):
     assert mism < 1e-2
 
 
+@pytest.mark.parametrize("M,N,K", [(1029, 3072, 768), (640, 4096, 1024), (3000, 1024, 256)])
+def test_linear_gelu_q4_large_w8(q4, M, N, K):
+    """M > 512 with prepacked weights: TN = 256 tiles, several m-blocks per CTA, ragged last
+    m-block.  Codes-only launches must equal the tap launch."""
+    x, wt, b = synth.hidden(M, K, f"gdx{M}"), synth.weight(N, K, f"gdw{N}_{K}"), synth.bias(N, f"gdb{N}")
+    a, sa = orc.quantize_rows(x)
+    w, sw = orc.quantize_rows(wt)
+    wd = dev(w)
+    w8 = q4.prepack_weights(wd)
+    out = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_GELU_Q4, bias=dev(b), f16_tap=True, w_i8=w8)
+    ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, orc.EPI_GELU_Q4, bias=b)
+    y = host(out["f16"])
+    assert_f16_close(y, ref["f16"], "GELU f16")
+    c2, s2 = orc.quantize_rows(y)
+    assert np.array_equal(host(out["codes"]), c2)
+    assert np.array_equal(host(out["scales"]), s2)
+    for _ in range(2):  # repeated launches: the self-resetting exchange counters
+        o2 = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_GELU_Q4, bias=dev(b), w_i8=w8)
+        assert np.array_equal(host(o2["codes"]), c2)
+        assert np.array_equal(host(o2["scales"]), s2)
+
+
 # ------------------------------------------------------------------ a6 residual + LN + requant
 @pytest.mark.parametrize("M,N,K", [(128, 768, 768), (257, 1024, 1024), (300, 768, 3072), (64, 1024, 4096), (7, 256, 512)])
 @pytest.mark.parametrize("mainloop", [1, 4], ids=["tcgen05", "tcgen05_w8"])
