@@ -61,6 +61,10 @@ def lib():
                                          P, P, P, P, I]
         L.oracle_attention.argtypes = [P, I64, I64, I, I, P, P, P, I]
         L.oracle_encoder_layer.argtypes = [P, P, I64, I64, P, P, P, P, P, P, P, I]
+        L.oracle_quantize_rows_i8.argtypes = [P, I64, I64, I64, F, P, P, I]
+        L.oracle_gemm_i32_i8.argtypes = [P, P, I64, I64, I64, P, I]
+        L.oracle_w8a8_linear.argtypes = [P, P, P, P, I64, I64, I64, I, P, P, P, P, D, F,
+                                         P, P, P, P, I]
         _lib = L
     return _lib
 
@@ -149,6 +153,50 @@ def w4a4_linear(a_codes, a_scales, w_codes, w_scales, M, N, K, epi=EPI_F16, bias
                                   epi, _p(bias), _p(residual), _p(gamma), _p(beta), ln_eps, clip,
                                   _p(i32), _p(f16), _p(codes), _p(scales), threads)
     _check(rc, "w4a4_linear")
+    return out
+
+
+# ---------------------------------------------------------------- O-11 .. O-13 (W8A8)
+def quantize_rows_i8(x: np.ndarray, clip: float = 0.0, threads: int = 0):
+    """O-11: x fp16 [rows, cols] -> (codes int8 [rows, cols], scales fp32 [rows] = fl32(amax/127))."""
+    x = _c(x, np.float16)
+    rows, cols = x.shape
+    codes = np.zeros((rows, cols), np.int8)
+    scales = np.zeros(rows, np.float32)
+    _check(lib().oracle_quantize_rows_i8(_p(x), rows, cols, cols, clip, _p(codes), _p(scales),
+                                         threads), "quantize_rows_i8")
+    return codes, scales
+
+
+def gemm_i32_i8(a_codes, w_codes, M, N, K, threads: int = 0) -> np.ndarray:
+    """O-12: exact int8 x int8 GEMM, acc [M, N] int32."""
+    a_codes, w_codes = _c(a_codes, np.int8), _c(w_codes, np.int8)
+    acc = np.zeros((M, N), np.int32)
+    _check(lib().oracle_gemm_i32_i8(_p(a_codes), _p(w_codes), M, N, K, _p(acc), threads), "gemm_i8")
+    return acc
+
+
+def w8a8_linear(a_codes, a_scales, w_codes, w_scales, M, N, K, epi=EPI_F16, bias=None,
+                residual=None, gamma=None, beta=None, ln_eps=1e-12, clip=0.0,
+                want_f16=True, threads: int = 0):
+    """O-13: the W4A4 epilogues on the int8 accumulator; requant kinds give int8 codes."""
+    a_codes, w_codes = _c(a_codes, np.int8), _c(w_codes, np.int8)
+    a_scales, w_scales = _c(a_scales, np.float32), _c(w_scales, np.float32)
+    bias, residual = _c(bias, np.float16), _c(residual, np.float16)
+    gamma, beta = _c(gamma, np.float16), _c(beta, np.float16)
+    out = {}
+    i32 = f16 = codes = scales = None
+    if epi == EPI_I32:
+        i32 = out["i32"] = np.zeros((M, N), np.int32)
+    if epi == EPI_F16 or epi == EPI_RESLN_Q4 or (epi == EPI_GELU_Q4 and want_f16):
+        f16 = out["f16"] = np.zeros((M, N), np.float16)
+    if epi in (EPI_GELU_Q4, EPI_RESLN_Q4):
+        codes = out["codes"] = np.zeros((M, N), np.int8)
+        scales = out["scales"] = np.zeros(M, np.float32)
+    rc = lib().oracle_w8a8_linear(_p(a_codes), _p(a_scales), _p(w_codes), _p(w_scales), M, N, K,
+                                  epi, _p(bias), _p(residual), _p(gamma), _p(beta), ln_eps, clip,
+                                  _p(i32), _p(f16), _p(codes), _p(scales), threads)
+    _check(rc, "w8a8_linear")
     return out
 
 

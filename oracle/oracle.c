@@ -66,9 +66,10 @@ static int64_t rhe_div(int64_t n, int64_t d) {
   return q;
 }
 
-/* One row: x' = clip(x); a = max|x'|; q = rhe(7 x'/a) exactly; scale = fl32(a/7).
- * fp16 values are integers times 2^-24, so 7x'/a = 7X/A with X, A integers (< 2^41). */
-static void quantize_row(const uint16_t* x, int64_t cols, double clip, int8_t* q, float* scale) {
+/* One row at b bits, qmax = 2^(b-1) - 1: x' = clip(x); a = max|x'|; q = rhe(qmax x'/a)
+ * exactly; scale = fl32(a/qmax).  fp16 values are integers times 2^-24, so qmax x'/a =
+ * qmax X/A with X, A integers (< 2^41; qmax X < 2^48 for b = 8). */
+static void quantize_row_q(const uint16_t* x, int64_t cols, double clip, int qmax, int8_t* q, float* scale) {
   double amax = 0.0;
   for (int64_t j = 0; j < cols; ++j) {
     double v = oracle_f16_to_f64(x[j]);
@@ -85,13 +86,17 @@ static void quantize_row(const uint16_t* x, int64_t cols, double clip, int8_t* q
     double v = oracle_f16_to_f64(x[j]);
     if (clip > 0.0) v = v > clip ? clip : (v < -clip ? -clip : v);
     int64_t X = (int64_t)ldexp(fabs(v), 24);
-    int64_t c = rhe_div(7 * X, A);
+    int64_t c = rhe_div((int64_t)qmax * X, A);
     if (v < 0) c = -c;
-    if (c > 7) c = 7;   /* clamp to [-2^(b-1), 2^(b-1)-1]; never binds */
-    if (c < -8) c = -8;
+    if (c > qmax) c = qmax; /* clamp to [-2^(b-1), 2^(b-1)-1]; never binds */
+    if (c < -qmax - 1) c = -qmax - 1;
     q[j] = (int8_t)c;
   }
-  *scale = (float)amax / 7.0f; /* IEEE fp32 division, correctly rounded (R6) */
+  *scale = (float)amax / (float)qmax; /* IEEE fp32 division, correctly rounded (R6) */
+}
+
+static void quantize_row(const uint16_t* x, int64_t cols, double clip, int8_t* q, float* scale) {
+  quantize_row_q(x, cols, clip, 7, q, scale);
 }
 
 static void pack_row(const int8_t* q, int64_t cols, uint8_t* out) {
@@ -119,6 +124,14 @@ int oracle_quantize_rows(const uint16_t* x, int64_t rows, int64_t cols, int64_t 
     pack_row(q, cols, codes + r * pb);
     free(q);
   }
+  return 0;
+}
+
+int oracle_quantize_rows_i8(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x,
+                            float clip, int8_t* codes, float* scales, int threads) {
+  if (rows < 0 || cols < 0 || ld_x < cols || !clip_is_f16(clip)) return -1;
+#pragma omp parallel for schedule(static) OMP_THREADS(threads)
+  for (int64_t r = 0; r < rows; ++r) quantize_row_q(x + r * ld_x, cols, (double)clip, 127, codes + r * cols, &scales[r]);
   return 0;
 }
 
@@ -169,27 +182,40 @@ int oracle_gemm_i32(const uint8_t* a_codes, const uint8_t* w_codes, int64_t M, i
   return overflow ? -1 : 0;
 }
 
+/* O-12: the same exact sum over int8 codes (no unpacking). */
+static int gemm_i32_q(const int8_t* qa, const int8_t* qw, int64_t M, int64_t N, int64_t K, int32_t* acc,
+                      int threads) {
+  int overflow = 0;
+#pragma omp parallel for schedule(static) OMP_THREADS(threads) reduction(| : overflow)
+  for (int64_t m = 0; m < M; ++m) {
+    for (int64_t n = 0; n < N; ++n) {
+      int64_t s = 0;
+      for (int64_t k = 0; k < K; ++k) s += (int64_t)qa[m * K + k] * (int64_t)qw[n * K + k];
+      if (s > INT32_MAX || s < INT32_MIN) overflow = 1;
+      acc[m * N + n] = (int32_t)s;
+    }
+  }
+  return overflow ? -1 : 0;
+}
+
+int oracle_gemm_i32_i8(const int8_t* a_codes, const int8_t* w_codes, int64_t M, int64_t N, int64_t K,
+                       int32_t* acc, int threads) {
+  if (M < 0 || N < 0 || K < 0) return -1;
+  return gemm_i32_q(a_codes, w_codes, M, N, K, acc, threads);
+}
+
 /* ------------------------------------------------------------------ O-5..O-7 */
 
 static double gelu_erf(double t) { return 0.5 * t * (1.0 + erf(t / sqrt(2.0))); }
 
-int oracle_w4a4_linear(const uint8_t* a_codes, const float* a_scales,
-                       const uint8_t* w_codes, const float* w_scales,
-                       int64_t M, int64_t N, int64_t K, int epi_kind,
-                       const uint16_t* bias, const uint16_t* residual,
-                       const uint16_t* gamma, const uint16_t* beta, double ln_eps, float clip,
-                       int32_t* out_i32, uint16_t* out_f16, uint8_t* out_codes, float* out_scales,
-                       int threads) {
-  if (M < 0 || N <= 0 || K <= 0 || !clip_is_f16(clip)) return -1;
-  if (epi_kind == ORACLE_EPI_I32 && !out_i32) return -1;
-  if (epi_kind == ORACLE_EPI_F16 && !out_f16) return -1;
-  if (epi_kind == ORACLE_EPI_GELU_Q4 && (!out_codes || !out_scales)) return -1;
-  if (epi_kind == ORACLE_EPI_RESLN_Q4 &&
-      (!out_codes || !out_scales || !out_f16 || !residual || !gamma || !beta))
-    return -1;
-  int32_t* acc = (int32_t*)malloc((size_t)(M * N > 0 ? M * N : 1) * sizeof(int32_t));
-  int rc = oracle_gemm_i32(a_codes, w_codes, M, N, K, acc, threads);
-  if (rc) { free(acc); return rc; }
+/* Dequant + bias + epilogue over an exact accumulator, requantizing to qmax = 7 (codes
+ * packed two per byte into out_codes4) or qmax = 127 (int8 codes into out_codes8). */
+static int linear_epilogue(const int32_t* acc, const float* a_scales, const float* w_scales,
+                           int64_t M, int64_t N, int epi_kind, const uint16_t* bias,
+                           const uint16_t* residual, const uint16_t* gamma, const uint16_t* beta,
+                           double ln_eps, float clip, int32_t* out_i32, uint16_t* out_f16,
+                           int qmax, uint8_t* out_codes4, int8_t* out_codes8, float* out_scales,
+                           int threads) {
   int64_t pb = (N + 1) / 2;
 #pragma omp parallel for schedule(static) OMP_THREADS(threads)
   for (int64_t m = 0; m < M; ++m) {
@@ -211,8 +237,9 @@ int oracle_w4a4_linear(const uint8_t* a_codes, const float* a_scales,
       case ORACLE_EPI_GELU_Q4:
         for (int64_t n = 0; n < N; ++n) y[n] = oracle_f64_to_f16(gelu_erf(t[n]));
         if (out_f16) memcpy(out_f16 + m * N, y, (size_t)N * sizeof(uint16_t));
-        quantize_row(y, N, (double)clip, q, &out_scales[m]);
-        pack_row(q, N, out_codes + m * pb);
+        quantize_row_q(y, N, (double)clip, qmax, q, &out_scales[m]);
+        if (qmax == 7) pack_row(q, N, out_codes4 + m * pb);
+        else memcpy(out_codes8 + m * N, q, (size_t)N);
         break;
       case ORACLE_EPI_RESLN_Q4: {
         double mu = 0.0, var = 0.0;
@@ -228,8 +255,9 @@ int oracle_w4a4_linear(const uint8_t* a_codes, const float* a_scales,
           y[n] = oracle_f64_to_f16((t[n] - mu) * rstd * oracle_f16_to_f64(gamma[n]) +
                                    oracle_f16_to_f64(beta[n]));
         memcpy(out_f16 + m * N, y, (size_t)N * sizeof(uint16_t));
-        quantize_row(y, N, (double)clip, q, &out_scales[m]);
-        pack_row(q, N, out_codes + m * pb);
+        quantize_row_q(y, N, (double)clip, qmax, q, &out_scales[m]);
+        if (qmax == 7) pack_row(q, N, out_codes4 + m * pb);
+        else memcpy(out_codes8 + m * N, q, (size_t)N);
         break;
       }
       default:
@@ -239,8 +267,53 @@ int oracle_w4a4_linear(const uint8_t* a_codes, const float* a_scales,
     free(y);
     free(q);
   }
-  free(acc);
   return (epi_kind >= ORACLE_EPI_I32 && epi_kind <= ORACLE_EPI_RESLN_Q4) ? 0 : -1;
+}
+
+static int epilogue_args_ok(int64_t M, int64_t N, int64_t K, int epi_kind, const uint16_t* residual,
+                            const uint16_t* gamma, const uint16_t* beta, float clip, const int32_t* out_i32,
+                            const uint16_t* out_f16, const void* out_codes, const float* out_scales) {
+  if (M < 0 || N <= 0 || K <= 0 || !clip_is_f16(clip)) return 0;
+  if (epi_kind == ORACLE_EPI_I32 && !out_i32) return 0;
+  if (epi_kind == ORACLE_EPI_F16 && !out_f16) return 0;
+  if (epi_kind == ORACLE_EPI_GELU_Q4 && (!out_codes || !out_scales)) return 0;
+  if (epi_kind == ORACLE_EPI_RESLN_Q4 && (!out_codes || !out_scales || !out_f16 || !residual || !gamma || !beta))
+    return 0;
+  return 1;
+}
+
+int oracle_w4a4_linear(const uint8_t* a_codes, const float* a_scales,
+                       const uint8_t* w_codes, const float* w_scales,
+                       int64_t M, int64_t N, int64_t K, int epi_kind,
+                       const uint16_t* bias, const uint16_t* residual,
+                       const uint16_t* gamma, const uint16_t* beta, double ln_eps, float clip,
+                       int32_t* out_i32, uint16_t* out_f16, uint8_t* out_codes, float* out_scales,
+                       int threads) {
+  if (!epilogue_args_ok(M, N, K, epi_kind, residual, gamma, beta, clip, out_i32, out_f16, out_codes, out_scales))
+    return -1;
+  int32_t* acc = (int32_t*)malloc((size_t)(M * N > 0 ? M * N : 1) * sizeof(int32_t));
+  int rc = oracle_gemm_i32(a_codes, w_codes, M, N, K, acc, threads);
+  if (!rc)
+    rc = linear_epilogue(acc, a_scales, w_scales, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, clip,
+                         out_i32, out_f16, 7, out_codes, NULL, out_scales, threads);
+  free(acc);
+  return rc;
+}
+
+int oracle_w8a8_linear(const int8_t* a_codes, const float* a_scales, const int8_t* w_codes,
+                       const float* w_scales, int64_t M, int64_t N, int64_t K, int epi_kind,
+                       const uint16_t* bias, const uint16_t* residual, const uint16_t* gamma,
+                       const uint16_t* beta, double ln_eps, float clip, int32_t* out_i32,
+                       uint16_t* out_f16, int8_t* out_codes, float* out_scales, int threads) {
+  if (!epilogue_args_ok(M, N, K, epi_kind, residual, gamma, beta, clip, out_i32, out_f16, out_codes, out_scales))
+    return -1;
+  int32_t* acc = (int32_t*)malloc((size_t)(M * N > 0 ? M * N : 1) * sizeof(int32_t));
+  int rc = gemm_i32_q(a_codes, w_codes, M, N, K, acc, threads);
+  if (!rc)
+    rc = linear_epilogue(acc, a_scales, w_scales, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, clip,
+                         out_i32, out_f16, 127, NULL, out_codes, out_scales, threads);
+  free(acc);
+  return rc;
 }
 
 /* ------------------------------------------------------------------ O-8 attention */

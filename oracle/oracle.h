@@ -116,6 +116,24 @@ int oracle_encoder_layer(const oracle_layer_cfg* cfg, const oracle_layer_weights
                          const float* hs_in, uint16_t* h_out, uint8_t* hq_out, float* hs_out,
                          const oracle_taps* taps, int threads);
 
+/* O-11..O-13  W8A8 variant of the same linear ("i8-qall": the
+ * paper's INT8 baseline that INT4 is measured against).  Identical definitions at
+ * b = 8 bits, qmax = 2^(b-1) - 1 = 127 (PAPER.md:703-708 with reading R1 at b = 8):
+ *   O-11 quantize_rows_i8: q = rhe(127 x'/a) exactly, scale = fl32(a/127); codes int8
+ *        [rows, cols], one per byte (no packing)
+ *   O-12 gemm_i32_i8: acc = sum_k qa qw over int8 codes, int64, checked to fit int32
+ *   O-13 w8a8_linear: O-5..O-7 on that accumulator; GELU_Q4 / RESLN_Q4 kinds requantize
+ *        with O-11 (int8 codes) instead of O-1 */
+int oracle_quantize_rows_i8(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x,
+                            float clip, int8_t* codes, float* scales, int threads);
+int oracle_gemm_i32_i8(const int8_t* a_codes, const int8_t* w_codes, int64_t M, int64_t N, int64_t K,
+                       int32_t* acc, int threads);
+int oracle_w8a8_linear(const int8_t* a_codes, const float* a_scales, const int8_t* w_codes,
+                       const float* w_scales, int64_t M, int64_t N, int64_t K, int epi_kind,
+                       const uint16_t* bias, const uint16_t* residual, const uint16_t* gamma,
+                       const uint16_t* beta, double ln_eps, float clip, int32_t* out_i32,
+                       uint16_t* out_f16, int8_t* out_codes, float* out_scales, int threads);
+
 #ifdef __cplusplus
 }
 #endif
