@@ -137,6 +137,33 @@ Q4_API q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, /
                          void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------
+ * W8A8 baseline: the same linear with 8-bit codes -- the paper's
+ * INT8 comparison point ("i8-qall"; INT4 vs INT8 GEMM, Fig.
+ * gemm_perf).  Definitions are those above at b = 8 bits (oracle O-11..O-13):
+ *
+ * q4_quantize_rows_i8: PAPER.md:703-708 with S = amax/127 (R1 at b = 8), round half to
+ *   even (R2), exact evaluation (R3).  codes [rows, cols] int8 (one per byte, in
+ *   [-127, 127]); scales [rows] fp32 = fl32(amax/127); all-zero row -> scale 1, codes 0.
+ *   Requirements as q4_quantize_rows, codes 8-byte aligned.
+ *
+ * q4_w8a8_linear: acc = sum_k qa[m,k] qw[n,k] exact in INT32 over int8 codes
+ *   a_codes [M, K] and w_codes [N, K] (nn.Linear [out, in] orientation, K-major, no
+ *   packing), then the Q4_EPI_* epilogues of q4_w4a4_linear with the requantizing kinds
+ *   (GELU_Q4 / RESLN_Q4) writing int8 codes out_codes [M, N] (q4_quantize_rows_i8 of the
+ *   fp16 y) and scales amax/127.  Both operands are TMA'd straight into the MMA stage
+ *   (no unpack).  epi->mainloop must be AUTO or TCGEN05; epi->w_i8 is ignored.
+ *   Requirements: N % 32 == 0 (row epilogues: N % 64 == 0),
+ *   K % 128 == 0, K <= 131072 (|acc| <= 128^2 K < 2^31), pointers 16-byte aligned;
+ *   workspace: q4_w8a8_linear_workspace (row epilogues).  Errors as q4_w4a4_linear. */
+Q4_API q4_status q4_quantize_rows_i8(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x,
+                                     float clip, int8_t* codes, float* scales, void* stream);
+Q4_API size_t q4_w8a8_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind);
+Q4_API q4_status q4_w8a8_linear(const int8_t* a_codes, const float* a_scales, /* [M,K], [M] */
+                                const int8_t* w_codes, const float* w_scales, /* [N,K], [N] */
+                                int64_t M, int64_t N, int64_t K, const q4_epilogue* epi,
+                                void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
  * a2' Offline weight prepack (once per weight, not on the forward path): packed INT4 codes
  * w_codes [N, K/2] -> w_i8 [N, K] int8 holding 16*q in the K order of the on-chip
  * activation unpack (per 32-element group: the 16 even-k values, then the 16 odd-k).

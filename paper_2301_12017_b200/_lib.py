@@ -20,7 +20,7 @@ EXPORTS = (
     "q4_last_error", "q4_version", "q4_launch_count", "q4_quantize_rows", "q4_prepack_weights",
     "q4_w4a4_linear_workspace", "q4_w4a4_linear", "q4_attention_f16_q4",
     "q4_encoder_layer_workspace", "q4_encoder_layer", "q4_encoder_stack_workspace",
-    "q4_encoder_stack",
+    "q4_encoder_stack", "q4_quantize_rows_i8", "q4_w8a8_linear_workspace", "q4_w8a8_linear",
 )
 
 
@@ -80,6 +80,10 @@ def lib():
         L.q4_w4a4_linear_workspace.restype = SZ
         L.q4_w4a4_linear.argtypes = [P, P, P, P, I64, I64, I64, C.POINTER(Epilogue), P, SZ, P]
         L.q4_attention_f16_q4.argtypes = [P, I64, I64, I32, I32, P, P, P, P]
+        L.q4_quantize_rows_i8.argtypes = [P, I64, I64, I64, F, P, P, P]
+        L.q4_w8a8_linear_workspace.argtypes = [I64, I64, I64, I32]
+        L.q4_w8a8_linear_workspace.restype = SZ
+        L.q4_w8a8_linear.argtypes = [P, P, P, P, I64, I64, I64, C.POINTER(Epilogue), P, SZ, P]
         L.q4_encoder_layer_workspace.argtypes = [C.POINTER(LayerCfg), I64, I64]
         L.q4_encoder_layer_workspace.restype = SZ
         L.q4_encoder_layer.argtypes = [C.POINTER(LayerCfg), C.POINTER(LayerWeights), I64, I64, P, P, P,
@@ -91,7 +95,8 @@ def lib():
         for name in EXPORTS:
             L[name].restype = L[name].restype if name in (
                 "q4_last_error", "q4_version", "q4_launch_count", "q4_w4a4_linear_workspace",
-                "q4_encoder_layer_workspace", "q4_encoder_stack_workspace") else C.c_int
+                "q4_encoder_layer_workspace", "q4_encoder_stack_workspace",
+                "q4_w8a8_linear_workspace") else C.c_int
         _lib = L
     return _lib
 

@@ -373,6 +373,57 @@ Q4_DEV uint32_t requant8_nofix(const uint32_t (&h)[4], float r7, float& dmax) {
   return (ev & 0x0F0F0F0Fu) | ((od << 4) & 0xF0F0F0F0u);
 }
 
+// ------------------------------------------------------------------ 8-bit codes (W8A8)
+// The same quantizer at b = 8 bits (qmax = 127; oracle O-11): n = rhe(127 y / amax).
+// p = y * RN(127/amax) differs from the exact 127 y / amax by <= 127 * 2^-23 < 1.6e-5, so
+// rint(p) is exact unless p is within 1e-4 of a half-integer; there the exact FMA
+// tie-break decides (127 y and amax * h are exact in the fma: 18- and 20-bit products).
+Q4_DEV int requant_code_i8(float y, float a, float rq) {
+  const float p = y * rq;
+  const float s = p + 12582912.0f;
+  const float fn = s - 12582912.0f;
+  int n = __float_as_int(s) - 0x4B400000;
+  const float d0 = p - fn;
+  if (fabsf(d0) > 0.4999f) {
+    const float h = fn + copysignf(0.5f, d0);
+    const float e = fmaf(-a, h, 127.0f * y);
+    const int lo = (int)floorf(h), hi = lo + 1;
+    n = e > 0.f ? hi : (e < 0.f ? lo : ((lo & 1) ? hi : lo));
+  }
+  return n;
+}
+// 8 fp16 values (4 packed words) -> 8 int8 codes (2 words, element i in byte i).  The low
+// byte of s = p + 1.5*2^23 is rint(p) in two's complement; PRMT gathers the bytes.
+Q4_DEV uint2 requant8_i8(const uint32_t (&h)[4], float amax, float rq, float clip) {
+  if (!(amax > 0.f)) return make_uint2(0u, 0u);
+  float2 y[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    y[j] = unpack_half2(h[j]);
+    if (clip > 0.f) y[j] = make_float2(fminf(fmaxf(y[j].x, -clip), clip), fminf(fmaxf(y[j].y, -clip), clip));
+  }
+  uint32_t sb[8];
+  float dmax = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 p = fmul2(y[j], f2(rq));
+    const float2 sm = fadd2(p, f2(12582912.0f));
+    const float2 d = ffma2(fadd2(sm, f2(-12582912.0f)), f2(-1.f), p);
+    dmax = fmaxf(dmax, fmaxf(fabsf(d.x), fabsf(d.y)));
+    sb[2 * j] = __float_as_uint(sm.x);
+    sb[2 * j + 1] = __float_as_uint(sm.y);
+  }
+  if (dmax > 0.4999f) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      sb[2 * j] = (uint32_t)requant_code_i8(y[j].x, amax, rq);
+      sb[2 * j + 1] = (uint32_t)requant_code_i8(y[j].y, amax, rq);
+    }
+  }
+  return make_uint2(prmt(prmt(sb[0], sb[1], 0x40u), prmt(sb[2], sb[3], 0x40u), 0x5410u),
+                    prmt(prmt(sb[4], sb[5], 0x40u), prmt(sb[6], sb[7], 0x40u), 0x5410u));
+}
+
 // GELU (erf form, reading R11) for two values, ~12 ops/element, |err| <= 5e-6 vs fp64
 // (float32 evaluation, scripts/fit_gelu.py):
 // GELU(x) = max(x,0) - |x| Q(|x|) with Q the normal upper tail, Q(t) = exp(-t^2/2) R(t) and

@@ -77,11 +77,13 @@ template <int KIND> struct EpiCfg {
 // BI8: B (weights) arrives prepacked as int8 "16*q" in the MMA's K order
 // (q4_prepack_weights) and is TMA'd straight into the swizzled operand stage; only the
 // activation operand A is unpacked on chip.
-template <int TN, bool BI8>
+// A8 (W8A8 baseline, with BI8): A arrives as int8 codes too and is TMA'd straight into the
+// operand stage like B -- no packed ring, no on-chip unpack.
+template <int TN, bool BI8, bool A8 = false>
 struct TcCfg {
   static constexpr int BM = 128, BK = 128;  // BK in int8 elements = 64 packed bytes
-  static constexpr int SP = BI8 ? 4 : 3, SU = BI8 ? 3 : 2;  // packed / unpacked smem stages
-  static constexpr int A_PK = BM * 64, B_PK = BI8 ? 0 : TN * 64;
+  static constexpr int SP = A8 ? 1 : BI8 ? 4 : 3, SU = BI8 ? 3 : 2;  // packed / unpacked smem stages
+  static constexpr int A_PK = A8 ? 0 : BM * 64, B_PK = BI8 ? 0 : TN * 64;
   static constexpr int A_UN = BM * 128, B_UN = TN * 128;
   static constexpr int UN_STAGE = A_UN + B_UN, PK_STAGE = A_PK + B_PK;
   static constexpr int OFF_UN = 0;
@@ -359,10 +361,11 @@ Q4_DEV void slab_load16(uint8_t* stg, const uint8_t* gbase, int row0, int r0, in
   }
 }
 
-template <int TN, int KIND, bool BI8>
+template <int TN, int KIND, bool BI8, bool A8>
 __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     w4a4_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
-  using C = TcCfg<TN, BI8>;
+  static_assert(!A8 || BI8, "W8A8 takes int8 weights through the BI8 path");
+  using C = TcCfg<TN, BI8, A8>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full_p = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int i = 0; i < C::SP; ++i) { mbar_init(&full_p[i], 1); mbar_init(&empty_p[i], 4); }
-    for (int i = 0; i < C::SU; ++i) { mbar_init(&full_u[i], BI8 ? 5 : 4); mbar_init(&empty_u[i], 1); }
+    for (int i = 0; i < C::SU; ++i) { mbar_init(&full_u[i], A8 ? 1 : BI8 ? 5 : 4); mbar_init(&empty_u[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EpiCfg<KIND>::EPW); }
     fence_mbar_init();
   }
@@ -410,6 +413,18 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     if (lane == 0) {
       uint32_t g = 0;
       while (it.next(mb, nb)) {
+        if constexpr (A8) {
+          // both int8 operands straight into the swizzled MMA stage
+          for (int kb = 0; kb < KB; ++kb, ++g) {
+            const int su = g % C::SU;
+            mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
+            uint8_t* ub = smem + C::OFF_UN + su * C::UN_STAGE;
+            mbar_arrive_expect_tx(&full_u[su], (uint32_t)C::UN_STAGE);
+            tma_load_2d(ub, &tmA, &full_u[su], kb * 128, mb * C::BM);
+            tma_load_2d(ub + C::A_UN, &tmB, &full_u[su], kb * 128, nb * TN);
+          }
+          continue;
+        }
         for (int kb = 0; kb < KB; ++kb, ++g) {
           const int s = g % C::SP;
           mbar_wait(&empty_p[s], ((g / C::SP) & 1u) ^ 1u);
@@ -481,7 +496,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     uint32_t g = 0;
     // profiling only (Q4_TRACE): k-block phase durations of thread 64, trace slot 63 of this CTA
     unsigned long long* utr = (p.trace && t == 0) ? p.trace + ((size_t)blockIdx.x * 64 + 63) * 8 : nullptr;
-    while (it.next(mb, nb)) {
+    while (!A8 && it.next(mb, nb)) {
       for (int kb = 0; kb < KB; ++kb, ++g) {
         const int s = g % C::SP, su = g % C::SU;
         const unsigned long long u0 = utr ? gtimer() : 0;
@@ -574,7 +589,8 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
       const bool row_ok = gm < p.M;
       const int c0 = nb * TN;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + b * TN;
-      const float sa = row_ok ? p.a_scales[gm] * (1.0f / 256.0f) : 0.f;
+      // W4A4: the unpacked operands are 16 q, so the accumulator is 256 x the code sum
+      const float sa = row_ok ? p.a_scales[gm] * (A8 ? 1.0f : 1.0f / 256.0f) : 0.f;
       const float2 sa2 = f2(sa);
       const uint4* resp = nullptr;
       uint4 rr[4];  // RESLN: residual of this thread's current chunk (first one loaded before the wait)
@@ -601,8 +617,9 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
             tmem_wait_ld();
             if (row_ok) {
               int4* o = reinterpret_cast<int4*>(p.out_i32 + (size_t)gm * N + c0 + c);
-              o[0] = make_int4((int)v[0] >> 8, (int)v[1] >> 8, (int)v[2] >> 8, (int)v[3] >> 8);
-              o[1] = make_int4((int)v[4] >> 8, (int)v[5] >> 8, (int)v[6] >> 8, (int)v[7] >> 8);
+              constexpr int SH = A8 ? 0 : 8;
+              o[0] = make_int4((int)v[0] >> SH, (int)v[1] >> SH, (int)v[2] >> SH, (int)v[3] >> SH);
+              o[1] = make_int4((int)v[4] >> SH, (int)v[5] >> SH, (int)v[6] >> SH, (int)v[7] >> SH);
             }
           }
         }
@@ -777,6 +794,31 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
         stamp(5);
         for (int kk = 0; kk < ntn; ++kk) amax = fmaxf(amax, __ldcg(&p.xamax[((size_t)mb * ntn + kk) * 128 + r]));
         // pass B: codes (R1-R3), packed, staged, coalesced stores
+        if constexpr (A8) {
+          // W8A8: int8 codes (O-11), 64 bytes per 64-column slab row
+          const float rq = amax > 0.f ? __fdiv_rn(127.0f, amax) : 0.f;
+          for (int k = 0; k < NSL; ++k) {
+#pragma unroll
+            for (int jj = 0; jj < 2; jj += NS) {
+              const int j = 2 * k + jj + sub;
+              uint32_t h[16];
+              tmem_ld16(tbase + 32 * j, h);
+              tmem_wait_ld();
+              uint2 c8[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const uint32_t hk[4] = {h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]};
+                c8[u] = requant8_i8(hk, amax, rq, clip);
+              }
+              *reinterpret_cast<uint4*>(stg + slab_off(lane, 2 * (j & 1))) = make_uint4(c8[0].x, c8[0].y, c8[1].x, c8[1].y);
+              *reinterpret_cast<uint4*>(stg + slab_off(lane, 2 * (j & 1) + 1)) = make_uint4(c8[2].x, c8[2].y, c8[3].x, c8[3].y);
+            }
+            slab_sync();
+            slab_store16(stg, p.out_codes, m0 + q * 32, RS * sub, RS, p.M, (size_t)N, (size_t)(c0 + 64 * k), 64, lane);
+            slab_sync();
+          }
+          if (row_ok && nb == 0 && sub == 0) p.out_scales[gm] = amax > 0.f ? __fdiv_rn(amax, 127.0f) : 1.0f;
+        } else {
         const float r7 = amax > 0.f ? __fdiv_rn(7.0f, amax) : 0.f;
         for (int k = 0; k < NSL; ++k) {
 #pragma unroll
@@ -795,6 +837,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
           slab_sync();
         }
         if (row_ok && nb == 0 && sub == 0) p.out_scales[gm] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
+        }
       }
       stamp(6);
       // accumulator buffer b may be overwritten by the MMA of tile tcount + 2
@@ -858,10 +901,10 @@ int num_sms() {
   return n;
 }
 
-template <int TN, int KIND, bool BI8>
+template <int TN, int KIND, bool BI8, bool A8>
 cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {
-  using C = TcCfg<TN, BI8>;
-  auto kern = w4a4_tc_kernel<TN, KIND, BI8>;
+  using C = TcCfg<TN, BI8, A8>;
+  auto kern = w4a4_tc_kernel<TN, KIND, BI8, A8>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -872,7 +915,9 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   const uint64_t kb = (uint64_t)g.K / 2;
   const bool okb = BI8 ? make_tmap(&tb, g.w_i8, (uint64_t)g.N, (uint64_t)g.K, TN, 128, true)
                        : make_tmap(&tb, g.w_codes, (uint64_t)g.N, kb, TN, 64);
-  if (!make_tmap(&ta, g.a_codes, (uint64_t)g.M, kb, 128, 64) || !okb) {
+  const bool oka = A8 ? make_tmap(&ta, g.a_i8, (uint64_t)g.M, (uint64_t)g.K, 128, 128, true)
+                     : make_tmap(&ta, g.a_codes, (uint64_t)g.M, kb, 128, 64);
+  if (!oka || !okb) {
     *why = "cuTensorMapEncodeTiled failed (driver entry point or alignment)";
     return cudaErrorInvalidValue;
   }
@@ -929,19 +974,23 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   return cudaGetLastError();
 }
 
-template <int TN, bool BI8>
+template <int TN, bool BI8, bool A8 = false>
 cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s, const char** why) {
   switch (g.kind) {
-    case EPI_I32: return run_tc<TN, EPI_I32, BI8>(g, ws, wsb, s, why);
-    case EPI_F16: return run_tc<TN, EPI_F16, BI8>(g, ws, wsb, s, why);
-    case EPI_GELU_Q4: return run_tc<TN, EPI_GELU_Q4, BI8>(g, ws, wsb, s, why);
-    case EPI_RESLN_Q4: return run_tc<TN, EPI_RESLN_Q4, BI8>(g, ws, wsb, s, why);
+    case EPI_I32: return run_tc<TN, EPI_I32, BI8, A8>(g, ws, wsb, s, why);
+    case EPI_F16: return run_tc<TN, EPI_F16, BI8, A8>(g, ws, wsb, s, why);
+    case EPI_GELU_Q4: return run_tc<TN, EPI_GELU_Q4, BI8, A8>(g, ws, wsb, s, why);
+    case EPI_RESLN_Q4: return run_tc<TN, EPI_RESLN_Q4, BI8, A8>(g, ws, wsb, s, why);
   }
   *why = "unknown epilogue kind";
   return cudaErrorInvalidValue;
 }
 template <int TN>
 cudaError_t run_tc_kind(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s, const char** why) {
+  if (g.a_i8) {
+    if (!g.w_i8) { *why = "W8A8 needs int8 weight codes"; return cudaErrorInvalidValue; }
+    return run_tc_kind2<TN, true, true>(g, ws, wsb, s, why);
+  }
   if (g.w_i8) return run_tc_kind2<TN, true>(g, ws, wsb, s, why);
   return run_tc_kind2<TN, false>(g, ws, wsb, s, why);
 }

@@ -38,6 +38,8 @@ cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, siz
 
 struct GemmArgs {
   const uint8_t* a_codes;  // [M, K/2]
+  const int8_t* a_i8;      // W8A8: int8 activation codes [M, K] (then w_i8 holds int8 weight codes
+                           // in natural K order and requant kinds write int8 codes [M, N]); else nullptr
   const float* a_scales;   // [M]
   const uint8_t* w_codes;  // [N, K/2]
   const int8_t* w_i8;      // [N, K] prepacked int8 (q4_prepack_weights) or nullptr
@@ -59,6 +61,8 @@ struct GemmArgs {
 cudaError_t launch_prepack_weights(const uint8_t* w_codes, int64_t N, int64_t K, int8_t* w_i8, cudaStream_t s);
 cudaError_t launch_quantize_rows(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
                                  uint8_t* codes, float* scales, cudaStream_t s);
+cudaError_t launch_quantize_rows_i8(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
+                                    int8_t* codes, float* scales, cudaStream_t s);
 // Returns cudaErrorNotSupported for shapes the tcgen05 path cannot take (message in *why).
 // Row epilogues (GELU_Q4 / RESLN_Q4) need `ws` of tc_workspace_bytes(M, N, tc_tile_n(...)).
 cudaError_t launch_w4a4_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why);

@@ -30,6 +30,7 @@ q4_status cuda_fail(cudaError_t e, const char* where) {
 }
 bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 bool al4(const void* p) { return ((uintptr_t)p & 3) == 0; }
+bool al8(const void* p) { return ((uintptr_t)p & 7) == 0; }
 
 bool clip_ok(float c) {
   if (c == 0.f) return true;
@@ -65,6 +66,97 @@ q4_status q4_quantize_rows(const uint16_t* x, int64_t rows, int64_t cols, int64_
   cudaError_t e = q4::launch_quantize_rows(reinterpret_cast<const __half*>(x), rows, (int)cols, ld_x, clip,
                                            codes, scales, (cudaStream_t)stream);
   return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_quantize_rows");
+}
+
+q4_status q4_quantize_rows_i8(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x, float clip,
+                              int8_t* codes, float* scales, void* stream) {
+  g_err[0] = 0;
+  if (rows < 0 || cols <= 0 || ld_x < cols)
+    return fail(Q4_ESHAPE, "q4_quantize_rows_i8: rows=%lld cols=%lld ld_x=%lld (need rows>=0, cols>0, ld_x>=cols)",
+                (long long)rows, (long long)cols, (long long)ld_x);
+  if (cols % 8 || ld_x % 8)
+    return fail(Q4_ESHAPE, "q4_quantize_rows_i8: cols=%lld and ld_x=%lld must be multiples of 8",
+                (long long)cols, (long long)ld_x);
+  if (cols > (1 << 30)) return fail(Q4_ESHAPE, "q4_quantize_rows_i8: cols=%lld too large", (long long)cols);
+  if (rows == 0) return Q4_OK;
+  if (!x || !codes || !scales) return fail(Q4_EINVAL, "q4_quantize_rows_i8: NULL x/codes/scales");
+  if (!al16(x) || !al8(codes) || !al4(scales))
+    return fail(Q4_EALIGN, "q4_quantize_rows_i8: x must be 16-byte aligned, codes 8-byte, scales 4-byte");
+  if (!clip_ok(clip)) return fail(Q4_EINVAL, "q4_quantize_rows_i8: clip=%g is not 0 or a positive fp16 value", clip);
+  cudaError_t e = q4::launch_quantize_rows_i8(reinterpret_cast<const __half*>(x), rows, (int)cols, ld_x, clip,
+                                              codes, scales, (cudaStream_t)stream);
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_quantize_rows_i8");
+}
+
+size_t q4_w8a8_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind) {
+  return q4_w4a4_linear_workspace(M, N, K, kind);
+}
+
+q4_status q4_w8a8_linear(const int8_t* a_codes, const float* a_scales, const int8_t* w_codes,
+                         const float* w_scales, int64_t M, int64_t N, int64_t K, const q4_epilogue* epi,
+                         void* workspace, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (!epi) return fail(Q4_EINVAL, "q4_w8a8_linear: epi is NULL");
+  if (M < 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1 << 24))
+    return fail(Q4_ESHAPE, "q4_w8a8_linear: bad shape M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
+  if (N % 32) return fail(Q4_ESHAPE, "q4_w8a8_linear: N=%lld must be a multiple of 32", (long long)N);
+  if (K % 128) return fail(Q4_ESHAPE, "q4_w8a8_linear: K=%lld must be a multiple of 128 (one TMA k-block)", (long long)K);
+  if (K > 131072) return fail(Q4_ESHAPE, "q4_w8a8_linear: K=%lld > 131072 would break the INT32 accumulator bound", (long long)K);
+  const int kind = epi->kind;
+  if (kind < Q4_EPI_I32 || kind > Q4_EPI_RESLN_Q4) return fail(Q4_EINVAL, "q4_w8a8_linear: unknown epilogue kind %d", kind);
+  if (epi->mainloop != Q4_MAINLOOP_AUTO && epi->mainloop != Q4_MAINLOOP_TCGEN05)
+    return fail(Q4_EUNSUPPORTED, "q4_w8a8_linear: mainloop %d (W8A8 runs on tcgen05 only)", epi->mainloop);
+  if (M == 0) return Q4_OK;
+  if (!a_codes || !a_scales || !w_codes || !w_scales)
+    return fail(Q4_EINVAL, "q4_w8a8_linear: NULL operand (a_codes/a_scales/w_codes/w_scales)");
+  if (!al16(a_codes) || !al16(w_codes) || !al4(a_scales) || !al16(w_scales))
+    return fail(Q4_EALIGN, "q4_w8a8_linear: codes and w_scales must be 16-byte aligned, a_scales 4-byte aligned");
+  if ((epi->bias && !al4(epi->bias)) || (epi->gamma && !al4(epi->gamma)) || (epi->beta && !al4(epi->beta)))
+    return fail(Q4_EALIGN, "q4_w8a8_linear: bias/gamma/beta must be 4-byte aligned");
+  switch (kind) {
+    case Q4_EPI_I32:
+      if (!epi->out_i32 || !al16(epi->out_i32)) return fail(Q4_EINVAL, "q4_w8a8_linear(I32): out_i32 NULL or not 16-byte aligned");
+      break;
+    case Q4_EPI_F16:
+      if (!epi->out_f16 || !al16(epi->out_f16)) return fail(Q4_EINVAL, "q4_w8a8_linear(F16): out_f16 NULL or not 16-byte aligned");
+      break;
+    case Q4_EPI_GELU_Q4:
+      if (!epi->out_codes || !epi->out_scales) return fail(Q4_EINVAL, "q4_w8a8_linear(GELU_Q): out_codes/out_scales NULL");
+      if (!al16(epi->out_codes) || (epi->out_f16 && !al16(epi->out_f16)))
+        return fail(Q4_EALIGN, "q4_w8a8_linear(GELU_Q): outputs must be 16-byte aligned");
+      break;
+    case Q4_EPI_RESLN_Q4:
+      if (!epi->out_codes || !epi->out_scales || !epi->out_f16 || !epi->residual || !epi->gamma || !epi->beta)
+        return fail(Q4_EINVAL, "q4_w8a8_linear(RESLN_Q): out_f16/out_codes/out_scales/residual/gamma/beta must be non-NULL");
+      if (!al16(epi->out_codes) || !al16(epi->out_f16) || !al16(epi->residual))
+        return fail(Q4_EALIGN, "q4_w8a8_linear(RESLN_Q): out_f16/out_codes/residual must be 16-byte aligned");
+      if (!(epi->ln_eps >= 0.f)) return fail(Q4_EINVAL, "q4_w8a8_linear(RESLN_Q): ln_eps=%g", epi->ln_eps);
+      break;
+  }
+  if (!clip_ok(epi->requant_clip)) return fail(Q4_EINVAL, "q4_w8a8_linear: requant_clip=%g is not 0 or a positive fp16 value", epi->requant_clip);
+  if (kind == Q4_EPI_GELU_Q4 || kind == Q4_EPI_RESLN_Q4) {
+    if (N % 64) return fail(Q4_ESHAPE, "q4_w8a8_linear: N=%lld must be a multiple of 64 for row epilogues", (long long)N);
+    const size_t need = q4_w8a8_linear_workspace(M, N, K, kind);
+    if (!workspace || ws_bytes < need)
+      return fail(Q4_EINVAL, "q4_w8a8_linear: workspace %zu bytes < required %zu (q4_w8a8_linear_workspace)", ws_bytes, need);
+    if (!al16(workspace)) return fail(Q4_EALIGN, "q4_w8a8_linear: workspace must be 16-byte aligned");
+  }
+  q4::GemmArgs g;
+  g.a_codes = nullptr; g.a_i8 = a_codes; g.a_scales = a_scales; g.w_codes = nullptr; g.w_i8 = w_codes;
+  g.w_scales = w_scales;
+  g.M = (int)M; g.N = (int)N; g.K = (int)K; g.kind = kind; g.mainloop = Q4_MAINLOOP_TCGEN05;
+  g.bias = reinterpret_cast<const __half*>(epi->bias);
+  g.residual = reinterpret_cast<const __half*>(epi->residual);
+  g.gamma = reinterpret_cast<const __half*>(epi->gamma);
+  g.beta = reinterpret_cast<const __half*>(epi->beta);
+  g.ln_eps = epi->ln_eps; g.clip = epi->requant_clip;
+  g.out_i32 = epi->out_i32; g.out_f16 = reinterpret_cast<__half*>(epi->out_f16);
+  g.out_codes = epi->out_codes; g.out_scales = epi->out_scales;
+  const char* why = "";
+  cudaError_t e = q4::launch_w4a4_tc(g, workspace, ws_bytes, (cudaStream_t)stream, &why);
+  if (e == cudaErrorNotSupported) return fail(Q4_EUNSUPPORTED, "q4_w8a8_linear: %s (M=%lld N=%lld K=%lld)", why, (long long)M, (long long)N, (long long)K);
+  if (e != cudaSuccess) return fail(Q4_ECUDA, "q4_w8a8_linear: %s %s", cudaGetErrorString(e), why);
+  return Q4_OK;
 }
 
 size_t q4_w4a4_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind) {
@@ -122,7 +214,7 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
     if (!al16(workspace)) return fail(Q4_EALIGN, "q4_w4a4_linear: workspace must be 16-byte aligned");
   }
   q4::GemmArgs g;
-  g.a_codes = a_codes; g.a_scales = a_scales; g.w_codes = w_codes; g.w_scales = w_scales;
+  g.a_codes = a_codes; g.a_i8 = nullptr; g.a_scales = a_scales; g.w_codes = w_codes; g.w_scales = w_scales;
   g.M = (int)M; g.N = (int)N; g.K = (int)K; g.kind = kind; g.mainloop = epi->mainloop;
   g.bias = reinterpret_cast<const __half*>(epi->bias);
   g.residual = reinterpret_cast<const __half*>(epi->residual);

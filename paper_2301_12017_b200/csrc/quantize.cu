@@ -1,5 +1,6 @@
 // quantize.cu -- a1/a2: symmetric per-row INT4 quantize + pack (PAPER.md:703-708,
 // 517-522; readings R1-R3, R5, R10).  Memory-bound: 2 B/elem in, 0.5 B/elem + 4 B/row out.
+// Also the 8-bit variant of the W8A8 baseline (int8 codes, 1 B/elem out; oracle O-11).
 //
 // One warp per row.  Each lane owns 16-byte vectors (8 halves) v = lane + 32*i, kept
 // in registers between the two passes (warp-shuffle max-abs, then codes), so x is read
@@ -10,7 +11,8 @@
 
 namespace q4 {
 
-template <int MAXV>
+// I8: the W8A8 variant (oracle O-11): int8 codes, one per byte, scale amax/127.
+template <int MAXV, bool I8>
 __global__ void __launch_bounds__(256) quantize_rows_kernel(const __half* __restrict__ x,
                                                             int64_t rows, int cols, int64_t ld_x,
                                                             float clip, uint8_t* __restrict__ codes,
@@ -43,20 +45,24 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(const __half* __rest
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-  uint32_t* cr = reinterpret_cast<uint32_t*>(codes + row * (int64_t)(cols >> 1));
-  const float r7 = amax > 0.f ? __fdiv_rn(7.0f, amax) : 0.f;
+  constexpr float QM = I8 ? 127.0f : 7.0f;
+  const float rq = amax > 0.f ? __fdiv_rn(QM, amax) : 0.f;
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
     const int vi = lane + 32 * i;
     if (vi < nvec) {
       const uint32_t hh[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-      cr[vi] = requant8(hh, amax, r7, clip);
+      if constexpr (I8)
+        reinterpret_cast<uint2*>(codes + row * (int64_t)cols)[vi] = requant8_i8(hh, amax, rq, clip);
+      else
+        reinterpret_cast<uint32_t*>(codes + row * (int64_t)(cols >> 1))[vi] = requant8(hh, amax, rq, clip);
     }
   }
-  if (lane == 0) scales[row] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
+  if (lane == 0) scales[row] = amax > 0.f ? __fdiv_rn(amax, QM) : 1.0f;
 }
 
 // Rows longer than 32*16*8 = 4096: two passes over global memory.
+template <bool I8>
 __global__ void __launch_bounds__(256) quantize_rows_long_kernel(const __half* __restrict__ x,
                                                                  int64_t rows, int cols,
                                                                  int64_t ld_x, float clip,
@@ -81,14 +87,17 @@ __global__ void __launch_bounds__(256) quantize_rows_long_kernel(const __half* _
     }
   }
   for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-  uint32_t* cr = reinterpret_cast<uint32_t*>(codes + row * (int64_t)(cols >> 1));
-  const float r7 = amax > 0.f ? __fdiv_rn(7.0f, amax) : 0.f;
+  constexpr float QM = I8 ? 127.0f : 7.0f;
+  const float rq = amax > 0.f ? __fdiv_rn(QM, amax) : 0.f;
   for (int vi = lane; vi < nvec; vi += 32) {
     const uint4 vv = __ldg(xr + vi);
     const uint32_t hh[4] = {vv.x, vv.y, vv.z, vv.w};
-    cr[vi] = requant8(hh, amax, r7, clip);
+    if constexpr (I8)
+      reinterpret_cast<uint2*>(codes + row * (int64_t)cols)[vi] = requant8_i8(hh, amax, rq, clip);
+    else
+      reinterpret_cast<uint32_t*>(codes + row * (int64_t)(cols >> 1))[vi] = requant8(hh, amax, rq, clip);
   }
-  if (lane == 0) scales[row] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
+  if (lane == 0) scales[row] = amax > 0.f ? __fdiv_rn(amax, QM) : 1.0f;
 }
 
 // Offline weight prep for the tcgen05 mainloop: packed INT4 [N, K/2] -> int8 [N, K] holding
@@ -112,20 +121,31 @@ cudaError_t launch_prepack_weights(const uint8_t* w_codes, int64_t N, int64_t K,
   return cudaGetLastError();
 }
 
-cudaError_t launch_quantize_rows(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
-                                 uint8_t* codes, float* scales, cudaStream_t s) {
+template <bool I8>
+static cudaError_t launch_quantize_impl(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
+                                        uint8_t* codes, float* scales, cudaStream_t s) {
   if (rows == 0) return cudaSuccess;
   const int warps = 8;
   const dim3 grid((unsigned)((rows + warps - 1) / warps)), block(32 * warps);
   const int nvec = cols / 8;
+  const bool pdl = rows <= kPdlMaxRows;
   note_launch();
-  if (nvec <= 32) return launch_pdl(rows <= kPdlMaxRows, quantize_rows_kernel<1>, grid, block, 0, s, x, rows, cols, ld_x, clip, codes, scales);
-  else if (nvec <= 64) return launch_pdl(rows <= kPdlMaxRows, quantize_rows_kernel<2>, grid, block, 0, s, x, rows, cols, ld_x, clip, codes, scales);
-  else if (nvec <= 128) return launch_pdl(rows <= kPdlMaxRows, quantize_rows_kernel<4>, grid, block, 0, s, x, rows, cols, ld_x, clip, codes, scales);
-  else if (nvec <= 256) quantize_rows_kernel<8><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
-  else if (nvec <= 512) quantize_rows_kernel<16><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
-  else quantize_rows_long_kernel<<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
+  if (nvec <= 32) return launch_pdl(pdl, quantize_rows_kernel<1, I8>, grid, block, 0, s, x, rows, cols, ld_x, clip, codes, scales);
+  else if (nvec <= 64) return launch_pdl(pdl, quantize_rows_kernel<2, I8>, grid, block, 0, s, x, rows, cols, ld_x, clip, codes, scales);
+  else if (nvec <= 128) return launch_pdl(pdl, quantize_rows_kernel<4, I8>, grid, block, 0, s, x, rows, cols, ld_x, clip, codes, scales);
+  else if (nvec <= 256) quantize_rows_kernel<8, I8><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
+  else if (nvec <= 512) quantize_rows_kernel<16, I8><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
+  else quantize_rows_long_kernel<I8><<<grid, block, 0, s>>>(x, rows, cols, ld_x, clip, codes, scales);
   return cudaGetLastError();
+}
+
+cudaError_t launch_quantize_rows(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
+                                 uint8_t* codes, float* scales, cudaStream_t s) {
+  return launch_quantize_impl<false>(x, rows, cols, ld_x, clip, codes, scales, s);
+}
+cudaError_t launch_quantize_rows_i8(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
+                                    int8_t* codes, float* scales, cudaStream_t s) {
+  return launch_quantize_impl<true>(x, rows, cols, ld_x, clip, reinterpret_cast<uint8_t*>(codes), scales, s);
 }
 
 }  // namespace q4

@@ -83,6 +83,54 @@ def w4a4_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None
     return o
 
 
+def quantize_rows_i8(x: torch.Tensor, clip: float = 0.0, codes=None, scales=None):
+    """W8A8 baseline: fp16 [rows, cols] -> (int8 codes [rows, cols], fp32 scales = amax/127)."""
+    _need(x, torch.float16, "x", 2)
+    rows, cols = x.shape
+    if codes is None:
+        codes = torch.empty(rows, cols, dtype=torch.int8, device=x.device)
+    if scales is None:
+        scales = torch.empty(rows, dtype=torch.float32, device=x.device)
+    check(lib().q4_quantize_rows_i8(_ptr(x), rows, cols, cols, clip, _ptr(codes), _ptr(scales), _stream()))
+    return codes, scales
+
+
+def w8a8_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None, residual=None,
+                gamma=None, beta=None, ln_eps=1e-12, clip=0.0, f16_tap=False, out=None, workspace=None):
+    """W8A8 baseline of w4a4_linear: int8 x int8 -> exact INT32 -> the same fused epilogues;
+    requantizing kinds return int8 codes [M, N]."""
+    _need(a_codes, torch.int8, "a_codes", 2)
+    _need(w_codes, torch.int8, "w_codes", 2)
+    _need(a_scales, torch.float32, "a_scales", 1)
+    _need(w_scales, torch.float32, "w_scales", 1)
+    for n, t in (("bias", bias), ("residual", residual), ("gamma", gamma), ("beta", beta)):
+        _need(t, torch.float16, n)
+    M, K = a_codes.shape
+    N = w_codes.shape[0]
+    if w_codes.shape[1] != K:
+        raise ValueError(f"K mismatch: a_codes {tuple(a_codes.shape)} vs w_codes {tuple(w_codes.shape)}")
+    dev = a_codes.device
+    o = dict(out or {})
+    if kind == EPI_I32:
+        o.setdefault("i32", torch.empty(M, N, dtype=torch.int32, device=dev))
+    if kind in (EPI_F16, EPI_RESLN_Q4) or (kind == EPI_GELU_Q4 and f16_tap):
+        o.setdefault("f16", torch.empty(M, N, dtype=torch.float16, device=dev))
+    if kind in (EPI_GELU_Q4, EPI_RESLN_Q4):
+        o.setdefault("codes", torch.empty(M, N, dtype=torch.int8, device=dev))
+        o.setdefault("scales", torch.empty(M, dtype=torch.float32, device=dev))
+    e = Epilogue(kind=kind, mainloop=0, bias=_ptr(bias), residual=_ptr(residual),
+                 gamma=_ptr(gamma), beta=_ptr(beta), ln_eps=ln_eps, requant_clip=clip,
+                 out_i32=_ptr(o.get("i32")), out_f16=_ptr(o.get("f16")),
+                 out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")), w_i8=None)
+    ws_bytes = lib().q4_w8a8_linear_workspace(M, N, K, kind)
+    if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
+        workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
+    check(lib().q4_w8a8_linear(_ptr(a_codes), _ptr(a_scales), _ptr(w_codes), _ptr(w_scales),
+                               M, N, K, C.byref(e), _ptr(workspace),
+                               0 if workspace is None else workspace.numel(), _stream()))
+    return o
+
+
 def attention_f16_q4(qkv, B, S, heads, head_dim=64, f16_tap=False):
     """a7: fp16 QKV [B*S, 3h] -> (ctx codes [B*S, h/2], ctx scales [B*S][, ctx fp16])."""
     _need(qkv, torch.float16, "qkv", 2)
