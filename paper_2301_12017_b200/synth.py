@@ -90,5 +90,10 @@ def random_packed(rows: int, cols: int, name: str, full_range: bool = False) -> 
     return (lo | (hi << 4)).astype(np.uint8)
 
 
+def random_i8(rows: int, cols: int, name: str) -> np.ndarray:
+    """Random int8 codes [rows, cols] uniform in [-127, 127] (W8A8 GEMM sweep operands)."""
+    return rng(name).integers(-127, 128, size=(rows, cols), dtype=np.int8)
+
+
 def random_scales(n: int, name: str) -> np.ndarray:
     return (rng(name).uniform(0.5, 1.5, n) / 16.0).astype(np.float32)
