@@ -235,6 +235,29 @@ Q4_API q4_status q4_encoder_stack(const q4_layer_cfg* cfg, const q4_layer_weight
                            int64_t B, int64_t S, const uint16_t* h_in, uint16_t* h_out,
                            void* workspace, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------------
+ * W8A8 baseline of a7 / a8 (the paper's end-to-end INT8 comparison,
+ * "i8-qall", Fig. e2e_i4_i8): the same layer and stack with 8-bit
+ * codes throughout -- q4_quantize_rows_i8 for the layer-0 input, q4_w8a8_linear for the
+ * four linears, and q4_attention_f16_q8 (as q4_attention_f16_q4, but ctx_codes [B*S, h]
+ * int8 with ctx_scales = amax/127, codes 8-byte aligned).  In q4_layer_weights the
+ * wqkv / wo / w1 / w2 fields then hold int8 codes [N, K] (q4_quantize_rows_i8 of the fp16
+ * weights) and the *8 prepack fields are ignored; hq_in / hq_out and the code taps are
+ * int8 [M, hidden] / [M, ffn].  Requirements and errors as the W4A4 entry points. */
+Q4_API q4_status q4_attention_f16_q8(const uint16_t* qkv, int64_t B, int64_t S, int32_t heads,
+                                     int32_t head_dim, uint16_t* ctx_f16, int8_t* ctx_codes,
+                                     float* ctx_scales, void* stream);
+Q4_API size_t q4_encoder_layer_w8a8_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S);
+Q4_API q4_status q4_encoder_layer_w8a8(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B,
+                                       int64_t S, const uint16_t* h_in, const int8_t* hq_in,
+                                       const float* hs_in, uint16_t* h_out, int8_t* hq_out,
+                                       float* hs_out, void* workspace, size_t ws_bytes,
+                                       const q4_taps* taps, void* stream);
+Q4_API size_t q4_encoder_stack_w8a8_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S);
+Q4_API q4_status q4_encoder_stack_w8a8(const q4_layer_cfg* cfg, const q4_layer_weights* layers,
+                                       int32_t L, int64_t B, int64_t S, const uint16_t* h_in,
+                                       uint16_t* h_out, void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

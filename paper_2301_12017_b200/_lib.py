@@ -21,6 +21,8 @@ EXPORTS = (
     "q4_w4a4_linear_workspace", "q4_w4a4_linear", "q4_attention_f16_q4",
     "q4_encoder_layer_workspace", "q4_encoder_layer", "q4_encoder_stack_workspace",
     "q4_encoder_stack", "q4_quantize_rows_i8", "q4_w8a8_linear_workspace", "q4_w8a8_linear",
+    "q4_attention_f16_q8", "q4_encoder_layer_w8a8_workspace", "q4_encoder_layer_w8a8",
+    "q4_encoder_stack_w8a8_workspace", "q4_encoder_stack_w8a8",
 )
 
 
@@ -92,11 +94,19 @@ def lib():
         L.q4_encoder_stack_workspace.restype = SZ
         L.q4_encoder_stack.argtypes = [C.POINTER(LayerCfg), C.POINTER(LayerWeights), I32, I64, I64, P,
                                        P, P, SZ, P]
+        L.q4_attention_f16_q8.argtypes = [P, I64, I64, I32, I32, P, P, P, P]
+        L.q4_encoder_layer_w8a8_workspace.argtypes = [C.POINTER(LayerCfg), I64, I64]
+        L.q4_encoder_layer_w8a8_workspace.restype = SZ
+        L.q4_encoder_layer_w8a8.argtypes = L.q4_encoder_layer.argtypes
+        L.q4_encoder_stack_w8a8_workspace.argtypes = [C.POINTER(LayerCfg), I64, I64]
+        L.q4_encoder_stack_w8a8_workspace.restype = SZ
+        L.q4_encoder_stack_w8a8.argtypes = L.q4_encoder_stack.argtypes
         for name in EXPORTS:
             L[name].restype = L[name].restype if name in (
                 "q4_last_error", "q4_version", "q4_launch_count", "q4_w4a4_linear_workspace",
                 "q4_encoder_layer_workspace", "q4_encoder_stack_workspace",
-                "q4_w8a8_linear_workspace") else C.c_int
+                "q4_w8a8_linear_workspace", "q4_encoder_layer_w8a8_workspace",
+                "q4_encoder_stack_w8a8_workspace") else C.c_int
         _lib = L
     return _lib
 

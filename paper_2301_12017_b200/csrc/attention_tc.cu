@@ -67,7 +67,7 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
 __global__ void __launch_bounds__(AT_THREADS, 2)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tq, int S, int heads, __half* __restrict__ ctx_f16,
                         uint8_t* __restrict__ ctx_codes, float* __restrict__ ctx_scales,
-                        unsigned long long* __restrict__ trace, int dbg, int G) {
+                        unsigned long long* __restrict__ trace, int dbg, int G, int i8) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* kv_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -329,6 +329,17 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
         if (tok >= S) continue;
         const float a = fmaxf(red[tok], red[128 + tok]);
         const size_t grow = (size_t)row0 + tok;
+        if (i8) {  // W8A8 baseline: int8 codes, scale amax/127 (oracle O-11)
+          uint2* c8 = reinterpret_cast<uint2*>(ctx_codes + grow * h);
+          if (lane == 0) ctx_scales[grow] = a > 0.f ? __fdiv_rn(a, 127.0f) : 1.0f;
+          const float rq = a > 0.f ? __fdiv_rn(127.0f, a) : 0.f;
+          for (int c = lane; c < h / 8; c += 32) {
+            const uint4 x = *reinterpret_cast<const uint4*>(qb + rr * 2048 + c * 16);
+            const uint32_t hh[4] = {x.x, x.y, x.z, x.w};
+            c8[c] = requant8_i8(hh, a, rq, 0.f);
+          }
+          continue;
+        }
         uint32_t* cw = reinterpret_cast<uint32_t*>(ctx_codes + grow * (h / 2));
         if (lane == 0) ctx_scales[grow] = a > 0.f ? __fdiv_rn(a, 7.0f) : 1.0f;
         if (!(a > 0.f)) {  // all-zero row (R5)
@@ -396,9 +407,10 @@ cluster_tail:
         asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(y) : "r"(rb) : "memory");
         a = fmaxf(a, fmaxf(x, y));
       }
+      const float qm = i8 ? 127.0f : 7.0f;
       amx[r] = a;
-      rr7[r] = a > 0.f ? __fdiv_rn(7.0f, a) : 0.f;
-      if (g == 0 && r < S) ctx_scales[row0 + r] = a > 0.f ? __fdiv_rn(a, 7.0f) : 1.0f;
+      rr7[r] = a > 0.f ? __fdiv_rn(qm, a) : 0.f;
+      if (g == 0 && r < S) ctx_scales[row0 + r] = a > 0.f ? __fdiv_rn(a, qm) : 1.0f;
     }
     __syncthreads();
     // this CTA's columns [64 j0, 64 (j0 + hpc)): cpr 16-byte chunks (8 values) per row
@@ -408,8 +420,11 @@ cluster_tail:
       const float a = amx[rw];
       const uint4 x = __ldcg(reinterpret_cast<const uint4*>(ctx_f16 + (size_t)(row0 + rw) * h + j0 * 64 + c * 8));
       const uint32_t hh[4] = {x.x, x.y, x.z, x.w};
-      reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] =
-          a > 0.f ? requant8(hh, a, rr7[rw], 0.f) : 0u;
+      if (i8)
+        reinterpret_cast<uint2*>(ctx_codes + (size_t)(row0 + rw) * h + j0 * 64)[c] = requant8_i8(hh, a, rr7[rw], 0.f);
+      else
+        reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] =
+            a > 0.f ? requant8(hh, a, rr7[rw], 0.f) : 0u;
     }
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
@@ -419,7 +434,7 @@ cluster_tail:
 }
 
 cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __half* ctx_f16, uint8_t* ctx_codes,
-                                float* ctx_scales, cudaStream_t s) {
+                                float* ctx_scales, cudaStream_t s, bool i8) {
   if (B == 0) return cudaSuccess;
   static EncodeFn enc = nullptr;
   if (!enc) {
@@ -473,7 +488,7 @@ cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __ha
   static const bool no_pdl = getenv("Q4_NO_PDL") != nullptr;  // profiling only
   cfg.numAttrs = (no_pdl || (int64_t)B * S > kPdlMaxRows) ? 1 : 2;
   cudaError_t le = cudaLaunchKernelEx(&cfg, attention_tc_kernel, tq, S, heads, ctx_f16, ctx_codes, ctx_scales,
-                                      trace_path ? trace_buf : nullptr, dbg, G);
+                                      trace_path ? trace_buf : nullptr, dbg, G, i8 ? 1 : 0);
   if (le != cudaSuccess) return le;
   if (trace_path) {  // profiling only: dump this launch's stamps
     static unsigned long long host[512 * 16 * 16];

@@ -71,7 +71,8 @@ size_t tc_workspace_bytes(int M, int N, int TN);
 cudaError_t launch_w4a4_legacy(const GemmArgs& g, bool s4, cudaStream_t s, const char** why);
 cudaError_t launch_attention(const __half* qkv, int B, int S, int heads, __half* ctx_f16,
                              uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s);
+// i8: W8A8 baseline -- int8 ctx codes [B*S, h] with scale amax/127 instead of packed INT4
 cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __half* ctx_f16,
-                                uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s);
+                                uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s, bool i8 = false);
 
 }  // namespace q4

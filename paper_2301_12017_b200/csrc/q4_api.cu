@@ -268,10 +268,29 @@ q4_status q4_attention_f16_q4(const uint16_t* qkv, int64_t B, int64_t S, int32_t
     return fail(Q4_EALIGN, "q4_attention_f16_q4: qkv/ctx_f16 must be 16-byte aligned, codes 4-byte");
   // tcgen05 kernel by default; the mma.sync kernel stays as the measured baseline (Q4_ATTN_LEGACY=1)
   static const bool legacy = [] { const char* e = getenv("Q4_ATTN_LEGACY"); return e && atoi(e) != 0; }();
-  cudaError_t e = (legacy ? q4::launch_attention : q4::launch_attention_tc)(
-      reinterpret_cast<const __half*>(qkv), (int)B, (int)S, heads, reinterpret_cast<__half*>(ctx_f16), ctx_codes,
-      ctx_scales, (cudaStream_t)stream);
+  const __half* q = reinterpret_cast<const __half*>(qkv);
+  __half* cf = reinterpret_cast<__half*>(ctx_f16);
+  cudaError_t e = legacy ? q4::launch_attention(q, (int)B, (int)S, heads, cf, ctx_codes, ctx_scales, (cudaStream_t)stream)
+                         : q4::launch_attention_tc(q, (int)B, (int)S, heads, cf, ctx_codes, ctx_scales, (cudaStream_t)stream);
   return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_attention_f16_q4");
+}
+
+q4_status q4_attention_f16_q8(const uint16_t* qkv, int64_t B, int64_t S, int32_t heads, int32_t head_dim,
+                              uint16_t* ctx_f16, int8_t* ctx_codes, float* ctx_scales, void* stream) {
+  g_err[0] = 0;
+  if (head_dim != 64) return fail(Q4_EUNSUPPORTED, "q4_attention_f16_q8: head_dim=%d (only 64)", head_dim);
+  if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "q4_attention_f16_q8: B=%lld S=%lld (need B>=0, 1<=S<=128)", (long long)B, (long long)S);
+  if (heads < 1 || heads * 64 > 1024) return fail(Q4_ESHAPE, "q4_attention_f16_q8: heads=%d (need 1..16)", heads);
+  if (B > 65535) return fail(Q4_ESHAPE, "q4_attention_f16_q8: B=%lld > 65535", (long long)B);
+  if (B == 0) return Q4_OK;
+  if (!qkv || !ctx_f16 || !ctx_codes || !ctx_scales)
+    return fail(Q4_EINVAL, "q4_attention_f16_q8: NULL qkv/ctx_f16/ctx_codes/ctx_scales");
+  if (!al16(qkv) || !al8(ctx_codes) || !al16(ctx_f16))
+    return fail(Q4_EALIGN, "q4_attention_f16_q8: qkv/ctx_f16 must be 16-byte aligned, codes 8-byte");
+  cudaError_t e = q4::launch_attention_tc(reinterpret_cast<const __half*>(qkv), (int)B, (int)S, heads,
+                                          reinterpret_cast<__half*>(ctx_f16), reinterpret_cast<uint8_t*>(ctx_codes),
+                                          ctx_scales, (cudaStream_t)stream, true);
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_attention_f16_q8");
 }
 
 // ------------------------------------------------------------------ encoder layer
@@ -291,10 +310,11 @@ struct LayerWs {
   float* f_scales;
   size_t bytes;
 };
-LayerWs layer_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base) {
+LayerWs layer_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base, bool i8 = false) {
   LayerWs w;
   size_t o = 0;
   const int64_t h = c->hidden, f = c->ffn;
+  const int64_t cd = i8 ? 1 : 2;  // elements per code byte
   auto take = [&](size_t n) { size_t r = o; o = align_up(o + n); return base ? base + r : nullptr; };
   size_t gw = 0;
   for (int64_t n : {h, f})
@@ -306,12 +326,12 @@ LayerWs layer_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base) {
   w.gemm_ws = take(gw);
   w.qkv = (uint16_t*)take((size_t)M * 3 * h * 2);
   w.ctx = (uint16_t*)take((size_t)M * h * 2);
-  w.ctx_codes = take((size_t)M * h / 2);
+  w.ctx_codes = take((size_t)(M * h / cd));
   w.ctx_scales = (float*)take((size_t)M * 4);
   w.h1 = (uint16_t*)take((size_t)M * h * 2);
-  w.h1_codes = take((size_t)M * h / 2);
+  w.h1_codes = take((size_t)(M * h / cd));
   w.h1_scales = (float*)take((size_t)M * 4);
-  w.f_codes = take((size_t)M * f / 2);
+  w.f_codes = take((size_t)(M * f / cd));
   w.f_scales = (float*)take((size_t)M * 4);
   w.bytes = o;
   return w;
@@ -331,20 +351,30 @@ size_t q4_encoder_layer_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S)
   return layer_ws(cfg, B * S, nullptr).bytes;
 }
 
-q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B, int64_t S,
-                           const uint16_t* h_in, const uint8_t* hq_in, const float* hs_in, uint16_t* h_out,
-                           uint8_t* hq_out, float* hs_out, void* workspace, size_t ws_bytes, const q4_taps* taps,
-                           void* stream) {
-  g_err[0] = 0;
-  q4_status st = check_cfg(cfg, "q4_encoder_layer");
+size_t q4_encoder_layer_w8a8_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S) {
+  if (!cfg) return 0;
+  return layer_ws(cfg, B * S, nullptr, true).bytes;
+}
+
+}  // extern "C"
+
+namespace {
+// One post-LN layer; i8 = the W8A8 baseline (int8 codes everywhere, q4_w8a8_linear and the
+// int8 ctx quantize; the weight fields hold int8 codes [N, K], the *8 fields are unused).
+q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B, int64_t S,
+                             const uint16_t* h_in, const uint8_t* hq_in, const float* hs_in, uint16_t* h_out,
+                             uint8_t* hq_out, float* hs_out, void* workspace, size_t ws_bytes, const q4_taps* taps,
+                             void* stream, bool i8) {
+  const char* who = i8 ? "q4_encoder_layer_w8a8" : "q4_encoder_layer";
+  q4_status st = check_cfg(cfg, who);
   if (st) return st;
-  if (!w) return fail(Q4_EINVAL, "q4_encoder_layer: weights NULL");
-  if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "q4_encoder_layer: B=%lld S=%lld", (long long)B, (long long)S);
+  if (!w) return fail(Q4_EINVAL, "%s: weights NULL", who);
+  if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "%s: B=%lld S=%lld", who, (long long)B, (long long)S);
   const int64_t M = B * S, h = cfg->hidden, f = cfg->ffn;
   if (M == 0) return Q4_OK;
-  LayerWs ws = layer_ws(cfg, M, (uint8_t*)workspace);
+  LayerWs ws = layer_ws(cfg, M, (uint8_t*)workspace, i8);
   if (!workspace || ws_bytes < ws.bytes)
-    return fail(Q4_EINVAL, "q4_encoder_layer: workspace %zu bytes < required %zu", ws_bytes, ws.bytes);
+    return fail(Q4_EINVAL, "%s: workspace %zu bytes < required %zu", who, ws_bytes, ws.bytes);
   q4_taps tp;
   memset(&tp, 0, sizeof tp);
   if (taps) tp = *taps;
@@ -360,6 +390,11 @@ q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, i
 
   auto lin = [&](const uint8_t* ac, const float* as, const uint8_t* wc, const float* wsc, int64_t N, int64_t K,
                  q4_epilogue e) -> q4_status {
+    if (i8) {
+      e.w_i8 = nullptr;
+      return q4_w8a8_linear(reinterpret_cast<const int8_t*>(ac), as, reinterpret_cast<const int8_t*>(wc), wsc, M, N, K,
+                            &e, ws.gemm_ws, ws.gemm_ws_bytes, stream);
+    }
     return q4_w4a4_linear(ac, as, wc, wsc, M, N, K, &e, ws.gemm_ws, ws.gemm_ws_bytes, stream);
   };
   auto acc_tap = [&](const uint8_t* ac, const float* as, const uint8_t* wc, const float* wsc, int64_t N, int64_t K,
@@ -369,6 +404,9 @@ q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, i
     memset(&e, 0, sizeof e);
     e.kind = Q4_EPI_I32;
     e.out_i32 = out;
+    if (i8)
+      return q4_w8a8_linear(reinterpret_cast<const int8_t*>(ac), as, reinterpret_cast<const int8_t*>(wc), wsc, M, N, K,
+                            &e, nullptr, 0, stream);
     return q4_w4a4_linear(ac, as, wc, wsc, M, N, K, &e, nullptr, 0, stream);
   };
   q4_epilogue e;
@@ -378,8 +416,10 @@ q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, i
   if ((st = lin(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, e))) return st;
   if ((st = acc_tap(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, tp.acc_qkv))) return st;
   // FP16 attention + fused per-token ctx quantize
-  if ((st = q4_attention_f16_q4(qkv, B, S, cfg->heads, cfg->head_dim, tp.ctx ? tp.ctx : ws.ctx, ctx_codes,
-                                ctx_scales, stream)))
+  if ((st = i8 ? q4_attention_f16_q8(qkv, B, S, cfg->heads, cfg->head_dim, tp.ctx ? tp.ctx : ws.ctx,
+                                     reinterpret_cast<int8_t*>(ctx_codes), ctx_scales, stream)
+              : q4_attention_f16_q4(qkv, B, S, cfg->heads, cfg->head_dim, tp.ctx ? tp.ctx : ws.ctx, ctx_codes,
+                                    ctx_scales, stream)))
     return st;
   // attention output: dequant + bias + residual(h_in) + LN1 + requant
   memset(&e, 0, sizeof e);
@@ -401,6 +441,27 @@ q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, i
   if ((st = acc_tap(f_codes, f_scales, w->w2, w->s2, h, f, tp.acc_2))) return st;
   return Q4_OK;
 }
+}  // namespace
+
+extern "C" {
+
+q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B, int64_t S,
+                           const uint16_t* h_in, const uint8_t* hq_in, const float* hs_in, uint16_t* h_out,
+                           uint8_t* hq_out, float* hs_out, void* workspace, size_t ws_bytes, const q4_taps* taps,
+                           void* stream) {
+  g_err[0] = 0;
+  return encoder_layer_impl(cfg, w, B, S, h_in, hq_in, hs_in, h_out, hq_out, hs_out, workspace, ws_bytes, taps,
+                            stream, false);
+}
+
+q4_status q4_encoder_layer_w8a8(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B, int64_t S,
+                                const uint16_t* h_in, const int8_t* hq_in, const float* hs_in, uint16_t* h_out,
+                                int8_t* hq_out, float* hs_out, void* workspace, size_t ws_bytes, const q4_taps* taps,
+                                void* stream) {
+  g_err[0] = 0;
+  return encoder_layer_impl(cfg, w, B, S, h_in, reinterpret_cast<const uint8_t*>(hq_in), hs_in, h_out,
+                            reinterpret_cast<uint8_t*>(hq_out), hs_out, workspace, ws_bytes, taps, stream, true);
+}
 
 // ------------------------------------------------------------------ encoder stack
 
@@ -412,16 +473,16 @@ struct StackWs {
   uint8_t* layer;
   size_t layer_bytes, bytes;
 };
-StackWs stack_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base) {
+StackWs stack_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base, bool i8 = false) {
   StackWs w;
   size_t o = 0;
   auto take = [&](size_t n) { size_t r = o; o = align_up(o + n); return base ? base + r : nullptr; };
   for (int i = 0; i < 2; ++i) {
     w.hid[i] = (uint16_t*)take((size_t)M * c->hidden * 2);
-    w.hq[i] = take((size_t)M * c->hidden / 2);
+    w.hq[i] = take((size_t)M * c->hidden / (i8 ? 1 : 2));
     w.hs[i] = (float*)take((size_t)M * 4);
   }
-  w.layer_bytes = layer_ws(c, M, nullptr).bytes;
+  w.layer_bytes = layer_ws(c, M, nullptr, i8).bytes;
   w.layer = take(w.layer_bytes);
   w.bytes = o;
   return w;
@@ -434,26 +495,21 @@ bool is_device_ptr(const void* p) {
   }
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
-}  // namespace
 
-size_t q4_encoder_stack_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S) {
-  if (!cfg) return 0;
-  return stack_ws(cfg, B * S, nullptr).bytes;
-}
-
-q4_status q4_encoder_stack(const q4_layer_cfg* cfg, const q4_layer_weights* layers, int32_t L, int64_t B, int64_t S,
-                           const uint16_t* h_in, uint16_t* h_out, void* workspace, size_t ws_bytes, void* stream) {
-  g_err[0] = 0;
-  q4_status st = check_cfg(cfg, "q4_encoder_stack");
+q4_status encoder_stack_impl(const q4_layer_cfg* cfg, const q4_layer_weights* layers, int32_t L, int64_t B,
+                             int64_t S, const uint16_t* h_in, uint16_t* h_out, void* workspace, size_t ws_bytes,
+                             void* stream, bool i8) {
+  const char* who = i8 ? "q4_encoder_stack_w8a8" : "q4_encoder_stack";
+  q4_status st = check_cfg(cfg, who);
   if (st) return st;
-  if (L < 1 || !layers) return fail(Q4_EINVAL, "q4_encoder_stack: L=%d layers=%p", L, (const void*)layers);
-  if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "q4_encoder_stack: B=%lld S=%lld", (long long)B, (long long)S);
+  if (L < 1 || !layers) return fail(Q4_EINVAL, "%s: L=%d layers=%p", who, L, (const void*)layers);
+  if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "%s: B=%lld S=%lld", who, (long long)B, (long long)S);
   const int64_t M = B * S, h = cfg->hidden;
   if (M == 0) return Q4_OK;
-  if (!h_in || !h_out) return fail(Q4_EINVAL, "q4_encoder_stack: NULL h_in/h_out");
-  StackWs ws = stack_ws(cfg, M, (uint8_t*)workspace);
+  if (!h_in || !h_out) return fail(Q4_EINVAL, "%s: NULL h_in/h_out", who);
+  StackWs ws = stack_ws(cfg, M, (uint8_t*)workspace, i8);
   if (!workspace || ws_bytes < ws.bytes)
-    return fail(Q4_EINVAL, "q4_encoder_stack: workspace %zu bytes < required %zu", ws_bytes, ws.bytes);
+    return fail(Q4_EINVAL, "%s: workspace %zu bytes < required %zu", who, ws_bytes, ws.bytes);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t hbytes = (size_t)M * h * 2;
   const uint16_t* x = h_in;
@@ -465,14 +521,16 @@ q4_status q4_encoder_stack(const q4_layer_cfg* cfg, const q4_layer_weights* laye
     return fail(Q4_EALIGN, "q4_encoder_stack: h_in must be 16-byte aligned");
   }
   // layer-0 activation quantize (the only standalone quantize in the forward)
-  if ((st = q4_quantize_rows(x, M, h, h, 0.f, ws.hq[1], ws.hs[1], stream))) return st;
+  if ((st = i8 ? q4_quantize_rows_i8(x, M, h, h, 0.f, reinterpret_cast<int8_t*>(ws.hq[1]), ws.hs[1], stream)
+               : q4_quantize_rows(x, M, h, h, 0.f, ws.hq[1], ws.hs[1], stream)))
+    return st;
   const bool out_dev = is_device_ptr(h_out);
   for (int l = 0; l < L; ++l) {
     const int o = l & 1;
     const uint16_t* hin = (l == 0) ? x : ws.hid[1 - o];
     uint16_t* hout = (l == L - 1 && out_dev) ? h_out : ws.hid[o];
-    if ((st = q4_encoder_layer(cfg, &layers[l], B, S, hin, ws.hq[1 - o], ws.hs[1 - o], hout, ws.hq[o], ws.hs[o],
-                               ws.layer, ws.layer_bytes, nullptr, stream)))
+    if ((st = encoder_layer_impl(cfg, &layers[l], B, S, hin, ws.hq[1 - o], ws.hs[1 - o], hout, ws.hq[o], ws.hs[o],
+                                 ws.layer, ws.layer_bytes, nullptr, stream, i8)))
       return st;
   }
   if (!out_dev) {
@@ -480,6 +538,28 @@ q4_status q4_encoder_stack(const q4_layer_cfg* cfg, const q4_layer_weights* laye
     if (e != cudaSuccess) return cuda_fail(e, "q4_encoder_stack: D2H copy");
   }
   return Q4_OK;
+}
+}  // namespace
+
+size_t q4_encoder_stack_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S) {
+  if (!cfg) return 0;
+  return stack_ws(cfg, B * S, nullptr).bytes;
+}
+size_t q4_encoder_stack_w8a8_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S) {
+  if (!cfg) return 0;
+  return stack_ws(cfg, B * S, nullptr, true).bytes;
+}
+
+q4_status q4_encoder_stack(const q4_layer_cfg* cfg, const q4_layer_weights* layers, int32_t L, int64_t B, int64_t S,
+                           const uint16_t* h_in, uint16_t* h_out, void* workspace, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  return encoder_stack_impl(cfg, layers, L, B, S, h_in, h_out, workspace, ws_bytes, stream, false);
+}
+q4_status q4_encoder_stack_w8a8(const q4_layer_cfg* cfg, const q4_layer_weights* layers, int32_t L, int64_t B,
+                                int64_t S, const uint16_t* h_in, uint16_t* h_out, void* workspace, size_t ws_bytes,
+                                void* stream) {
+  g_err[0] = 0;
+  return encoder_stack_impl(cfg, layers, L, B, S, h_in, h_out, workspace, ws_bytes, stream, true);
 }
 
 }  // extern "C"

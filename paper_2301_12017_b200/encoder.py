@@ -13,12 +13,17 @@ from ._lib import LayerWeights, check, lib
 
 
 class W4A4Encoder:
+    bits = 4
+
     def __init__(self, cfg: dict, layers: list, device="cuda"):
         """cfg: BERT dims (hidden, heads, head_dim, ffn, ln_eps); layers: per-layer fp16
         parameter dicts (synth.layer_params) -- quantized on the device here (offline)."""
         self.cfg = dict(cfg)
         self.device = torch.device(device)
-        self.weights = [ops.quantize_layer(p, self.device) for p in layers]
+        self.weights = [ops.quantize_layer(p, self.device, bits=self.bits) for p in layers]
+        i8 = self.bits == 8
+        self._ws_fn = lib().q4_encoder_stack_w8a8_workspace if i8 else lib().q4_encoder_stack_workspace
+        self._stack_fn = lib().q4_encoder_stack_w8a8 if i8 else lib().q4_encoder_stack
         self.L = len(self.weights)
         self._lw = (LayerWeights * self.L)(*[ops.layer_weights(w) for w in self.weights])
         self._lc = ops.layer_cfg(self.cfg)
@@ -28,7 +33,7 @@ class W4A4Encoder:
 
     def workspace(self, B: int, S: int) -> torch.Tensor:
         if self._ws_shape != (B, S):
-            n = lib().q4_encoder_stack_workspace(C.byref(self._lc), B, S)
+            n = self._ws_fn(C.byref(self._lc), B, S)
             self._ws = torch.zeros(max(n, 1), dtype=torch.uint8, device=self.device)
             self._ws_shape = (B, S)
         return self._ws
@@ -37,7 +42,7 @@ class W4A4Encoder:
         """h_in / h_out: fp16 [B*S, hidden], CUDA tensors or (pinned) CPU tensors -- with
         host tensors the H2D / D2H copies happen inside the C call (end-to-end path)."""
         ws = self.workspace(B, S)
-        check(lib().q4_encoder_stack(C.byref(self._lc), self._lw, self.L, B, S,
+        check(self._stack_fn(C.byref(self._lc), self._lw, self.L, B, S,
                                      C.c_void_p(h_in.data_ptr()), C.c_void_p(h_out.data_ptr()),
                                      C.c_void_p(ws.data_ptr()), ws.numel(),
                                      C.c_void_p(torch.cuda.current_stream().cuda_stream)))
@@ -60,3 +65,9 @@ class W4A4Encoder:
 
     def replay(self):
         self.graph.replay()
+
+
+class W8A8Encoder(W4A4Encoder):
+    """The W8A8 baseline encoder (the paper's INT8 comparison point,
+    PAPER.md:496-502): the same stack with 8-bit codes (q4_encoder_stack_w8a8)."""
+    bits = 8

@@ -144,6 +144,19 @@ def attention_f16_q4(qkv, B, S, heads, head_dim=64, f16_tap=False):
     return (codes, scales, ctx) if f16_tap else (codes, scales)
 
 
+def attention_f16_q8(qkv, B, S, heads, head_dim=64, f16_tap=False):
+    """W8A8 baseline of a7: (ctx int8 codes [B*S, h], ctx scales = amax/127[, ctx fp16])."""
+    _need(qkv, torch.float16, "qkv", 2)
+    h = heads * head_dim
+    dev = qkv.device
+    codes = torch.empty(B * S, h, dtype=torch.int8, device=dev)
+    scales = torch.empty(B * S, dtype=torch.float32, device=dev)
+    ctx = torch.empty(B * S, h, dtype=torch.float16, device=dev)
+    check(lib().q4_attention_f16_q8(_ptr(qkv), B, S, heads, head_dim, _ptr(ctx), _ptr(codes),
+                                    _ptr(scales), _stream()))
+    return (codes, scales, ctx) if f16_tap else (codes, scales)
+
+
 def layer_cfg(cfg: dict) -> LayerCfg:
     return LayerCfg(cfg["hidden"], cfg["heads"], cfg["head_dim"], cfg["ffn"], cfg.get("ln_eps", 1e-12))
 
@@ -164,13 +177,18 @@ def layer_weights(w: dict) -> LayerWeights:
                            for k in _lib.WEIGHT_FIELDS})
 
 
-def quantize_layer(params: dict, device="cuda", prepack: bool = True) -> dict:
+def quantize_layer(params: dict, device="cuda", prepack: bool = True, bits: int = 4) -> dict:
     """Offline weight prep (a2, not timed): fp16 [out, in] weights -> per-output-channel
     INT4 codes + scales on the device (and, with prepack, the MMA-ready int8 copy);
-    biases and LN parameters copied as fp16."""
+    biases and LN parameters copied as fp16.  bits=8: the W8A8 baseline's int8 codes."""
+    if bits not in (4, 8):
+        raise ValueError(f"bits={bits} (4 or 8)")
     w = {}
     for k in ("wqkv", "wo", "w1", "w2"):
         t = torch.as_tensor(params[k]).to(device=device, dtype=torch.float16).contiguous()
+        if bits == 8:
+            w[k], w["s" + k[1:]] = quantize_rows_i8(t)
+            continue
         w[k], w["s" + k[1:]] = quantize_rows(t)
         if prepack:
             w[k + "8"] = prepack_weights(w[k])
@@ -180,16 +198,20 @@ def quantize_layer(params: dict, device="cuda", prepack: bool = True) -> dict:
 
 
 def encoder_layer(cfg: dict, w: dict, B: int, S: int, h_in, hq_in, hs_in, taps: bool = False,
-                  workspace=None):
-    """a8: one post-LN BERT layer (qall).  Returns dict(h_out, hq_out, hs_out[, taps...])."""
+                  workspace=None, bits: int = 4):
+    """a8: one post-LN BERT layer (qall).  Returns dict(h_out, hq_out, hs_out[, taps...]).
+    bits=8: the W8A8 baseline (q4_encoder_layer_w8a8; int8 codes, weights from
+    quantize_layer(bits=8))."""
     M, h, f = B * S, cfg["hidden"], cfg["ffn"]
     dev = h_in.device
     lc = layer_cfg(cfg)
-    ws_bytes = lib().q4_encoder_layer_workspace(C.byref(lc), B, S)
+    i8 = bits == 8
+    ws_bytes = (lib().q4_encoder_layer_w8a8_workspace if i8 else lib().q4_encoder_layer_workspace)(C.byref(lc), B, S)
     if workspace is None:
         workspace = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    cdt, cdiv = (torch.int8, 1) if i8 else (torch.uint8, 2)
     out = {"h_out": torch.empty(M, h, dtype=torch.float16, device=dev),
-           "hq_out": torch.empty(M, h // 2, dtype=torch.uint8, device=dev),
+           "hq_out": torch.empty(M, h // cdiv, dtype=cdt, device=dev),
            "hs_out": torch.empty(M, dtype=torch.float32, device=dev)}
     tp = None
     if taps:
@@ -197,14 +219,15 @@ def encoder_layer(cfg: dict, w: dict, B: int, S: int, h_in, hq_in, hs_in, taps: 
                   "h1": ((M, h), torch.float16), "ffn1": ((M, f), torch.float16),
                   "acc_qkv": ((M, 3 * h), torch.int32), "acc_o": ((M, h), torch.int32),
                   "acc_1": ((M, f), torch.int32), "acc_2": ((M, h), torch.int32),
-                  "ctx_codes": ((M, h // 2), torch.uint8), "h1_codes": ((M, h // 2), torch.uint8),
-                  "f_codes": ((M, f // 2), torch.uint8), "ctx_scales": ((M,), torch.float32),
+                  "ctx_codes": ((M, h // cdiv), cdt), "h1_codes": ((M, h // cdiv), cdt),
+                  "f_codes": ((M, f // cdiv), cdt), "ctx_scales": ((M,), torch.float32),
                   "h1_scales": ((M,), torch.float32), "f_scales": ((M,), torch.float32)}
         for k, (shp, dt) in shapes.items():
             out[k] = torch.empty(shp, dtype=dt, device=dev)
         tp = Taps(**{k: out[k].data_ptr() for k in _lib.TAP_FIELDS})
     lw = layer_weights(w)
-    check(lib().q4_encoder_layer(C.byref(lc), C.byref(lw), B, S, _ptr(h_in), _ptr(hq_in),
+    fn = lib().q4_encoder_layer_w8a8 if i8 else lib().q4_encoder_layer
+    check(fn(C.byref(lc), C.byref(lw), B, S, _ptr(h_in), _ptr(hq_in),
                                  _ptr(hs_in), _ptr(out["h_out"]), _ptr(out["hq_out"]),
                                  _ptr(out["hs_out"]), _ptr(workspace), workspace.numel(),
                                  C.byref(tp) if tp is not None else None, _stream()))

@@ -124,3 +124,85 @@ def test_w8a8_errors(q4):
     w = torch.zeros(64, 96, dtype=torch.int8, device="cuda")
     with pytest.raises(Exception, match="multiple of 128"):
         q4.w8a8_linear(a, s, w, torch.ones(64, dtype=torch.float32, device="cuda"), q4.EPI_F16)
+
+
+# ------------------------------------------------------------------ a7 / a8 at 8 bits
+@pytest.mark.parametrize("B,S,H", [(2, 128, 12), (3, 128, 16), (1, 77, 16), (4, 1, 2)])
+def test_attention_q8(q4, B, S, H):
+    qkv = synth.hidden(B * S, 3 * H * 64, f"a8q{B}_{S}_{H}")
+    codes, scales, ctx = q4.attention_f16_q8(dev(qkv), B, S, H, 64, f16_tap=True)
+    rctx, _, _ = orc.attention(qkv, B, S, H, 64)
+    c = host(ctx)
+    assert_f16_close(c, rctx, "ctx")
+    c2, s2 = orc.quantize_rows_i8(c)  # O-11 on the GPU's own fp16 ctx (R13)
+    assert np.array_equal(host(codes), c2) and np.array_equal(host(scales), s2)
+
+
+@pytest.mark.parametrize("size,B", [("base", 2), ("large", 1)])
+def test_encoder_layer_w8a8_teacher_forced(q4, size, B):
+    """Every sub-step of q4_encoder_layer_w8a8 against the W8A8 oracle on the GPU's own
+    inputs (taps): INT32 bit-exact, fp16 within tolerance, codes = O-11(GPU fp16)."""
+    cfg = synth.BERT[size]
+    S, M, h, f = 128, B * 128, cfg["hidden"], cfg["ffn"]
+    p = synth.layer_params(cfg, 0, "enc8")
+    x = synth.hidden(M, h, "enc8_x")
+    w = q4.quantize_layer(p, bits=8)
+    for k in ("wqkv", "wo", "w1", "w2"):
+        rc, rs = orc.quantize_rows_i8(p[k])
+        assert np.array_equal(host(w[k]), rc) and np.array_equal(host(w["s" + k[1:]]), rs), k
+    xq, xs = q4.quantize_rows_i8(dev(x))
+    out = q4.encoder_layer(cfg, w, B, S, dev(x), xq, xs, taps=True, bits=8)
+    T = {k: host(v) for k, v in out.items()}
+    W = {k: host(v) for k, v in w.items()}
+    xq_, xs_ = host(xq), host(xs)
+    assert np.array_equal(T["acc_qkv"], orc.gemm_i32_i8(xq_, W["wqkv"], M, 3 * h, h))
+    rq = orc.w8a8_linear(xq_, xs_, W["wqkv"], W["sqkv"], M, 3 * h, h, orc.EPI_F16, bias=p["bqkv"])
+    assert_f16_close(T["qkv"], rq["f16"], "qkv")
+    rctx, _, _ = orc.attention(T["qkv"], B, S, cfg["heads"], 64)
+    assert_f16_close(T["ctx"], rctx, "ctx")
+    c2, s2 = orc.quantize_rows_i8(T["ctx"])
+    assert np.array_equal(T["ctx_codes"], c2) and np.array_equal(T["ctx_scales"], s2)
+    assert np.array_equal(T["acc_o"], orc.gemm_i32_i8(T["ctx_codes"], W["wo"], M, h, h))
+    r1 = orc.w8a8_linear(T["ctx_codes"], T["ctx_scales"], W["wo"], W["so"], M, h, h, orc.EPI_RESLN_Q4,
+                         bias=p["bo"], residual=x, gamma=p["ln1_g"], beta=p["ln1_b"])
+    assert_f16_close(T["h1"], r1["f16"], "h1")
+    c2, s2 = orc.quantize_rows_i8(T["h1"])
+    assert np.array_equal(T["h1_codes"], c2) and np.array_equal(T["h1_scales"], s2)
+    assert np.array_equal(T["acc_1"], orc.gemm_i32_i8(T["h1_codes"], W["w1"], M, f, h))
+    r2 = orc.w8a8_linear(T["h1_codes"], T["h1_scales"], W["w1"], W["s1"], M, f, h, orc.EPI_GELU_Q4, bias=p["b1"])
+    assert_f16_close(T["ffn1"], r2["f16"], "ffn1")
+    c2, s2 = orc.quantize_rows_i8(T["ffn1"])
+    assert np.array_equal(T["f_codes"], c2) and np.array_equal(T["f_scales"], s2)
+    assert np.array_equal(T["acc_2"], orc.gemm_i32_i8(T["f_codes"], W["w2"], M, h, f))
+    r3 = orc.w8a8_linear(T["f_codes"], T["f_scales"], W["w2"], W["s2"], M, h, f, orc.EPI_RESLN_Q4,
+                         bias=p["b2"], residual=T["h1"], gamma=p["ln2_g"], beta=p["ln2_b"])
+    assert_f16_close(T["h_out"], r3["f16"], "h_out")
+    c2, s2 = orc.quantize_rows_i8(T["h_out"])
+    assert np.array_equal(T["hq_out"], c2) and np.array_equal(T["hs_out"], s2)
+
+
+def test_encoder_stack_w8a8_host_device_graph(q4):
+    """The W8A8 stack: device call == host-buffer (end-to-end) call == CUDA-graph replay,
+    and layer 0 of the stack equals q4_encoder_layer_w8a8 on the same input."""
+    cfg = synth.BERT["base"]
+    B, S, L = 2, 128, 3
+    layers = [synth.layer_params(cfg, l, "stk8") for l in range(L)]
+    x = synth.hidden(B * S, cfg["hidden"], "stk8_x")
+    enc = q4.W8A8Encoder(cfg, layers)
+    xd = dev(x)
+    o1 = torch.empty_like(xd)
+    enc.forward(xd, o1, B, S)
+    oh = torch.empty(xd.shape, dtype=torch.float16).pin_memory()
+    enc.forward(torch.from_numpy(x).pin_memory(), oh, B, S)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, o1.cpu())
+    o2 = torch.empty_like(xd)
+    enc.capture(xd, o2, B, S)
+    enc.replay()
+    assert torch.equal(o2, o1)
+    one = q4.W8A8Encoder(cfg, layers[:1])
+    o3 = torch.empty_like(xd)
+    one.forward(xd, o3, B, S)
+    xq, xs = q4.quantize_rows_i8(xd)
+    ref = q4.encoder_layer(cfg, one.weights[0], B, S, xd, xq, xs, bits=8)
+    assert torch.equal(o3, ref["h_out"])
