@@ -411,7 +411,8 @@ def main():
 
 
 def side_measurements(q4, synth, torch, np, dev, args):
-    """Latency configs (BASELINE configs[1], [2]) and the FFN GEMM TOPS (configs[4])."""
+    """Latency configs (BASELINE configs[1], [2]), the FFN GEMM TOPS (configs[4]) and the
+    W8A8 baseline (encoder and GEMM at 8 bits, same kernels)."""
     out = {}
     stream = torch.cuda.current_stream()
     base = dict(synth.BERT["base"])
@@ -433,6 +434,28 @@ def side_measurements(q4, synth, torch, np, dev, args):
         out[name] = t[100]
         out[name.replace("p50", "p10")] = t[20]
         out[name.replace("p50", "p90")] = t[180]
+    # The paper's INT4-vs-INT8 comparison (Fig. e2e_i4_i8): the W8A8
+    # baseline encoder (same kernels at 8 bits) on the bench workload and the latency config
+    for size, L, B, name in (("large", 24, 256, "w8a8_bert_large_24l_bs256"), ("base", 12, 1, "w8a8_bert_base_12l_bs1")):
+        c = dict(synth.BERT[size])
+        enc = q4.W8A8Encoder(c, [synth.layer_params(c, l, "bert") for l in range(L)], device=dev)
+        x = torch.from_numpy(np.concatenate([synth.hidden(128, c["hidden"], "input", b) for b in range(B)])).to(dev)
+        o = torch.empty_like(x)
+        enc.capture(x, o, B, 128)
+        for _ in range(5):
+            enc.replay()
+        n = 20 if B > 1 else 200
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
+        torch.cuda.synchronize()
+        evs[0].record(stream)
+        for i in range(n):
+            enc.replay()
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        t = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(n))
+        out[name + "_p50_ms"] = t[n // 2]
+        out[name + "_seq_per_s"] = B / (t[n // 2] * 1e-3)
+        del enc
     # GEMM TOPS at the BERT-large FFN shapes, M = 32768 (tcgen05 vs legacy mma.sync)
     pk = peaks()
     for (Nn, K) in ((4096, 1024), (1024, 4096)):
@@ -441,6 +464,20 @@ def side_measurements(q4, synth, torch, np, dev, args):
         w = torch.from_numpy(synth.random_packed(Nn, K, f"sw_w{Nn}")).to(dev)
         sa = torch.from_numpy(synth.random_scales(M, "sw_sa")).to(dev)
         sw = torch.from_numpy(synth.random_scales(Nn, "sw_sw")).to(dev)
+        a8 = torch.from_numpy(synth.random_i8(M, K, f"sw_a8{K}")).to(dev)
+        w8 = torch.from_numpy(synth.random_i8(Nn, K, f"sw_w8{Nn}")).to(dev)
+        o = q4.w8a8_linear(a8, sa, w8, sw, q4.EPI_F16)
+        for _ in range(3):
+            q4.w8a8_linear(a8, sa, w8, sw, q4.EPI_F16, out=o)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(10):
+            q4.w8a8_linear(a8, sa, w8, sw, q4.EPI_F16, out=o)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tops = 2.0 * M * Nn * K / (e0.elapsed_time(e1) / 10 * 1e-3) / 1e12
+        out[f"gemm_f16_M{M}_N{Nn}_K{K}_w8a8_tcgen05_TOPS"] = tops
+        out[f"gemm_f16_M{M}_N{Nn}_K{K}_w8a8_tcgen05_frac_int8_peak"] = tops / pk["int8_tops"]
         for ml, mname in ((1, "tcgen05"), (2, "mma_sync_s8"), (3, "mma_sync_s4")):
             o = q4.w4a4_linear(a, sa, w, sw, q4.EPI_F16, mainloop=ml)
             for _ in range(3):
