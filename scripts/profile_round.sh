@@ -9,7 +9,7 @@ B="python bench.py --steps 2 --warmup 1 --no-extras --no-cpu-baseline --no-e2e"
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv \
   --log-file gpurun_out/${R}_launches.csv $B > gpurun_out/${R}_ncu_list.log 2>&1
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on \
-  --kernel-name-base mangled -k regex:"ILi256ELi2ELb1" -s 2 -c 1 -o gpurun_out/${R}_ffn1 \
+  --kernel-name-base mangled -k regex:"ILi256ELi2ELb1ELb0" -s 1 -c 1 -o gpurun_out/${R}_ffn1 \
   python bench.py --steps 2 --warmup 1 --layers 1 --no-extras --no-cpu-baseline --no-e2e > gpurun_out/${R}_ncu_full.log 2>&1
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on \
   -k regex:"attention|w4a4" -s 0 -c 5 -o gpurun_out/${R}_layer \
