@@ -65,6 +65,7 @@ def lib():
         L.oracle_gemm_i32_i8.argtypes = [P, P, I64, I64, I64, P, I]
         L.oracle_w8a8_linear.argtypes = [P, P, P, P, I64, I64, I64, I, P, P, P, P, D, F,
                                          P, P, P, P, I]
+        L.oracle_f16_linear.argtypes = [P, P, I64, I64, I64, I, P, P, P, P, D, F, P, P, P, I]
         _lib = L
     return _lib
 
@@ -197,6 +198,25 @@ def w8a8_linear(a_codes, a_scales, w_codes, w_scales, M, N, K, epi=EPI_F16, bias
                                   epi, _p(bias), _p(residual), _p(gamma), _p(beta), ln_eps, clip,
                                   _p(i32), _p(f16), _p(codes), _p(scales), threads)
     _check(rc, "w8a8_linear")
+    return out
+
+
+def f16_linear(a, w, M, N, K, epi=EPI_F16, bias=None, residual=None, gamma=None, beta=None,
+               ln_eps=1e-12, clip=0.0, want_f16=True, threads: int = 0):
+    """O-14: fp16 operands, fp64 sum, the O-5..O-7 epilogues (INT4 codes for *_Q4)."""
+    a, w = _c(a, np.float16), _c(w, np.float16)
+    bias, residual = _c(bias, np.float16), _c(residual, np.float16)
+    gamma, beta = _c(gamma, np.float16), _c(beta, np.float16)
+    out = {}
+    f16 = codes = scales = None
+    if epi == EPI_F16 or epi == EPI_RESLN_Q4 or (epi == EPI_GELU_Q4 and want_f16):
+        f16 = out["f16"] = np.zeros((M, N), np.float16)
+    if epi in (EPI_GELU_Q4, EPI_RESLN_Q4):
+        codes = out["codes"] = np.zeros((M, (N + 1) // 2), np.uint8)
+        scales = out["scales"] = np.zeros(M, np.float32)
+    rc = lib().oracle_f16_linear(_p(a), _p(w), M, N, K, epi, _p(bias), _p(residual), _p(gamma), _p(beta),
+                                 ln_eps, clip, _p(f16), _p(codes), _p(scales), threads)
+    _check(rc, "f16_linear")
     return out
 
 

@@ -210,7 +210,7 @@ static double gelu_erf(double t) { return 0.5 * t * (1.0 + erf(t / sqrt(2.0))); 
 
 /* Dequant + bias + epilogue over an exact accumulator, requantizing to qmax = 7 (codes
  * packed two per byte into out_codes4) or qmax = 127 (int8 codes into out_codes8). */
-static int linear_epilogue(const int32_t* acc, const float* a_scales, const float* w_scales,
+static int linear_epilogue(const int32_t* acc, const double* dacc, const float* a_scales, const float* w_scales,
                            int64_t M, int64_t N, int epi_kind, const uint16_t* bias,
                            const uint16_t* residual, const uint16_t* gamma, const uint16_t* beta,
                            double ln_eps, float clip, int32_t* out_i32, uint16_t* out_f16,
@@ -224,7 +224,7 @@ static int linear_epilogue(const int32_t* acc, const float* a_scales, const floa
     int8_t* q = (int8_t*)malloc((size_t)N);
     for (int64_t n = 0; n < N; ++n) {
       /* dequantize with the token x channel scales, add bias */
-      t[n] = (double)acc[m * N + n] * (double)a_scales[m] * (double)w_scales[n] +
+      t[n] = (dacc ? dacc[m * N + n] : (double)acc[m * N + n] * (double)a_scales[m] * (double)w_scales[n]) +
              (bias ? oracle_f16_to_f64(bias[n]) : 0.0);
     }
     switch (epi_kind) {
@@ -294,7 +294,7 @@ int oracle_w4a4_linear(const uint8_t* a_codes, const float* a_scales,
   int32_t* acc = (int32_t*)malloc((size_t)(M * N > 0 ? M * N : 1) * sizeof(int32_t));
   int rc = oracle_gemm_i32(a_codes, w_codes, M, N, K, acc, threads);
   if (!rc)
-    rc = linear_epilogue(acc, a_scales, w_scales, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, clip,
+    rc = linear_epilogue(acc, NULL, a_scales, w_scales, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, clip,
                          out_i32, out_f16, 7, out_codes, NULL, out_scales, threads);
   free(acc);
   return rc;
@@ -310,9 +310,32 @@ int oracle_w8a8_linear(const int8_t* a_codes, const float* a_scales, const int8_
   int32_t* acc = (int32_t*)malloc((size_t)(M * N > 0 ? M * N : 1) * sizeof(int32_t));
   int rc = gemm_i32_q(a_codes, w_codes, M, N, K, acc, threads);
   if (!rc)
-    rc = linear_epilogue(acc, a_scales, w_scales, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, clip,
+    rc = linear_epilogue(acc, NULL, a_scales, w_scales, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, clip,
                          out_i32, out_f16, 127, NULL, out_codes, out_scales, threads);
   free(acc);
+  return rc;
+}
+
+/* O-14: the unquantized (FP16) linear of a per-part strategy: t = sum_k a w in fp64 over the
+ * fp16 operands, then the O-5..O-7 epilogues (INT4 requant for the *_Q4 kinds). */
+int oracle_f16_linear(const uint16_t* a, const uint16_t* w, int64_t M, int64_t N, int64_t K, int epi_kind,
+                      const uint16_t* bias, const uint16_t* residual, const uint16_t* gamma,
+                      const uint16_t* beta, double ln_eps, float clip, uint16_t* out_f16,
+                      uint8_t* out_codes, float* out_scales, int threads) {
+  if (epi_kind == ORACLE_EPI_I32) return -1;
+  if (!epilogue_args_ok(M, N, K, epi_kind, residual, gamma, beta, clip, NULL, out_f16, out_codes, out_scales))
+    return -1;
+  double* dacc = (double*)malloc((size_t)(M * N > 0 ? M * N : 1) * sizeof(double));
+#pragma omp parallel for schedule(static) OMP_THREADS(threads)
+  for (int64_t m = 0; m < M; ++m)
+    for (int64_t n = 0; n < N; ++n) {
+      double sacc = 0.0;
+      for (int64_t k = 0; k < K; ++k) sacc += oracle_f16_to_f64(a[m * K + k]) * oracle_f16_to_f64(w[n * K + k]);
+      dacc[m * N + n] = sacc;
+    }
+  int rc = linear_epilogue(NULL, dacc, NULL, NULL, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, clip, NULL,
+                           out_f16, 7, out_codes, NULL, out_scales, threads);
+  free(dacc);
   return rc;
 }
 

@@ -134,6 +134,15 @@ int oracle_w8a8_linear(const int8_t* a_codes, const float* a_scales, const int8_
                        const uint16_t* beta, double ln_eps, float clip, int32_t* out_i32,
                        uint16_t* out_f16, int8_t* out_codes, float* out_scales, int threads);
 
+/* O-14  FP16 linear of the unquantized parts of a per-part quantization strategy
+ * (SURVEY 8(f) NEXT-1): t = sum_k a[m,k] w[n,k] over fp16 operands in
+ * fp64 (+ bias), then the O-5..O-7 epilogues F16 / GELU_Q4 / RESLN_Q4 (INT4 requant by O-1).
+ * I32 is not defined here (-1). */
+int oracle_f16_linear(const uint16_t* a, const uint16_t* w, int64_t M, int64_t N, int64_t K, int epi_kind,
+                      const uint16_t* bias, const uint16_t* residual, const uint16_t* gamma,
+                      const uint16_t* beta, double ln_eps, float clip, uint16_t* out_f16,
+                      uint8_t* out_codes, float* out_scales, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -141,3 +141,36 @@ def test_w8a8_gelu_and_resln_epilogues(orc):
     assert f16ulp_close(out["f16"], ref.numpy().astype(np.float16), 1)
     c2, s2 = orc.quantize_rows_i8(out["f16"])
     assert np.array_equal(c2, out["codes"]) and np.array_equal(s2, out["scales"])
+
+
+# ------------------------------------------------------------------ O-14 (FP16 parts, NEXT-1)
+def test_f16_linear_vs_torch_fp64(orc):
+    """The unquantized linear of a per-part strategy: fp64 F.linear on the fp16 operands
+    (1 fp16 ulp), torch F.gelu / F.layer_norm for the fused epilogues, codes = O-1(y)."""
+    M, N, K = 48, 512, 384
+    a, w = synth.hidden(M, K, "t16_a"), synth.weight(N, K, "t16_w") * 8
+    b = synth.bias(N, "t16_b")
+    t = F.linear(torch.tensor(a, dtype=torch.float64), torch.tensor(w, dtype=torch.float64),
+                 torch.tensor(b, dtype=torch.float64))
+    out = orc.f16_linear(a, w, M, N, K, orc.EPI_F16, bias=b)
+    assert f16ulp_close(out["f16"], t.numpy().astype(np.float16), 1)
+    out = orc.f16_linear(a, w, M, N, K, orc.EPI_GELU_Q4, bias=b)
+    assert f16ulp_close(out["f16"], F.gelu(t, approximate="none").numpy().astype(np.float16), 1)
+    c2, s2 = orc.quantize_rows(out["f16"])
+    assert np.array_equal(c2, out["codes"]) and np.array_equal(s2, out["scales"])
+    res = synth.hidden(M, N, "t16_r")
+    gam, bet = synth.ln_params(N, "t16_ln")
+    out = orc.f16_linear(a, w, M, N, K, orc.EPI_RESLN_Q4, bias=b, residual=res, gamma=gam, beta=bet)
+    ref = F.layer_norm(t + torch.tensor(res.astype(np.float64)), (N,), torch.tensor(gam, dtype=torch.float64),
+                       torch.tensor(bet, dtype=torch.float64), eps=1e-12)
+    assert f16ulp_close(out["f16"], ref.numpy().astype(np.float16), 1)
+    c2, s2 = orc.quantize_rows(out["f16"])
+    assert np.array_equal(c2, out["codes"]) and np.array_equal(s2, out["scales"])
+    # an fp16 operand pair that is exactly an INT4 problem gives the W4A4 oracle's result
+    g = np.random.default_rng(15)
+    qa = g.integers(-7, 8, (M, K)).astype(np.int8)
+    qw = g.integers(-7, 8, (N, K)).astype(np.int8)
+    f = orc.f16_linear(qa.astype(np.float16), qw.astype(np.float16), M, N, K, orc.EPI_F16)["f16"]
+    q = orc.w4a4_linear(orc.pack_int4(qa), np.ones(M, np.float32), orc.pack_int4(qw), np.ones(N, np.float32),
+                        M, N, K, orc.EPI_F16)["f16"]
+    assert np.array_equal(f, q)
