@@ -164,6 +164,19 @@ Q4_API q4_status q4_w8a8_linear(const int8_t* a_codes, const float* a_scales, /*
                                 void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------
+ * FP16 linear for the unquantized parts of a per-part quantization strategy (SURVEY 8(f)
+ * NEXT-1; "the four model parts as modular components where quantization
+ * can be enabled or disabled separately").  a [M, K] and w [N, K] fp16 (nn.Linear
+ * orientation), t = sum_k a w in fp32 on the tensor cores (tcgen05.mma kind::f16) + bias;
+ * epilogues Q4_EPI_F16, Q4_EPI_GELU_Q4 and Q4_EPI_RESLN_Q4 exactly as q4_w4a4_linear
+ * (the *_Q4 kinds still emit INT4 codes for a quantized successor, plus the fp16 output).
+ * Requirements: N % 32 == 0 (row epilogues N % 64 == 0), K % 64 == 0, pointers 16-byte
+ * aligned; workspace q4_f16_linear_workspace for the row epilogues. */
+Q4_API size_t q4_f16_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind);
+Q4_API q4_status q4_f16_linear(const uint16_t* a, const uint16_t* w, int64_t M, int64_t N, int64_t K,
+                               const q4_epilogue* epi, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
  * a2' Offline weight prepack (once per weight, not on the forward path): packed INT4 codes
  * w_codes [N, K/2] -> w_i8 [N, K] int8 holding 16*q in the K order of the on-chip
  * activation unpack (per 32-element group: the 16 even-k values, then the 16 odd-k).

@@ -22,7 +22,7 @@ EXPORTS = (
     "q4_encoder_layer_workspace", "q4_encoder_layer", "q4_encoder_stack_workspace",
     "q4_encoder_stack", "q4_quantize_rows_i8", "q4_w8a8_linear_workspace", "q4_w8a8_linear",
     "q4_attention_f16_q8", "q4_encoder_layer_w8a8_workspace", "q4_encoder_layer_w8a8",
-    "q4_encoder_stack_w8a8_workspace", "q4_encoder_stack_w8a8",
+    "q4_encoder_stack_w8a8_workspace", "q4_encoder_stack_w8a8", "q4_f16_linear_workspace", "q4_f16_linear",
 )
 
 
@@ -95,6 +95,9 @@ def lib():
         L.q4_encoder_stack.argtypes = [C.POINTER(LayerCfg), C.POINTER(LayerWeights), I32, I64, I64, P,
                                        P, P, SZ, P]
         L.q4_attention_f16_q8.argtypes = [P, I64, I64, I32, I32, P, P, P, P]
+        L.q4_f16_linear_workspace.argtypes = [I64, I64, I64, I32]
+        L.q4_f16_linear_workspace.restype = SZ
+        L.q4_f16_linear.argtypes = [P, P, I64, I64, I64, C.POINTER(Epilogue), P, SZ, P]
         L.q4_encoder_layer_w8a8_workspace.argtypes = [C.POINTER(LayerCfg), I64, I64]
         L.q4_encoder_layer_w8a8_workspace.restype = SZ
         L.q4_encoder_layer_w8a8.argtypes = L.q4_encoder_layer.argtypes
@@ -106,7 +109,7 @@ def lib():
                 "q4_last_error", "q4_version", "q4_launch_count", "q4_w4a4_linear_workspace",
                 "q4_encoder_layer_workspace", "q4_encoder_stack_workspace",
                 "q4_w8a8_linear_workspace", "q4_encoder_layer_w8a8_workspace",
-                "q4_encoder_stack_w8a8_workspace") else C.c_int
+                "q4_encoder_stack_w8a8_workspace", "q4_f16_linear_workspace") else C.c_int
         _lib = L
     return _lib
 

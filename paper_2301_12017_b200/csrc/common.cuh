@@ -137,6 +137,13 @@ Q4_DEV void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t id
       : "memory");
 }
 // Arrive on an mbarrier when all previously issued tcgen05 ops of this thread complete.
+Q4_DEV void umma_f16kk(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
 Q4_DEV void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -199,6 +206,11 @@ Q4_DEV uint64_t umma_smem_desc(uint32_t saddr, uint32_t sbo_bytes, uint32_t layo
   d |= (uint64_t)1 << 46;                               // version = 1 (Blackwell)
   d |= (uint64_t)(layout & 7) << 61;
   return d;
+}
+// Instruction descriptor for kind::f16: f16 x f16 -> f32, both K-major, M x N.
+__host__ __device__ constexpr uint32_t umma_idesc_f16kk(int M, int N) {
+  return (1u << 4)  // c_format = F32 (a_format = b_format = F16: 0)
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 // Instruction descriptor for kind::i8: s8 x s8 -> s32, both K-major, M x N.
 __host__ __device__ constexpr uint32_t umma_idesc_i8(int M, int N) {

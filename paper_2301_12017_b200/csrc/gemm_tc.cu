@@ -261,6 +261,8 @@ Q4_DEV void requant16(const uint32_t (&h)[8], float amax, float r7, float clip, 
 
 // 32 accumulators (raw = 256*acc) of one row -> fp16 of t = acc*sa*sw + b (or GELU(t)),
 // packed in 16 words.  Column params come from the group's smem copy (broadcast LDS).
+// FACC: the accumulator holds fp32 bits (fp16-operand MMA) instead of an integer.
+template <bool FACC = false>
 Q4_DEV void dequant32(const uint32_t (&v)[32], float2 sa2, const float* sw, const float* bs, uint32_t (&h)[16],
                       bool gelu = false) {
   const float4* pw = reinterpret_cast<const float4*>(sw);
@@ -268,10 +270,12 @@ Q4_DEV void dequant32(const uint32_t (&v)[32], float2 sa2, const float* sw, cons
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const float4 w = pw[j], bb = pb[j];
-    float2 t0 = ffma2(fmul2(make_float2((float)(int)v[4 * j], (float)(int)v[4 * j + 1]), sa2), make_float2(w.x, w.y),
-                      make_float2(bb.x, bb.y));
-    float2 t1 = ffma2(fmul2(make_float2((float)(int)v[4 * j + 2], (float)(int)v[4 * j + 3]), sa2),
-                      make_float2(w.z, w.w), make_float2(bb.z, bb.w));
+    const float2 a0 = FACC ? make_float2(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]))
+                           : make_float2((float)(int)v[4 * j], (float)(int)v[4 * j + 1]);
+    const float2 a1 = FACC ? make_float2(__uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]))
+                           : make_float2((float)(int)v[4 * j + 2], (float)(int)v[4 * j + 3]);
+    float2 t0 = ffma2(fmul2(a0, sa2), make_float2(w.x, w.y), make_float2(bb.x, bb.y));
+    float2 t1 = ffma2(fmul2(a1, sa2), make_float2(w.z, w.w), make_float2(bb.z, bb.w));
     if (gelu) {
       t0 = gelu2(t0);
       t1 = gelu2(t1);
@@ -361,10 +365,15 @@ Q4_DEV void slab_load16(uint8_t* stg, const uint8_t* gbase, int row0, int r0, in
   }
 }
 
-template <int TN, int KIND, bool BI8, bool A8>
+// H16 (with A8, BI8): fp16 operands (the unquantized parts of a per-part quantization
+// strategy).  The byte-level staging is the A8 path unchanged (a 128-byte
+// k-block row = 64 fp16), the MMA is kind::f16 with fp32 accumulators, and the epilogue
+// reads the accumulator as fp32 with unit scales.
+template <int TN, int KIND, bool BI8, bool A8, bool H16 = false>
 __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     w4a4_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
   static_assert(!A8 || BI8, "W8A8 takes int8 weights through the BI8 path");
+  static_assert(!H16 || A8, "fp16 operands use the A8 staging");
   using C = TcCfg<TN, BI8, A8>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -451,7 +460,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
   } else if (warp == WM) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_i8(128, TN);
+      constexpr uint32_t idesc = H16 ? umma_idesc_f16kk(128, TN) : umma_idesc_i8(128, TN);
       uint32_t g = 0, tcount = 0;
       // profiling only (Q4_TRACE): per-tile (wait tempty, wait full_u total, issue span), slot 62
       unsigned long long* mtr = p.trace ? p.trace + ((size_t)blockIdx.x * 64 + 62) * 8 : nullptr;
@@ -473,9 +482,14 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
           const uint32_t ub = ua + C::A_UN;
           if (!(p.dbg & 4)) {
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks)
-              umma_i8(dt, umma_smem_desc(ua + ks * 32, 1024, 2), umma_smem_desc(ub + ks * 32, 1024, 2), idesc,
-                      (kb | ks) != 0);
+            for (int ks = 0; ks < 4; ++ks) {
+              if constexpr (H16)
+                umma_f16kk(dt, umma_smem_desc(ua + ks * 32, 1024, 2), umma_smem_desc(ub + ks * 32, 1024, 2), idesc,
+                           (kb | ks) != 0);
+              else
+                umma_i8(dt, umma_smem_desc(ua + ks * 32, 1024, 2), umma_smem_desc(ub + ks * 32, 1024, 2), idesc,
+                        (kb | ks) != 0);
+            }
           }
           umma_commit(&empty_u[su]);
         }
@@ -558,7 +572,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     {
       const int c0 = (blockIdx.x % p.ntn) * TN;
       for (int i = ew * 32 + lane; i < TN; i += 2 * GT) {
-        prm[i] = p.w_scales[c0 + i];
+        prm[i] = p.w_scales ? p.w_scales[c0 + i] : 1.0f;
         prm[TN + i] = p.bias ? __half2float(p.bias[c0 + i]) : 0.f;
         if constexpr (KIND == EPI_RESLN_Q4) {
           prm[2 * TN + i] = __half2float(p.gamma[c0 + i]);
@@ -590,7 +604,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
       const int c0 = nb * TN;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + b * TN;
       // W4A4: the unpacked operands are 16 q, so the accumulator is 256 x the code sum
-      const float sa = row_ok ? p.a_scales[gm] * (A8 ? 1.0f : 1.0f / 256.0f) : 0.f;
+      const float sa = row_ok ? (H16 ? 1.0f : p.a_scales[gm] * (A8 ? 1.0f : 1.0f / 256.0f)) : 0.f;
       const float2 sa2 = f2(sa);
       const uint4* resp = nullptr;
       uint4 rr[4];  // RESLN: residual of this thread's current chunk (first one loaded before the wait)
@@ -633,7 +647,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
               tmem_ld32(tbase + 32 * j, v);
               tmem_wait_ld();
               uint32_t h[16];
-              dequant32(v, sa2, prm + 32 * j, prm + TN + 32 * j, h);
+              dequant32<H16>(v, sa2, prm + 32 * j, prm + TN + 32 * j, h);
 #pragma unroll
               for (int u = 0; u < 4; ++u)
                 *reinterpret_cast<uint4*>(stg + slab_off(lane, (j & 1) * 4 + u)) =
@@ -674,7 +688,8 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
 #pragma unroll
               for (int hh = 0; hh < 2; ++hh) {
                 const int e = 4 * jj + 2 * hh;
-                const float2 t = ffma2(fmul2(make_float2((float)(int)v[e], (float)(int)v[e + 1]), sa2),
+                const float2 t = ffma2(fmul2(H16 ? make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1]))
+                                                 : make_float2((float)(int)v[e], (float)(int)v[e + 1]), sa2),
                                        hh ? make_float2(w.z, w.w) : make_float2(w.x, w.y),
                                        hh ? make_float2(bb.z, bb.w) : make_float2(bb.x, bb.y));
                 const float2 z = add_half2_f32(ru[e / 2], t);
@@ -754,7 +769,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
                 h[2 * i4 + 1] = pack_half2(y1.x, y1.y);
               }
             } else {
-              dequant32(v, sa2, prm + 32 * j, prm + TN + 32 * j, h, true);
+              dequant32<H16>(v, sa2, prm + 32 * j, prm + TN + 32 * j, h, true);
             }
             if (clip > 0.f) {
               const __half2 cl = __float2half2_rn(clip);
@@ -794,7 +809,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
         stamp(5);
         for (int kk = 0; kk < ntn; ++kk) amax = fmaxf(amax, __ldcg(&p.xamax[((size_t)mb * ntn + kk) * 128 + r]));
         // pass B: codes (R1-R3), packed, staged, coalesced stores
-        if constexpr (A8) {
+        if constexpr (A8 && !H16) {
           // W8A8: int8 codes (O-11), 64 bytes per 64-column slab row
           const float rq = amax > 0.f ? __fdiv_rn(127.0f, amax) : 0.f;
           for (int k = 0; k < NSL; ++k) {
@@ -901,10 +916,10 @@ int num_sms() {
   return n;
 }
 
-template <int TN, int KIND, bool BI8, bool A8>
+template <int TN, int KIND, bool BI8, bool A8, bool H16 = false>
 cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {
   using C = TcCfg<TN, BI8, A8>;
-  auto kern = w4a4_tc_kernel<TN, KIND, BI8, A8>;
+  auto kern = w4a4_tc_kernel<TN, KIND, BI8, A8, H16>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -976,6 +991,17 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
 
 template <int TN, bool BI8, bool A8 = false>
 cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s, const char** why) {
+  if constexpr (A8) {
+    if (g.f16_ops) {  // fp16 operands (q4_f16_linear): no I32 epilogue
+      switch (g.kind) {
+        case EPI_F16: return run_tc<TN, EPI_F16, true, true, true>(g, ws, wsb, s, why);
+        case EPI_GELU_Q4: return run_tc<TN, EPI_GELU_Q4, true, true, true>(g, ws, wsb, s, why);
+        case EPI_RESLN_Q4: return run_tc<TN, EPI_RESLN_Q4, true, true, true>(g, ws, wsb, s, why);
+      }
+      *why = "fp16 operands: no such epilogue";
+      return cudaErrorInvalidValue;
+    }
+  }
   switch (g.kind) {
     case EPI_I32: return run_tc<TN, EPI_I32, BI8, A8>(g, ws, wsb, s, why);
     case EPI_F16: return run_tc<TN, EPI_F16, BI8, A8>(g, ws, wsb, s, why);

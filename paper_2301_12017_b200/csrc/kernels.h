@@ -40,6 +40,8 @@ struct GemmArgs {
   const uint8_t* a_codes;  // [M, K/2]
   const int8_t* a_i8;      // W8A8: int8 activation codes [M, K] (then w_i8 holds int8 weight codes
                            // in natural K order and requant kinds write int8 codes [M, N]); else nullptr
+  bool f16_ops = false;    // with a_i8 / w_i8 pointing at fp16 [M, K] / [N, K] and K counted in
+                           // bytes (2 x elements): kind::f16 MMA, unit scales, INT4 requant
   const float* a_scales;   // [M]
   const uint8_t* w_codes;  // [N, K/2]
   const int8_t* w_i8;      // [N, K] prepacked int8 (q4_prepack_weights) or nullptr

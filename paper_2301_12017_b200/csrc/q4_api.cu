@@ -159,6 +159,69 @@ q4_status q4_w8a8_linear(const int8_t* a_codes, const float* a_scales, const int
   return Q4_OK;
 }
 
+size_t q4_f16_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind) {
+  return q4_w4a4_linear_workspace(M, N, K, kind);
+}
+
+q4_status q4_f16_linear(const uint16_t* a, const uint16_t* w, int64_t M, int64_t N, int64_t K, const q4_epilogue* epi,
+                        void* workspace, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (!epi) return fail(Q4_EINVAL, "q4_f16_linear: epi is NULL");
+  if (M < 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1 << 24) || K > (1 << 20))
+    return fail(Q4_ESHAPE, "q4_f16_linear: bad shape M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
+  if (N % 32) return fail(Q4_ESHAPE, "q4_f16_linear: N=%lld must be a multiple of 32", (long long)N);
+  if (K % 64) return fail(Q4_ESHAPE, "q4_f16_linear: K=%lld must be a multiple of 64 (one 128-byte k-block)", (long long)K);
+  const int kind = epi->kind;
+  if (kind != Q4_EPI_F16 && kind != Q4_EPI_GELU_Q4 && kind != Q4_EPI_RESLN_Q4)
+    return fail(Q4_EINVAL, "q4_f16_linear: epilogue kind %d (F16, GELU_Q4 or RESLN_Q4)", kind);
+  if (epi->mainloop != Q4_MAINLOOP_AUTO && epi->mainloop != Q4_MAINLOOP_TCGEN05)
+    return fail(Q4_EUNSUPPORTED, "q4_f16_linear: mainloop %d (tcgen05 only)", epi->mainloop);
+  if (M == 0) return Q4_OK;
+  if (!a || !w) return fail(Q4_EINVAL, "q4_f16_linear: NULL a/w");
+  if (!al16(a) || !al16(w)) return fail(Q4_EALIGN, "q4_f16_linear: a and w must be 16-byte aligned");
+  if ((epi->bias && !al4(epi->bias)) || (epi->gamma && !al4(epi->gamma)) || (epi->beta && !al4(epi->beta)))
+    return fail(Q4_EALIGN, "q4_f16_linear: bias/gamma/beta must be 4-byte aligned");
+  if (kind == Q4_EPI_F16 && (!epi->out_f16 || !al16(epi->out_f16)))
+    return fail(Q4_EINVAL, "q4_f16_linear(F16): out_f16 NULL or not 16-byte aligned");
+  if (kind == Q4_EPI_GELU_Q4) {
+    if (!epi->out_codes || !epi->out_scales) return fail(Q4_EINVAL, "q4_f16_linear(GELU_Q4): out_codes/out_scales NULL");
+    if (!al16(epi->out_codes) || (epi->out_f16 && !al16(epi->out_f16)))
+      return fail(Q4_EALIGN, "q4_f16_linear(GELU_Q4): outputs must be 16-byte aligned");
+  }
+  if (kind == Q4_EPI_RESLN_Q4) {
+    if (!epi->out_codes || !epi->out_scales || !epi->out_f16 || !epi->residual || !epi->gamma || !epi->beta)
+      return fail(Q4_EINVAL, "q4_f16_linear(RESLN_Q4): out_f16/out_codes/out_scales/residual/gamma/beta must be non-NULL");
+    if (!al16(epi->out_codes) || !al16(epi->out_f16) || !al16(epi->residual))
+      return fail(Q4_EALIGN, "q4_f16_linear(RESLN_Q4): out_f16/out_codes/residual must be 16-byte aligned");
+    if (!(epi->ln_eps >= 0.f)) return fail(Q4_EINVAL, "q4_f16_linear(RESLN_Q4): ln_eps=%g", epi->ln_eps);
+  }
+  if (!clip_ok(epi->requant_clip)) return fail(Q4_EINVAL, "q4_f16_linear: requant_clip=%g is not 0 or a positive fp16 value", epi->requant_clip);
+  if (kind == Q4_EPI_GELU_Q4 || kind == Q4_EPI_RESLN_Q4) {
+    if (N % 64) return fail(Q4_ESHAPE, "q4_f16_linear: N=%lld must be a multiple of 64 for row epilogues", (long long)N);
+    const size_t need = q4_f16_linear_workspace(M, N, K, kind);
+    if (!workspace || ws_bytes < need)
+      return fail(Q4_EINVAL, "q4_f16_linear: workspace %zu bytes < required %zu (q4_f16_linear_workspace)", ws_bytes, need);
+    if (!al16(workspace)) return fail(Q4_EALIGN, "q4_f16_linear: workspace must be 16-byte aligned");
+  }
+  q4::GemmArgs g;
+  g.a_codes = nullptr; g.a_i8 = reinterpret_cast<const int8_t*>(a); g.a_scales = nullptr;
+  g.w_codes = nullptr; g.w_i8 = reinterpret_cast<const int8_t*>(w); g.w_scales = nullptr;
+  g.f16_ops = true;
+  g.M = (int)M; g.N = (int)N; g.K = (int)(2 * K); g.kind = kind; g.mainloop = Q4_MAINLOOP_TCGEN05;
+  g.bias = reinterpret_cast<const __half*>(epi->bias);
+  g.residual = reinterpret_cast<const __half*>(epi->residual);
+  g.gamma = reinterpret_cast<const __half*>(epi->gamma);
+  g.beta = reinterpret_cast<const __half*>(epi->beta);
+  g.ln_eps = epi->ln_eps; g.clip = epi->requant_clip;
+  g.out_i32 = nullptr; g.out_f16 = reinterpret_cast<__half*>(epi->out_f16);
+  g.out_codes = epi->out_codes; g.out_scales = epi->out_scales;
+  const char* why = "";
+  cudaError_t e = q4::launch_w4a4_tc(g, workspace, ws_bytes, (cudaStream_t)stream, &why);
+  if (e == cudaErrorNotSupported) return fail(Q4_EUNSUPPORTED, "q4_f16_linear: %s (M=%lld N=%lld K=%lld)", why, (long long)M, (long long)N, (long long)K);
+  if (e != cudaSuccess) return fail(Q4_ECUDA, "q4_f16_linear: %s %s", cudaGetErrorString(e), why);
+  return Q4_OK;
+}
+
 size_t q4_w4a4_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind) {
   (void)K;
   if (kind != Q4_EPI_GELU_Q4 && kind != Q4_EPI_RESLN_Q4) return 0;

@@ -131,6 +131,37 @@ def w8a8_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None
     return o
 
 
+def f16_linear(a, w, kind=EPI_F16, *, bias=None, residual=None, gamma=None, beta=None, ln_eps=1e-12,
+               clip=0.0, f16_tap=False, out=None, workspace=None):
+    """FP16 linear (unquantized part of a per-part strategy): fp16 [M,K] x fp16 [N,K] on the
+    tensor cores + the same fused epilogues (F16 | GELU_Q4 | RESLN_Q4, INT4 codes)."""
+    _need(a, torch.float16, "a", 2)
+    _need(w, torch.float16, "w", 2)
+    for n, t in (("bias", bias), ("residual", residual), ("gamma", gamma), ("beta", beta)):
+        _need(t, torch.float16, n)
+    M, K = a.shape
+    N = w.shape[0]
+    if w.shape[1] != K:
+        raise ValueError(f"K mismatch: a {tuple(a.shape)} vs w {tuple(w.shape)}")
+    dev = a.device
+    o = dict(out or {})
+    if kind in (EPI_F16, EPI_RESLN_Q4) or (kind == EPI_GELU_Q4 and f16_tap):
+        o.setdefault("f16", torch.empty(M, N, dtype=torch.float16, device=dev))
+    if kind in (EPI_GELU_Q4, EPI_RESLN_Q4):
+        o.setdefault("codes", torch.empty(M, N // 2, dtype=torch.uint8, device=dev))
+        o.setdefault("scales", torch.empty(M, dtype=torch.float32, device=dev))
+    e = Epilogue(kind=kind, mainloop=0, bias=_ptr(bias), residual=_ptr(residual),
+                 gamma=_ptr(gamma), beta=_ptr(beta), ln_eps=ln_eps, requant_clip=clip,
+                 out_i32=None, out_f16=_ptr(o.get("f16")),
+                 out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")), w_i8=None)
+    ws_bytes = lib().q4_f16_linear_workspace(M, N, K, kind)
+    if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
+        workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
+    check(lib().q4_f16_linear(_ptr(a), _ptr(w), M, N, K, C.byref(e), _ptr(workspace),
+                              0 if workspace is None else workspace.numel(), _stream()))
+    return o
+
+
 def attention_f16_q4(qkv, B, S, heads, head_dim=64, f16_tap=False):
     """a7: fp16 QKV [B*S, 3h] -> (ctx codes [B*S, h/2], ctx scales [B*S][, ctx fp16])."""
     _need(qkv, torch.float16, "qkv", 2)

@@ -206,3 +206,30 @@ def test_encoder_stack_w8a8_host_device_graph(q4):
     xq, xs = q4.quantize_rows_i8(xd)
     ref = q4.encoder_layer(cfg, one.weights[0], B, S, xd, xq, xs, bits=8)
     assert torch.equal(o3, ref["h_out"])
+
+
+# ------------------------------------------------------------------ NEXT-1: FP16 parts
+@pytest.mark.parametrize("M,N,K", [(1, 768, 768), (129, 2304, 768), (300, 1024, 4096), (1029, 4096, 1024)])
+def test_f16_linear(q4, M, N, K):
+    """The FP16 tcgen05 GEMM (kind::f16, fp32 accumulate) with the fused epilogues against
+    O-14; INT4 codes decided from the GPU's own fp16 (R13)."""
+    a, w, b = synth.hidden(M, K, f"h16a{M}"), synth.weight(N, K, f"h16w{N}_{K}"), synth.bias(N, f"h16b{N}")
+    out = q4.f16_linear(dev(a), dev(w), q4.EPI_F16, bias=dev(b))
+    ref = orc.f16_linear(a, w, M, N, K, orc.EPI_F16, bias=b)["f16"]
+    assert_f16_close(host(out["f16"]), ref, "F16 linear")
+    out = q4.f16_linear(dev(a), dev(w), q4.EPI_GELU_Q4, bias=dev(b), f16_tap=True)
+    ref = orc.f16_linear(a, w, M, N, K, orc.EPI_GELU_Q4, bias=b)
+    y = host(out["f16"])
+    assert_f16_close(y, ref["f16"], "F16 linear GELU")
+    c2, s2 = orc.quantize_rows(y)
+    assert np.array_equal(host(out["codes"]), c2) and np.array_equal(host(out["scales"]), s2)
+    if N <= 1024:
+        res = synth.hidden(M, N, f"h16r{M}")
+        gam, bet = synth.ln_params(N, f"h16ln{N}")
+        out = q4.f16_linear(dev(a), dev(w), q4.EPI_RESLN_Q4, bias=dev(b), residual=dev(res), gamma=dev(gam),
+                            beta=dev(bet))
+        ref = orc.f16_linear(a, w, M, N, K, orc.EPI_RESLN_Q4, bias=b, residual=res, gamma=gam, beta=bet)
+        y = host(out["f16"])
+        assert_f16_close(y, ref["f16"], "F16 linear RESLN")
+        c2, s2 = orc.quantize_rows(y)
+        assert np.array_equal(host(out["codes"]), c2) and np.array_equal(host(out["scales"]), s2)
