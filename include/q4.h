@@ -216,6 +216,13 @@ Q4_API q4_status q4_attention_f16_q4(const uint16_t* qkv, int64_t B, int64_t S, 
 typedef struct {
   int32_t hidden, heads, head_dim, ffn;
   float ln_eps;
+  /* Per-part quantization strategy: bit 0 QKV
+   * projection, bit 1 attention output, bit 2 MLP intermediate, bit 3 MLP output run in
+   * FP16 (q4_f16_linear on the fp16 weights of the f* fields and the fp16 activations the
+   * previous step already produces); 0 = all four parts quantized ("qall").  The paper's
+   * best small-batch strategy "q3" (only the MLP intermediate quantized) is 0xB.  W4A4
+   * entry points only (the *_w8a8 ones require 0). */
+  int32_t fp16_parts;
 } q4_layer_cfg;
 typedef struct {
   const uint8_t *wqkv, *wo, *w1, *w2;   /* packed [3h,h/2], [h,h/2], [ffn,h/2], [h,ffn/2] */
@@ -223,6 +230,8 @@ typedef struct {
   const float *sqkv, *so, *s1, *s2;     /* per-output-channel scales                       */
   const uint16_t *bqkv, *bo, *b1, *b2;  /* fp16 biases                                      */
   const uint16_t *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+  const uint16_t *fqkv, *fo, *f1, *f2;  /* fp16 [N, K] weights of the FP16 parts (cfg->fp16_parts);
+                                           NULL when the part is quantized               */
 } q4_layer_weights;
 typedef struct {
   uint16_t *qkv, *ctx, *h1, *ffn1;

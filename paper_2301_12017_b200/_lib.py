@@ -44,11 +44,11 @@ class Epilogue(C.Structure):
 
 class LayerCfg(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("heads", C.c_int32), ("head_dim", C.c_int32),
-                ("ffn", C.c_int32), ("ln_eps", C.c_float)]
+                ("ffn", C.c_int32), ("ln_eps", C.c_float), ("fp16_parts", C.c_int32)]
 
 
 WEIGHT_FIELDS = ("wqkv", "wo", "w1", "w2", "wqkv8", "wo8", "w18", "w28", "sqkv", "so", "s1", "s2",
-                 "bqkv", "bo", "b1", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")
+                 "bqkv", "bo", "b1", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b", "fqkv", "fo", "f1", "f2")
 TAP_FIELDS = ("qkv", "ctx", "h1", "ffn1", "acc_qkv", "acc_o", "acc_1", "acc_2", "ctx_codes",
               "h1_codes", "f_codes", "ctx_scales", "h1_scales", "f_scales")
 

@@ -371,6 +371,7 @@ struct LayerWs {
   float* h1_scales;
   uint8_t* f_codes;
   float* f_scales;
+  uint16_t* ffn1;  // fp16 MLP intermediate, only when the MLP output part runs in FP16
   size_t bytes;
 };
 LayerWs layer_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base, bool i8 = false) {
@@ -396,6 +397,7 @@ LayerWs layer_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base, bool i8 = fals
   w.h1_scales = (float*)take((size_t)M * 4);
   w.f_codes = take((size_t)(M * f / cd));
   w.f_scales = (float*)take((size_t)M * 4);
+  w.ffn1 = (!i8 && (c->fp16_parts & 8)) ? (uint16_t*)take((size_t)M * f * 2) : nullptr;
   w.bytes = o;
   return w;
 }
@@ -405,6 +407,7 @@ q4_status check_cfg(const q4_layer_cfg* c, const char* who) {
     return fail(Q4_EUNSUPPORTED, "%s: hidden=%d heads=%d head_dim=%d (need head_dim 64, hidden = 64*heads <= 1024)",
                 who, c->hidden, c->heads, c->head_dim);
   if (c->ffn % 32 || c->ffn <= 0 || c->ffn > 4096) return fail(Q4_ESHAPE, "%s: ffn=%d (need multiple of 32, <= 4096)", who, c->ffn);
+  if (c->fp16_parts < 0 || c->fp16_parts > 15) return fail(Q4_EINVAL, "%s: fp16_parts=%d (bits 0..3)", who, c->fp16_parts);
   return Q4_OK;
 }
 }  // namespace
@@ -435,6 +438,10 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
   if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "%s: B=%lld S=%lld", who, (long long)B, (long long)S);
   const int64_t M = B * S, h = cfg->hidden, f = cfg->ffn;
   if (M == 0) return Q4_OK;
+  const int fp = cfg->fp16_parts;
+  if (i8 && fp) return fail(Q4_EUNSUPPORTED, "%s: fp16_parts=%d (the W8A8 baseline quantizes all four parts)", who, fp);
+  if (((fp & 1) && !w->fqkv) || ((fp & 2) && !w->fo) || ((fp & 4) && !w->f1) || ((fp & 8) && !w->f2))
+    return fail(Q4_EINVAL, "%s: fp16_parts=%d needs the fp16 weights (fqkv/fo/f1/f2) of those parts", who, fp);
   LayerWs ws = layer_ws(cfg, M, (uint8_t*)workspace, i8);
   if (!workspace || ws_bytes < ws.bytes)
     return fail(Q4_EINVAL, "%s: workspace %zu bytes < required %zu", who, ws_bytes, ws.bytes);
@@ -472,36 +479,58 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
                             &e, nullptr, 0, stream);
     return q4_w4a4_linear(ac, as, wc, wsc, M, N, K, &e, nullptr, 0, stream);
   };
+  // an FP16 part (strategy bit set): fp16 activation x fp16 weight, same epilogue
+  auto f16lin = [&](const uint16_t* a, const uint16_t* wf, int64_t N, int64_t K, q4_epilogue e) -> q4_status {
+    e.w_i8 = nullptr;
+    return q4_f16_linear(a, wf, M, N, K, &e, ws.gemm_ws, ws.gemm_ws_bytes, stream);
+  };
+  uint16_t* ctx_f16 = tp.ctx ? tp.ctx : ws.ctx;
+  uint16_t* ffn1 = tp.ffn1 ? tp.ffn1 : ws.ffn1;  // NULL unless tapped or the MLP output is FP16
   q4_epilogue e;
   // QKV projection: dequant + bias -> fp16
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_F16; e.bias = w->bqkv; e.out_f16 = qkv; e.w_i8 = w->wqkv8;
-  if ((st = lin(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, e))) return st;
-  if ((st = acc_tap(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, tp.acc_qkv))) return st;
+  if (fp & 1) {
+    if ((st = f16lin(h_in, w->fqkv, 3 * h, h, e))) return st;
+  } else {
+    if ((st = lin(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, e))) return st;
+    if ((st = acc_tap(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, tp.acc_qkv))) return st;
+  }
   // FP16 attention + fused per-token ctx quantize
-  if ((st = i8 ? q4_attention_f16_q8(qkv, B, S, cfg->heads, cfg->head_dim, tp.ctx ? tp.ctx : ws.ctx,
+  if ((st = i8 ? q4_attention_f16_q8(qkv, B, S, cfg->heads, cfg->head_dim, ctx_f16,
                                      reinterpret_cast<int8_t*>(ctx_codes), ctx_scales, stream)
-              : q4_attention_f16_q4(qkv, B, S, cfg->heads, cfg->head_dim, tp.ctx ? tp.ctx : ws.ctx, ctx_codes,
-                                    ctx_scales, stream)))
+              : q4_attention_f16_q4(qkv, B, S, cfg->heads, cfg->head_dim, ctx_f16, ctx_codes, ctx_scales, stream)))
     return st;
   // attention output: dequant + bias + residual(h_in) + LN1 + requant
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_RESLN_Q4; e.bias = w->bo; e.residual = h_in; e.gamma = w->ln1_g; e.beta = w->ln1_b;
   e.ln_eps = cfg->ln_eps; e.out_f16 = h1; e.out_codes = h1_codes; e.out_scales = h1_scales; e.w_i8 = w->wo8;
-  if ((st = lin(ctx_codes, ctx_scales, w->wo, w->so, h, h, e))) return st;
-  if ((st = acc_tap(ctx_codes, ctx_scales, w->wo, w->so, h, h, tp.acc_o))) return st;
-  // MLP intermediate: dequant + bias + GELU + requant
+  if (fp & 2) {
+    if ((st = f16lin(ctx_f16, w->fo, h, h, e))) return st;
+  } else {
+    if ((st = lin(ctx_codes, ctx_scales, w->wo, w->so, h, h, e))) return st;
+    if ((st = acc_tap(ctx_codes, ctx_scales, w->wo, w->so, h, h, tp.acc_o))) return st;
+  }
+  // MLP intermediate: dequant + bias + GELU + requant (+ fp16 output for an FP16 MLP output)
   memset(&e, 0, sizeof e);
-  e.kind = Q4_EPI_GELU_Q4; e.bias = w->b1; e.out_f16 = tp.ffn1; e.out_codes = f_codes; e.out_scales = f_scales;
+  e.kind = Q4_EPI_GELU_Q4; e.bias = w->b1; e.out_f16 = ffn1; e.out_codes = f_codes; e.out_scales = f_scales;
   e.w_i8 = w->w18;
-  if ((st = lin(h1_codes, h1_scales, w->w1, w->s1, f, h, e))) return st;
-  if ((st = acc_tap(h1_codes, h1_scales, w->w1, w->s1, f, h, tp.acc_1))) return st;
+  if (fp & 4) {
+    if ((st = f16lin(h1, w->f1, f, h, e))) return st;
+  } else {
+    if ((st = lin(h1_codes, h1_scales, w->w1, w->s1, f, h, e))) return st;
+    if ((st = acc_tap(h1_codes, h1_scales, w->w1, w->s1, f, h, tp.acc_1))) return st;
+  }
   // MLP output: dequant + bias + residual(h1) + LN2 + requant
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_RESLN_Q4; e.bias = w->b2; e.residual = h1; e.gamma = w->ln2_g; e.beta = w->ln2_b;
   e.ln_eps = cfg->ln_eps; e.out_f16 = h_out; e.out_codes = hq_out; e.out_scales = hs_out; e.w_i8 = w->w28;
-  if ((st = lin(f_codes, f_scales, w->w2, w->s2, h, f, e))) return st;
-  if ((st = acc_tap(f_codes, f_scales, w->w2, w->s2, h, f, tp.acc_2))) return st;
+  if (fp & 8) {
+    if ((st = f16lin(ffn1, w->f2, h, f, e))) return st;
+  } else {
+    if ((st = lin(f_codes, f_scales, w->w2, w->s2, h, f, e))) return st;
+    if ((st = acc_tap(f_codes, f_scales, w->w2, w->s2, h, f, tp.acc_2))) return st;
+  }
   return Q4_OK;
 }
 }  // namespace

@@ -189,7 +189,8 @@ def attention_f16_q8(qkv, B, S, heads, head_dim=64, f16_tap=False):
 
 
 def layer_cfg(cfg: dict) -> LayerCfg:
-    return LayerCfg(cfg["hidden"], cfg["heads"], cfg["head_dim"], cfg["ffn"], cfg.get("ln_eps", 1e-12))
+    return LayerCfg(cfg["hidden"], cfg["heads"], cfg["head_dim"], cfg["ffn"], cfg.get("ln_eps", 1e-12),
+                    int(cfg.get("fp16_parts", 0)))
 
 
 def prepack_weights(w_codes: torch.Tensor) -> torch.Tensor:
@@ -208,15 +209,20 @@ def layer_weights(w: dict) -> LayerWeights:
                            for k in _lib.WEIGHT_FIELDS})
 
 
-def quantize_layer(params: dict, device="cuda", prepack: bool = True, bits: int = 4) -> dict:
+def quantize_layer(params: dict, device="cuda", prepack: bool = True, bits: int = 4,
+                   fp16_parts: int = 0) -> dict:
     """Offline weight prep (a2, not timed): fp16 [out, in] weights -> per-output-channel
     INT4 codes + scales on the device (and, with prepack, the MMA-ready int8 copy);
-    biases and LN parameters copied as fp16.  bits=8: the W8A8 baseline's int8 codes."""
+    biases and LN parameters copied as fp16.  bits=8: the W8A8 baseline's int8 codes.
+    fp16_parts (strategy bits, q4_layer_cfg): those parts also keep their fp16 weights
+    (fqkv / fo / f1 / f2)."""
     if bits not in (4, 8):
         raise ValueError(f"bits={bits} (4 or 8)")
     w = {}
-    for k in ("wqkv", "wo", "w1", "w2"):
+    for i, k in enumerate(("wqkv", "wo", "w1", "w2")):
         t = torch.as_tensor(params[k]).to(device=device, dtype=torch.float16).contiguous()
+        if fp16_parts >> i & 1:
+            w["f" + k[1:]] = t
         if bits == 8:
             w[k], w["s" + k[1:]] = quantize_rows_i8(t)
             continue

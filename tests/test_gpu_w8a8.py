@@ -233,3 +233,61 @@ def test_f16_linear(q4, M, N, K):
         assert_f16_close(y, ref["f16"], "F16 linear RESLN")
         c2, s2 = orc.quantize_rows(y)
         assert np.array_equal(host(out["codes"]), c2) and np.array_equal(host(out["scales"]), s2)
+
+
+@pytest.mark.parametrize("fp16_parts", [0xB, 0x4, 0xF, 0x6])
+def test_encoder_layer_strategy_teacher_forced(q4, fp16_parts):
+    """Per-part quantization strategy: each part runs W4A4 or FP16 as the
+    mask says; every sub-step checked on the GPU's own inputs against O-5..O-8 / O-14."""
+    cfg = dict(synth.BERT["base"], fp16_parts=fp16_parts)
+    B, S = 2, 128
+    M, h, f = B * S, cfg["hidden"], cfg["ffn"]
+    p = synth.layer_params(cfg, 0, "encs")
+    x = synth.hidden(M, h, "encs_x")
+    w = q4.quantize_layer(p, fp16_parts=fp16_parts)
+    xq, xs = q4.quantize_rows(dev(x))
+    out = q4.encoder_layer(cfg, w, B, S, dev(x), xq, xs, taps=True)
+    T = {k: host(v) for k, v in out.items()}
+    W = {k: host(v) for k, v in w.items()}
+
+    def part(i, a16, codes, scales, wname, N, K, epi, **kw):
+        if fp16_parts >> i & 1:
+            return orc.f16_linear(a16, p["w" + wname], M, N, K, epi, **kw)
+        return orc.w4a4_linear(codes, scales, W["w" + wname], W["s" + wname], M, N, K, epi, **kw)
+
+    rq = part(0, x, host(xq), host(xs), "qkv", 3 * h, h, orc.EPI_F16, bias=p["bqkv"])
+    assert_f16_close(T["qkv"], rq["f16"], "qkv")
+    rctx, _, _ = orc.attention(T["qkv"], B, S, cfg["heads"], 64)
+    assert_f16_close(T["ctx"], rctx, "ctx")
+    r1 = part(1, T["ctx"], T["ctx_codes"], T["ctx_scales"], "o", h, h, orc.EPI_RESLN_Q4, bias=p["bo"],
+              residual=x, gamma=p["ln1_g"], beta=p["ln1_b"])
+    assert_f16_close(T["h1"], r1["f16"], "h1")
+    c2, s2 = orc.quantize_rows(T["h1"])
+    assert np.array_equal(T["h1_codes"], c2) and np.array_equal(T["h1_scales"], s2)
+    r2 = part(2, T["h1"], T["h1_codes"], T["h1_scales"], "1", f, h, orc.EPI_GELU_Q4, bias=p["b1"])
+    assert_f16_close(T["ffn1"], r2["f16"], "ffn1")
+    c2, s2 = orc.quantize_rows(T["ffn1"])
+    assert np.array_equal(T["f_codes"], c2) and np.array_equal(T["f_scales"], s2)
+    r3 = part(3, T["ffn1"], T["f_codes"], T["f_scales"], "2", h, f, orc.EPI_RESLN_Q4, bias=p["b2"],
+              residual=T["h1"], gamma=p["ln2_g"], beta=p["ln2_b"])
+    assert_f16_close(T["h_out"], r3["f16"], "h_out")
+
+
+def test_encoder_stack_strategy_graph(q4):
+    """q3-only strategy (0xB): device call == host-buffer call == graph replay."""
+    cfg = synth.BERT["base"]
+    B, S, L = 1, 128, 2
+    layers = [synth.layer_params(cfg, l, "stks") for l in range(L)]
+    x = synth.hidden(B * S, cfg["hidden"], "stks_x")
+    enc = q4.W4A4Encoder(cfg, layers, fp16_parts=0xB)
+    xd = dev(x)
+    o1 = torch.empty_like(xd)
+    enc.forward(xd, o1, B, S)
+    oh = torch.empty(xd.shape, dtype=torch.float16).pin_memory()
+    enc.forward(torch.from_numpy(x).pin_memory(), oh, B, S)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, o1.cpu())
+    o2 = torch.empty_like(xd)
+    enc.capture(xd, o2, B, S)
+    enc.replay()
+    assert torch.equal(o2, o1)
