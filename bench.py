@@ -456,6 +456,17 @@ def side_measurements(q4, synth, torch, np, dev, args):
         out[name + "_p50_ms"] = t[n // 2]
         out[name + "_seq_per_s"] = B / (t[n // 2] * 1e-3)
         del enc
+    # Per-part quantization strategy tuner (Fig. e2e_i4_fti8 annotations):
+    # all 16 strategies of BERT-base 12 L at the paper's small (bs-seq) points and the
+    # latency config; argmin reported with the qall and all-FP16 times
+    from paper_2301_12017_b200 import tune
+    base12 = [synth.layer_params(base, l, "bert") for l in range(12)]
+    for (B, S) in ((1, 32), (8, 32), (1, 128)):
+        x = torch.from_numpy(np.concatenate([synth.hidden(S, 768, "input", b) for b in range(B)])).to(dev)
+        r = tune.tune(base, base12, B, S, device=dev, reps=50, x=x)
+        out[f"strategy_bert_base_12l_bs{B}_seq{S}"] = {"best": r["best"], "best_ms": r["times"][r["best"]],
+                                                       "qall_ms": r["times"]["qall"], "fp16_ms": r["times"]["fp16"],
+                                                       "q3_ms": r["times"]["q3"], "times": r["times"]}
     # GEMM TOPS at the BERT-large FFN shapes, M = 32768 (tcgen05 vs legacy mma.sync)
     pk = peaks()
     for (Nn, K) in ((4096, 1024), (1024, 4096)):

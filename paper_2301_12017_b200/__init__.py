@@ -12,6 +12,7 @@ from ._lib import (EPI_F16, EPI_GELU_Q4, EPI_I32, EPI_RESLN_Q4, MAINLOOP_AUTO,
 from .ops import (attention_f16_q4, encoder_layer, prepack_weights, quantize_layer, quantize_rows,
                   quantize_rows_i8, w4a4_linear, w8a8_linear, attention_f16_q8, f16_linear)
 from .encoder import W4A4Encoder, W8A8Encoder
+from . import tune
 
 __all__ = [
     "EPI_I32", "EPI_F16", "EPI_GELU_Q4", "EPI_RESLN_Q4", "MAINLOOP_AUTO", "MAINLOOP_TCGEN05",
