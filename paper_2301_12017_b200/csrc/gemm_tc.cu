@@ -325,14 +325,15 @@ Q4_DEV void slab_load(uint8_t* stg, const uint8_t* gbase, int row0, int M, size_
 Q4_DEV void exchange_sync(unsigned* cnt, size_t dep, int ntn, int bar_id, int nthreads, bool leader, int dbg = 0) {
   named_bar(bar_id, nthreads);
   if (leader && !(dbg & 32)) {
-    __threadfence();
-    atomicAdd(cnt, 1u);
+    // release-add: the group's partial stores (ordered before it by the bar.sync) become
+    // visible with the arrival; the acquire loads order the partial reads after the others'
+    // arrivals (same pattern as a grid barrier; no full fences needed)
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
     unsigned polls = 0;
     while (ld_acquire_gpu(cnt) < (unsigned)ntn) {
       __nanosleep(32);
       if (++polls > (1u << 26)) __trap();
     }
-    __threadfence();
     if (atomicAdd(cnt + dep, 1u) == (unsigned)ntn - 1) {  // everyone has seen the full count
       cnt[0] = 0u;
       cnt[dep] = 0u;
