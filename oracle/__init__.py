@@ -66,6 +66,8 @@ def lib():
         L.oracle_w8a8_linear.argtypes = [P, P, P, P, I64, I64, I64, I, P, P, P, P, D, F,
                                          P, P, P, P, I]
         L.oracle_f16_linear.argtypes = [P, P, I64, I64, I64, I, P, P, P, P, D, F, P, P, P, I]
+        L.oracle_quantize_rows_asym.argtypes = [P, I64, I64, I64, P, P, P, I]
+        L.oracle_w4a4_asym_linear.argtypes = [P, P, P, P, P, I64, I64, I64, I, P, P, P, I]
         _lib = L
     return _lib
 
@@ -217,6 +219,46 @@ def f16_linear(a, w, M, N, K, epi=EPI_F16, bias=None, residual=None, gamma=None,
     rc = lib().oracle_f16_linear(_p(a), _p(w), M, N, K, epi, _p(bias), _p(residual), _p(gamma), _p(beta),
                                  ln_eps, clip, _p(f16), _p(codes), _p(scales), threads)
     _check(rc, "f16_linear")
+    return out
+
+
+# ---------------------------------------------------------------- O-15 / O-16 (asymmetric)
+def quantize_rows_asym(x: np.ndarray, threads: int = 0):
+    """O-15: x fp16 [rows, cols] -> (codes uint8 [rows, cols/2] unsigned nibbles, scales, zeros)."""
+    x = _c(x, np.float16)
+    rows, cols = x.shape
+    codes = np.zeros((rows, (cols + 1) // 2), np.uint8)
+    scales = np.zeros(rows, np.float32)
+    zeros = np.zeros(rows, np.float32)
+    _check(lib().oracle_quantize_rows_asym(_p(x), rows, cols, cols, _p(codes), _p(scales), _p(zeros), threads),
+           "quantize_rows_asym")
+    return codes, scales, zeros
+
+
+def unpack_u4(packed: np.ndarray, cols: int) -> np.ndarray:
+    """Unsigned nibbles (low = even index) -> uint8 [rows, cols] in [0, 15]."""
+    packed = np.asarray(packed, np.uint8)
+    q = np.zeros((packed.shape[0], cols), np.uint8)
+    q[:, 0::2] = packed[:, : (cols + 1) // 2] & 0xF
+    q[:, 1::2] = packed[:, : cols // 2] >> 4
+    return q
+
+
+def w4a4_asym_linear(a_codes, a_scales, a_zeros, w_codes, w_scales, M, N, K, epi=EPI_F16, bias=None,
+                     threads: int = 0):
+    """O-16: asymmetric-activation W4A4 linear, F16 or I32 epilogue."""
+    a_codes, w_codes = _c(a_codes, np.uint8), _c(w_codes, np.uint8)
+    a_scales, a_zeros, w_scales = _c(a_scales, np.float32), _c(a_zeros, np.float32), _c(w_scales, np.float32)
+    bias = _c(bias, np.float16)
+    out = {}
+    i32 = f16 = None
+    if epi == EPI_I32:
+        i32 = out["i32"] = np.zeros((M, N), np.int32)
+    else:
+        f16 = out["f16"] = np.zeros((M, N), np.float16)
+    rc = lib().oracle_w4a4_asym_linear(_p(a_codes), _p(a_scales), _p(a_zeros), _p(w_codes), _p(w_scales), M, N, K,
+                                       epi, _p(bias), _p(i32), _p(f16), threads)
+    _check(rc, "w4a4_asym_linear")
     return out
 
 

@@ -135,6 +135,43 @@ int oracle_quantize_rows_i8(const uint16_t* x, int64_t rows, int64_t cols, int64
   return 0;
 }
 
+/* O-15: asymmetric per-row INT4 (readings R17, R18).  x_zero = min(x'),
+ * D = max(x') - min(x') (exact), q = rhe(15 (x' - x_zero) / D) exactly in [0, 15] (integers in
+ * units of 2^-24: 15 (X - Z) < 2^46), scale = fl32(fl64(D) / 15) (fp64 division, then fp32);
+ * constant row -> scale 1, codes 0, zero = the constant.  Codes packed as
+ * unsigned nibbles, low nibble = even index. */
+int oracle_quantize_rows_asym(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x,
+                              uint8_t* codes, float* scales, float* zeros, int threads) {
+  if (rows < 0 || cols <= 0 || ld_x < cols) return -1;
+  int64_t pb = (cols + 1) / 2;
+#pragma omp parallel for schedule(static) OMP_THREADS(threads)
+  for (int64_t r = 0; r < rows; ++r) {
+    const uint16_t* xr = x + r * ld_x;
+    double mn = oracle_f16_to_f64(xr[0]), mx = mn;
+    for (int64_t j = 1; j < cols; ++j) {
+      double v = oracle_f16_to_f64(xr[j]);
+      if (v < mn) mn = v;
+      if (v > mx) mx = v;
+    }
+    zeros[r] = (float)mn;
+    uint8_t* out = codes + r * pb;
+    memset(out, 0, (size_t)pb);
+    if (mx == mn) {
+      scales[r] = 1.0f;
+      continue;
+    }
+    int64_t Dq = (int64_t)ldexp(mx - mn, 24);  /* exact: fp16 values are multiples of 2^-24 */
+    for (int64_t j = 0; j < cols; ++j) {
+      int64_t Xq = (int64_t)ldexp(oracle_f16_to_f64(xr[j]) - mn, 24);
+      int64_t c = rhe_div(15 * Xq, Dq);
+      if (c > 15) c = 15;  /* clamp to [0, 2^b - 1] (R17); never binds */
+      out[j / 2] |= (uint8_t)((c & 0xF) << (4 * (j & 1)));
+    }
+    scales[r] = (float)((mx - mn) / 15.0);
+  }
+  return 0;
+}
+
 /* ------------------------------------------------------------------ O-2 pack */
 
 int oracle_pack_int4(const int8_t* q, int64_t rows, int64_t cols, uint8_t* packed, int64_t* bad) {
@@ -337,6 +374,44 @@ int oracle_f16_linear(const uint16_t* a, const uint16_t* w, int64_t M, int64_t N
                            out_f16, 7, out_codes, NULL, out_scales, threads);
   free(dacc);
   return rc;
+}
+
+/* O-16: W4A4 linear with asymmetric activations: the dequantized activation is
+ * scale * qa + zero, so  t = sw[n] (sa[m] sum_k qa qw + za[m] sum_k qw[n,k]) + b[n]  (fp64),
+ * qa unsigned [0, 15], qw signed (symmetric per output channel); F16 and I32 (acc = sum qa qw)
+ * epilogues. */
+int oracle_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales, const float* a_zeros,
+                            const uint8_t* w_codes, const float* w_scales, int64_t M, int64_t N, int64_t K,
+                            int epi_kind, const uint16_t* bias, int32_t* out_i32, uint16_t* out_f16,
+                            int threads) {
+  if (M < 0 || N <= 0 || K <= 0) return -1;
+  if (epi_kind != ORACLE_EPI_I32 && epi_kind != ORACLE_EPI_F16) return -1;
+  if ((epi_kind == ORACLE_EPI_I32 && !out_i32) || (epi_kind == ORACLE_EPI_F16 && !out_f16)) return -1;
+  int64_t pb = (K + 1) / 2;
+  uint8_t* qa = (uint8_t*)malloc((size_t)(M * K > 0 ? M * K : 1));
+  int8_t* qw = (int8_t*)malloc((size_t)(N * K));
+  for (int64_t m = 0; m < M; ++m)
+    for (int64_t k = 0; k < K; ++k) qa[m * K + k] = (uint8_t)((a_codes[m * pb + k / 2] >> (4 * (k & 1))) & 0xF);
+  oracle_unpack_int4(w_codes, N, K, qw);
+#pragma omp parallel for schedule(static) OMP_THREADS(threads)
+  for (int64_t m = 0; m < M; ++m)
+    for (int64_t n = 0; n < N; ++n) {
+      int64_t acc = 0, cs = 0;
+      for (int64_t k = 0; k < K; ++k) {
+        acc += (int64_t)qa[m * K + k] * (int64_t)qw[n * K + k];
+        cs += qw[n * K + k];
+      }
+      if (epi_kind == ORACLE_EPI_I32) {
+        out_i32[m * N + n] = (int32_t)acc;
+      } else {
+        double t = (double)w_scales[n] * ((double)a_scales[m] * (double)acc + (double)a_zeros[m] * (double)cs) +
+                   (bias ? oracle_f16_to_f64(bias[n]) : 0.0);
+        out_f16[m * N + n] = oracle_f64_to_f16(t);
+      }
+    }
+  free(qa);
+  free(qw);
+  return 0;
 }
 
 /* ------------------------------------------------------------------ O-8 attention */

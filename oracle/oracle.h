@@ -143,6 +143,19 @@ int oracle_f16_linear(const uint16_t* a, const uint16_t* w, int64_t M, int64_t N
                       const uint16_t* beta, double ln_eps, float clip, uint16_t* out_f16,
                       uint8_t* out_codes, float* out_scales, int threads);
 
+/* O-15 / O-16  Asymmetric activation quantization (the
+ * paper's "asym" rows, "slower because of the bias term" PAPER.md:499).  O-15: per row
+ * x_zero = min, q = rhe(15 (x - min) / (max - min)) in [0, 15] (unsigned nibbles), scale =
+ * fl32(fl64(max - min) / 15), constant row -> scale 1, codes 0 (reading R18).  O-16: the
+ * linear on those codes x symmetric INT4 weights, F16 / I32 epilogues:
+ * t = sw (sa acc + za colsum(qw)) + b. */
+int oracle_quantize_rows_asym(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x,
+                              uint8_t* codes, float* scales, float* zeros, int threads);
+int oracle_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales, const float* a_zeros,
+                            const uint8_t* w_codes, const float* w_scales, int64_t M, int64_t N, int64_t K,
+                            int epi_kind, const uint16_t* bias, int32_t* out_i32, uint16_t* out_f16,
+                            int threads);
+
 #ifdef __cplusplus
 }
 #endif
