@@ -177,6 +177,27 @@ Q4_API q4_status q4_f16_linear(const uint16_t* a, const uint16_t* w, int64_t M, 
                                const q4_epilogue* epi, void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------
+ * Asymmetric activation quantization (the paper's
+ * "asym" rows -- "slower ... because of less required computation for bias term" for sym,
+ * PAPER.md:499).  Oracle O-15 / O-16, readings R17 / R18.
+ * q4_quantize_rows_asym: per row zero = min(x), q = rhe(15 (x - min) / (max - min)) in
+ *   [0, 15] (exact rational; unsigned nibbles, low = even index), scale = fl32(fl64(max -
+ *   min) / 15); constant row -> scale 1, codes 0, zero = the constant.  cols % 8 == 0,
+ *   cols <= 4096.
+ * q4_weight_code_sums: sums[n] = sum_k qw[n, k] of packed INT4 weights (offline, as float).
+ * q4_w4a4_asym_linear: unsigned activation codes x signed weight codes on tcgen05 (u8 x s8),
+ *   t = w_scales[n] (a_scales[m] acc + a_zeros[m] w_sums[n]) + bias[n]; epilogues F16 and
+ *   I32 (acc = sum qa qw); epi->w_i8 (prepacked weights) honoured.  No workspace. */
+Q4_API q4_status q4_quantize_rows_asym(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x,
+                                       uint8_t* codes, float* scales, float* zeros, void* stream);
+Q4_API q4_status q4_weight_code_sums(const uint8_t* w_codes, int64_t N, int64_t K, float* sums,
+                                     void* stream);
+Q4_API q4_status q4_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales,
+                                     const float* a_zeros, const uint8_t* w_codes,
+                                     const float* w_scales, const float* w_sums, int64_t M, int64_t N,
+                                     int64_t K, const q4_epilogue* epi, void* stream);
+
+/* ---------------------------------------------------------------------------------
  * a2' Offline weight prepack (once per weight, not on the forward path): packed INT4 codes
  * w_codes [N, K/2] -> w_i8 [N, K] int8 holding 16*q in the K order of the on-chip
  * activation unpack (per 32-element group: the 16 even-k values, then the 16 odd-k).

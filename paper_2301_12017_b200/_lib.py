@@ -23,6 +23,7 @@ EXPORTS = (
     "q4_encoder_stack", "q4_quantize_rows_i8", "q4_w8a8_linear_workspace", "q4_w8a8_linear",
     "q4_attention_f16_q8", "q4_encoder_layer_w8a8_workspace", "q4_encoder_layer_w8a8",
     "q4_encoder_stack_w8a8_workspace", "q4_encoder_stack_w8a8", "q4_f16_linear_workspace", "q4_f16_linear",
+    "q4_quantize_rows_asym", "q4_weight_code_sums", "q4_w4a4_asym_linear",
 )
 
 
@@ -98,6 +99,9 @@ def lib():
         L.q4_f16_linear_workspace.argtypes = [I64, I64, I64, I32]
         L.q4_f16_linear_workspace.restype = SZ
         L.q4_f16_linear.argtypes = [P, P, I64, I64, I64, C.POINTER(Epilogue), P, SZ, P]
+        L.q4_quantize_rows_asym.argtypes = [P, I64, I64, I64, P, P, P, P]
+        L.q4_weight_code_sums.argtypes = [P, I64, I64, P, P]
+        L.q4_w4a4_asym_linear.argtypes = [P, P, P, P, P, P, I64, I64, I64, C.POINTER(Epilogue), P]
         L.q4_encoder_layer_w8a8_workspace.argtypes = [C.POINTER(LayerCfg), I64, I64]
         L.q4_encoder_layer_w8a8_workspace.restype = SZ
         L.q4_encoder_layer_w8a8.argtypes = L.q4_encoder_layer.argtypes

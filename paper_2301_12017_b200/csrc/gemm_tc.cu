@@ -39,6 +39,8 @@ struct TcParams {
   int groups;   // row epilogues: gridDim.x / ntn
   const float* a_scales;
   const float* w_scales;
+  const float* a_zeros;  // asymmetric activations (NEXT-3): per-row zero point (min), else nullptr
+  const float* w_sums;   // with a_zeros: per-output-channel sum of the weight codes (float, exact)
   const __half* bias;
   const __half* residual;
   const __half* gamma;
@@ -285,6 +287,26 @@ Q4_DEV void dequant32(const uint32_t (&v)[32], float2 sa2, const float* sw, cons
   }
 }
 
+// Asymmetric activations (NEXT-3, oracle O-16): t = sw (sa acc + za colsum(qw)) + b.
+Q4_DEV void dequant32_asym(const uint32_t (&v)[32], float2 sa2, float2 za2, const float* sw, const float* cs,
+                           const float* bs, uint32_t (&h)[16]) {
+  const float4* pw = reinterpret_cast<const float4*>(sw);
+  const float4* pc = reinterpret_cast<const float4*>(cs);
+  const float4* pb = reinterpret_cast<const float4*>(bs);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 w = pw[j], c = pc[j], bb = pb[j];
+    const float2 u0 = ffma2(make_float2((float)(int)v[4 * j], (float)(int)v[4 * j + 1]), sa2,
+                            fmul2(za2, make_float2(c.x, c.y)));
+    const float2 u1 = ffma2(make_float2((float)(int)v[4 * j + 2], (float)(int)v[4 * j + 3]), sa2,
+                            fmul2(za2, make_float2(c.z, c.w)));
+    const float2 t0 = ffma2(u0, make_float2(w.x, w.y), make_float2(bb.x, bb.y));
+    const float2 t1 = ffma2(u1, make_float2(w.z, w.w), make_float2(bb.z, bb.w));
+    h[2 * j] = pack_half2(t0.x, t0.y);
+    h[2 * j + 1] = pack_half2(t1.x, t1.y);
+  }
+}
+
 // ------------------------------------------------------------------ epilogue pieces
 // Per-warp staging slab: 32 rows x 128 bytes, 16-byte chunks XOR-swizzled by row.
 Q4_DEV uint32_t slab_off(int row, int chunk) { return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4)); }
@@ -461,7 +483,9 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
   } else if (warp == WM) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = H16 ? umma_idesc_f16kk(128, TN) : umma_idesc_i8(128, TN);
+      // asymmetric activations: unsigned A codes (a_format bit 7 = 0: u8 x s8)
+      const uint32_t idesc = H16 ? umma_idesc_f16kk(128, TN)
+                                 : (p.a_zeros ? umma_idesc_i8(128, TN) & ~(1u << 7) : umma_idesc_i8(128, TN));
       uint32_t g = 0, tcount = 0;
       // profiling only (Q4_TRACE): per-tile (wait tempty, wait full_u total, issue span), slot 62
       unsigned long long* mtr = p.trace ? p.trace + ((size_t)blockIdx.x * 64 + 62) * 8 : nullptr;
@@ -575,6 +599,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
       for (int i = ew * 32 + lane; i < TN; i += 2 * GT) {
         prm[i] = p.w_scales ? p.w_scales[c0 + i] : 1.0f;
         prm[TN + i] = p.bias ? __half2float(p.bias[c0 + i]) : 0.f;
+        if (KIND == EPI_F16 && p.a_zeros) prm[2 * TN + i] = p.w_sums[c0 + i];
         if constexpr (KIND == EPI_RESLN_Q4) {
           prm[2 * TN + i] = __half2float(p.gamma[c0 + i]);
           prm[3 * TN + i] = __half2float(p.beta[c0 + i]);
@@ -607,6 +632,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
       // W4A4: the unpacked operands are 16 q, so the accumulator is 256 x the code sum
       const float sa = row_ok ? (H16 ? 1.0f : p.a_scales[gm] * (A8 ? 1.0f : 1.0f / 256.0f)) : 0.f;
       const float2 sa2 = f2(sa);
+      const float2 za2 = f2(row_ok && p.a_zeros ? p.a_zeros[gm] : 0.f);
       const uint4* resp = nullptr;
       uint4 rr[4];  // RESLN: residual of this thread's current chunk (first one loaded before the wait)
       if constexpr (KIND == EPI_RESLN_Q4) {
@@ -648,7 +674,10 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
               tmem_ld32(tbase + 32 * j, v);
               tmem_wait_ld();
               uint32_t h[16];
-              dequant32<H16>(v, sa2, prm + 32 * j, prm + TN + 32 * j, h);
+              if (p.a_zeros)
+                dequant32_asym(v, sa2, za2, prm + 32 * j, prm + 2 * TN + 32 * j, prm + TN + 32 * j, h);
+              else
+                dequant32<H16>(v, sa2, prm + 32 * j, prm + TN + 32 * j, h);
 #pragma unroll
               for (int u = 0; u < 4; ++u)
                 *reinterpret_cast<uint4*>(stg + slab_off(lane, (j & 1) * 4 + u)) =
@@ -942,6 +971,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.ntn = g.N / TN;
   p.mblocks = (g.M + 127) / 128;
   p.a_scales = g.a_scales; p.w_scales = g.w_scales;
+  p.a_zeros = g.a_zeros; p.w_sums = g.w_sums;
   p.bias = g.bias; p.residual = g.residual; p.gamma = g.gamma; p.beta = g.beta;
   p.ln_eps = g.ln_eps; p.clip = g.clip;
   p.out_i32 = g.out_i32; p.out_f16 = g.out_f16; p.out_codes = g.out_codes; p.out_scales = g.out_scales;

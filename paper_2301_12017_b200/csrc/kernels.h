@@ -40,6 +40,8 @@ struct GemmArgs {
   const uint8_t* a_codes;  // [M, K/2]
   const int8_t* a_i8;      // W8A8: int8 activation codes [M, K] (then w_i8 holds int8 weight codes
                            // in natural K order and requant kinds write int8 codes [M, N]); else nullptr
+  const float* a_zeros = nullptr;  // asymmetric activations: per-row zero point; a_codes unsigned nibbles
+  const float* w_sums = nullptr;   // with a_zeros: per-output-channel weight-code sums (as float)
   bool f16_ops = false;    // with a_i8 / w_i8 pointing at fp16 [M, K] / [N, K] and K counted in
                            // bytes (2 x elements): kind::f16 MMA, unit scales, INT4 requant
   const float* a_scales;   // [M]
@@ -61,6 +63,9 @@ struct GemmArgs {
 };
 
 cudaError_t launch_prepack_weights(const uint8_t* w_codes, int64_t N, int64_t K, int8_t* w_i8, cudaStream_t s);
+cudaError_t launch_quantize_rows_asym(const __half* x, int64_t rows, int cols, int64_t ld_x, uint8_t* codes,
+                                      float* scales, float* zeros, cudaStream_t s);
+cudaError_t launch_weight_code_sums(const uint8_t* w_codes, int64_t N, int64_t K, float* sums, cudaStream_t s);
 cudaError_t launch_quantize_rows(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
                                  uint8_t* codes, float* scales, cudaStream_t s);
 cudaError_t launch_quantize_rows_i8(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,

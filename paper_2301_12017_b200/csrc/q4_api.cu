@@ -159,6 +159,70 @@ q4_status q4_w8a8_linear(const int8_t* a_codes, const float* a_scales, const int
   return Q4_OK;
 }
 
+q4_status q4_quantize_rows_asym(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x, uint8_t* codes,
+                                float* scales, float* zeros, void* stream) {
+  g_err[0] = 0;
+  if (rows < 0 || cols <= 0 || ld_x < cols)
+    return fail(Q4_ESHAPE, "q4_quantize_rows_asym: rows=%lld cols=%lld ld_x=%lld", (long long)rows, (long long)cols,
+                (long long)ld_x);
+  if (cols % 8 || ld_x % 8 || cols > 4096)
+    return fail(Q4_ESHAPE, "q4_quantize_rows_asym: cols=%lld / ld_x=%lld (multiples of 8, cols <= 4096)",
+                (long long)cols, (long long)ld_x);
+  if (rows == 0) return Q4_OK;
+  if (!x || !codes || !scales || !zeros) return fail(Q4_EINVAL, "q4_quantize_rows_asym: NULL x/codes/scales/zeros");
+  if (!al16(x) || !al4(codes) || !al4(scales) || !al4(zeros))
+    return fail(Q4_EALIGN, "q4_quantize_rows_asym: x 16-byte aligned, codes/scales/zeros 4-byte aligned");
+  cudaError_t e = q4::launch_quantize_rows_asym(reinterpret_cast<const __half*>(x), rows, (int)cols, ld_x, codes,
+                                                scales, zeros, (cudaStream_t)stream);
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_quantize_rows_asym");
+}
+
+q4_status q4_weight_code_sums(const uint8_t* w_codes, int64_t N, int64_t K, float* sums, void* stream) {
+  g_err[0] = 0;
+  if (N < 0 || K <= 0 || K % 2) return fail(Q4_ESHAPE, "q4_weight_code_sums: N=%lld K=%lld", (long long)N, (long long)K);
+  if (N == 0) return Q4_OK;
+  if (!w_codes || !sums) return fail(Q4_EINVAL, "q4_weight_code_sums: NULL w_codes/sums");
+  cudaError_t e = q4::launch_weight_code_sums(w_codes, N, K, sums, (cudaStream_t)stream);
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_weight_code_sums");
+}
+
+q4_status q4_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales, const float* a_zeros,
+                              const uint8_t* w_codes, const float* w_scales, const float* w_sums, int64_t M, int64_t N,
+                              int64_t K, const q4_epilogue* epi, void* stream) {
+  g_err[0] = 0;
+  if (!epi) return fail(Q4_EINVAL, "q4_w4a4_asym_linear: epi is NULL");
+  if (epi->kind != Q4_EPI_F16 && epi->kind != Q4_EPI_I32)
+    return fail(Q4_EUNSUPPORTED, "q4_w4a4_asym_linear: epilogue kind %d (F16 or I32)", epi->kind);
+  if (epi->mainloop != Q4_MAINLOOP_AUTO && epi->mainloop != Q4_MAINLOOP_TCGEN05 && epi->mainloop != Q4_MAINLOOP_TCGEN05_W8)
+    return fail(Q4_EUNSUPPORTED, "q4_w4a4_asym_linear: mainloop %d (tcgen05 only)", epi->mainloop);
+  if (!a_zeros || (epi->kind == Q4_EPI_F16 && !w_sums))
+    return fail(Q4_EINVAL, "q4_w4a4_asym_linear: NULL a_zeros / w_sums");
+  if (epi->kind == Q4_EPI_F16 && !al16(w_sums)) return fail(Q4_EALIGN, "q4_w4a4_asym_linear: w_sums 16-byte aligned");
+  // the shared validation / dispatch of q4_w4a4_linear with the asymmetric fields set
+  if (M < 0 || N <= 0 || K <= 0 || N % 32 || K % 32 || K > 8192)
+    return fail(Q4_ESHAPE, "q4_w4a4_asym_linear: M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
+  if (M == 0) return Q4_OK;
+  if (!a_codes || !a_scales || !w_codes || !w_scales || !al16(a_codes) || !al16(w_codes) || !al16(w_scales))
+    return fail(Q4_EALIGN, "q4_w4a4_asym_linear: NULL or misaligned operand");
+  if ((epi->kind == Q4_EPI_F16 && (!epi->out_f16 || !al16(epi->out_f16))) ||
+      (epi->kind == Q4_EPI_I32 && (!epi->out_i32 || !al16(epi->out_i32))))
+    return fail(Q4_EINVAL, "q4_w4a4_asym_linear: output NULL or not 16-byte aligned");
+  q4::GemmArgs g;
+  g.a_codes = a_codes; g.a_i8 = nullptr; g.a_scales = a_scales; g.w_codes = w_codes; g.w_scales = w_scales;
+  g.a_zeros = a_zeros; g.w_sums = w_sums;
+  g.M = (int)M; g.N = (int)N; g.K = (int)K; g.kind = epi->kind; g.mainloop = epi->mainloop;
+  g.bias = reinterpret_cast<const __half*>(epi->bias);
+  g.residual = nullptr; g.gamma = nullptr; g.beta = nullptr; g.ln_eps = 0.f; g.clip = 0.f;
+  g.out_i32 = epi->out_i32; g.out_f16 = reinterpret_cast<__half*>(epi->out_f16); g.out_codes = nullptr;
+  g.out_scales = nullptr;
+  g.w_i8 = (epi->mainloop != Q4_MAINLOOP_TCGEN05 && epi->w_i8) ? epi->w_i8 : nullptr;
+  const char* why = "";
+  cudaError_t e = q4::launch_w4a4_tc(g, nullptr, 0, (cudaStream_t)stream, &why);
+  if (e == cudaErrorNotSupported) return fail(Q4_EUNSUPPORTED, "q4_w4a4_asym_linear: %s", why);
+  if (e != cudaSuccess) return fail(Q4_ECUDA, "q4_w4a4_asym_linear: %s %s", cudaGetErrorString(e), why);
+  return Q4_OK;
+}
+
 size_t q4_f16_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind) {
   return q4_w4a4_linear_workspace(M, N, K, kind);
 }

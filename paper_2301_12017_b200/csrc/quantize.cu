@@ -121,6 +121,118 @@ cudaError_t launch_prepack_weights(const uint8_t* w_codes, int64_t N, int64_t K,
   return cudaGetLastError();
 }
 
+// Asymmetric per-token INT4 (NEXT-3, oracle O-15, readings R17/R18):
+// zero = min, q = rhe(15 (x - min) / (max - min)) in [0, 15], scale = fl32(fl64(max-min)/15).
+// x - min and max - min of two fp16 values are exact in fp64 (<= 41 significant bits), so
+// p = d * (15/D) in fp64 is within 1e-14 of the rational; near a half-integer the exact
+// fp64 residual 15 d - D h (both products exact) decides.  Warp per row, one HBM read.
+__device__ __forceinline__ uint32_t asym_code(float x, double mn, double D, double r15) {
+  const double d = (double)x - mn;
+  const double p = d * r15;
+  double n = rint(p);
+  if (fabs(p - n) > 0.4999999) {
+    const double h = floor(p) + 0.5;
+    const double e = fma(-D, h, 15.0 * d);
+    n = e > 0.0 ? h + 0.5 : (e < 0.0 ? h - 0.5 : (fmod(h - 0.5, 2.0) == 0.0 ? h - 0.5 : h + 0.5));
+  }
+  return (uint32_t)(int)fmin(n, 15.0);
+}
+
+template <int MAXV>
+__global__ void __launch_bounds__(256) quantize_rows_asym_kernel(const __half* __restrict__ x, int64_t rows, int cols,
+                                                                 int64_t ld_x, uint8_t* __restrict__ codes,
+                                                                 float* __restrict__ scales, float* __restrict__ zeros) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nvec = cols >> 3;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * ld_x);
+  uint4 v[MAXV];
+  float mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int vi = lane + 32 * i;
+    if (vi < nvec) {
+      v[i] = __ldg(xr + vi);
+      const uint32_t* u = reinterpret_cast<const uint32_t*>(&v[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack_half2(u[j]);
+        mn = fminf(mn, fminf(f.x, f.y));
+        mx = fmaxf(mx, fmaxf(f.x, f.y));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  const double D = (double)mx - (double)mn;
+  const double r15 = D > 0.0 ? 15.0 / D : 0.0;
+  uint32_t* cr = reinterpret_cast<uint32_t*>(codes + row * (int64_t)(cols >> 1));
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int vi = lane + 32 * i;
+    if (vi < nvec) {
+      uint32_t w = 0;
+      if (D > 0.0) {
+        const uint32_t* u = reinterpret_cast<const uint32_t*>(&v[i]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = unpack_half2(u[j]);
+          w |= asym_code(f.x, (double)mn, D, r15) << (8 * j);
+          w |= asym_code(f.y, (double)mn, D, r15) << (8 * j + 4);
+        }
+      }
+      cr[vi] = w;
+    }
+  }
+  if (lane == 0) {
+    scales[row] = D > 0.0 ? (float)(D / 15.0) : 1.0f;
+    zeros[row] = mn;
+  }
+}
+
+// Per-output-channel sum of the INT4 weight codes (asymmetric activations' zero-point term).
+__global__ void weight_code_sums_kernel(const uint8_t* __restrict__ w, int64_t N, int64_t kb, float* __restrict__ sums) {
+  const int64_t n = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (n >= N) return;
+  int s = 0;
+  for (int64_t j = lane; j < kb; j += 32) {
+    const uint32_t b = w[n * kb + j];
+    s += ((int)(b << 28) >> 28) + ((int)(b << 24) >> 28);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) sums[n] = (float)s;
+}
+
+cudaError_t launch_quantize_rows_asym(const __half* x, int64_t rows, int cols, int64_t ld_x, uint8_t* codes,
+                                      float* scales, float* zeros, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  const int warps = 8;
+  const dim3 grid((unsigned)((rows + warps - 1) / warps)), block(32 * warps);
+  const int nvec = cols / 8;
+  const bool pdl = rows <= kPdlMaxRows;
+  note_launch();
+  if (nvec <= 32) return launch_pdl(pdl, quantize_rows_asym_kernel<1>, grid, block, 0, s, x, rows, cols, ld_x, codes, scales, zeros);
+  if (nvec <= 64) return launch_pdl(pdl, quantize_rows_asym_kernel<2>, grid, block, 0, s, x, rows, cols, ld_x, codes, scales, zeros);
+  if (nvec <= 128) return launch_pdl(pdl, quantize_rows_asym_kernel<4>, grid, block, 0, s, x, rows, cols, ld_x, codes, scales, zeros);
+  if (nvec <= 512) return launch_pdl(pdl, quantize_rows_asym_kernel<16>, grid, block, 0, s, x, rows, cols, ld_x, codes, scales, zeros);
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_weight_code_sums(const uint8_t* w_codes, int64_t N, int64_t K, float* sums, cudaStream_t s) {
+  if (N == 0) return cudaSuccess;
+  note_launch();
+  weight_code_sums_kernel<<<(unsigned)((N + 7) / 8), 256, 0, s>>>(w_codes, N, K / 2, sums);
+  return cudaGetLastError();
+}
+
 template <bool I8>
 static cudaError_t launch_quantize_impl(const __half* x, int64_t rows, int cols, int64_t ld_x, float clip,
                                         uint8_t* codes, float* scales, cudaStream_t s) {

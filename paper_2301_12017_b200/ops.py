@@ -162,6 +162,46 @@ def f16_linear(a, w, kind=EPI_F16, *, bias=None, residual=None, gamma=None, beta
     return o
 
 
+def quantize_rows_asym(x: torch.Tensor):
+    """NEXT-3: fp16 [rows, cols] -> (unsigned INT4 codes uint8 [rows, cols/2], scales, zeros)."""
+    _need(x, torch.float16, "x", 2)
+    rows, cols = x.shape
+    codes = torch.empty(rows, cols // 2, dtype=torch.uint8, device=x.device)
+    scales = torch.empty(rows, dtype=torch.float32, device=x.device)
+    zeros = torch.empty(rows, dtype=torch.float32, device=x.device)
+    check(lib().q4_quantize_rows_asym(_ptr(x), rows, cols, cols, _ptr(codes), _ptr(scales), _ptr(zeros), _stream()))
+    return codes, scales, zeros
+
+
+def weight_code_sums(w_codes: torch.Tensor) -> torch.Tensor:
+    _need(w_codes, torch.uint8, "w_codes", 2)
+    N, K = w_codes.shape[0], w_codes.shape[1] * 2
+    out = torch.empty(N, dtype=torch.float32, device=w_codes.device)
+    check(lib().q4_weight_code_sums(_ptr(w_codes), N, K, _ptr(out), _stream()))
+    return out
+
+
+def w4a4_asym_linear(a_codes, a_scales, a_zeros, w_codes, w_scales, w_sums, kind=EPI_F16, *, bias=None,
+                     mainloop=0, w_i8=None, out=None):
+    """NEXT-3: asymmetric activations x symmetric INT4 weights, F16 or I32 epilogue."""
+    _need(a_codes, torch.uint8, "a_codes", 2)
+    _need(w_codes, torch.uint8, "w_codes", 2)
+    M, K = a_codes.shape[0], a_codes.shape[1] * 2
+    N = w_codes.shape[0]
+    dev = a_codes.device
+    o = dict(out or {})
+    if kind == EPI_I32:
+        o.setdefault("i32", torch.empty(M, N, dtype=torch.int32, device=dev))
+    else:
+        o.setdefault("f16", torch.empty(M, N, dtype=torch.float16, device=dev))
+    e = Epilogue(kind=kind, mainloop=mainloop, bias=_ptr(bias), residual=None, gamma=None, beta=None, ln_eps=0.0,
+                 requant_clip=0.0, out_i32=_ptr(o.get("i32")), out_f16=_ptr(o.get("f16")), out_codes=None,
+                 out_scales=None, w_i8=_ptr(w_i8))
+    check(lib().q4_w4a4_asym_linear(_ptr(a_codes), _ptr(a_scales), _ptr(a_zeros), _ptr(w_codes), _ptr(w_scales),
+                                    _ptr(w_sums), M, N, K, C.byref(e), _stream()))
+    return o
+
+
 def attention_f16_q4(qkv, B, S, heads, head_dim=64, f16_tap=False):
     """a7: fp16 QKV [B*S, 3h] -> (ctx codes [B*S, h/2], ctx scales [B*S][, ctx fp16])."""
     _need(qkv, torch.float16, "qkv", 2)
