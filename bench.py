@@ -489,6 +489,24 @@ def side_measurements(q4, synth, torch, np, dev, args):
         tops = 2.0 * M * Nn * K / (e0.elapsed_time(e1) / 10 * 1e-3) / 1e12
         out[f"gemm_f16_M{M}_N{Nn}_K{K}_w8a8_tcgen05_TOPS"] = tops
         out[f"gemm_f16_M{M}_N{Nn}_K{K}_w8a8_tcgen05_frac_int8_peak"] = tops / pk["int8_tops"]
+        # symmetric vs asymmetric activations (NEXT-3), prepacked weights, F16 epilogue
+        w8p = q4.prepack_weights(w)
+        xa = torch.from_numpy(synth.hidden(M, K, f"sw_asym{K}") + np.float16(0.5)).to(dev)
+        ac, asc, az = q4.quantize_rows_asym(xa)
+        wsum = q4.weight_code_sums(w)
+        for nm, fn in (("w8_sym", lambda o: q4.w4a4_linear(a, sa, w, sw, q4.EPI_F16, w_i8=w8p, out=o)),
+                       ("w8_asym", lambda o: q4.w4a4_asym_linear(ac, asc, az, w, sw, wsum, q4.EPI_F16, w_i8=w8p,
+                                                                  out=o))):
+            o = fn(None)
+            for _ in range(3):
+                fn(o)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(10):
+                fn(o)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            out[f"gemm_f16_M{M}_N{Nn}_K{K}_tcgen05_{nm}_TOPS"] = 2.0 * M * Nn * K / (e0.elapsed_time(e1) / 10 * 1e-3) / 1e12
         for ml, mname in ((1, "tcgen05"), (2, "mma_sync_s8"), (3, "mma_sync_s4")):
             o = q4.w4a4_linear(a, sa, w, sw, q4.EPI_F16, mainloop=ml)
             for _ in range(3):
