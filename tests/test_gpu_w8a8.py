@@ -291,3 +291,37 @@ def test_encoder_stack_strategy_graph(q4):
     enc.capture(xd, o2, B, S)
     enc.replay()
     assert torch.equal(o2, o1)
+
+
+def test_w8a8_full_size_layer_sampled(q4):
+    """The W8A8 baseline at the bench's launch configuration (BERT-large, M = 32768): sampled
+    sequences checked teacher-forced against the W8A8 oracle (independent sub-problems)."""
+    cfg = synth.BERT["large"]
+    B, S = 256, 128
+    M, h, f = B * S, cfg["hidden"], cfg["ffn"]
+    p = synth.layer_params(cfg, 0, "full8")
+    x = synth.hidden(M, h, "full8_x")
+    w = q4.quantize_layer(p, bits=8)
+    xq, xs = q4.quantize_rows_i8(dev(x))
+    out = q4.encoder_layer(cfg, w, B, S, dev(x), xq, xs, taps=True, bits=8)
+    torch.cuda.synchronize()
+    W = {k: host(v) for k, v in w.items()}
+    for bsel in (0, 201, 255):
+        rows = slice(bsel * S, (bsel + 1) * S)
+        T = {k: host(v[rows]) for k, v in out.items()}
+        xq_, xs_ = host(xq[rows]), host(xs[rows])
+        assert np.array_equal(T["acc_qkv"], orc.gemm_i32_i8(xq_, W["wqkv"], S, 3 * h, h))
+        rctx, _, _ = orc.attention(T["qkv"], 1, S, cfg["heads"], 64)
+        assert_f16_close(T["ctx"], rctx, "ctx")
+        c2, s2 = orc.quantize_rows_i8(T["ctx"])
+        assert np.array_equal(T["ctx_codes"], c2) and np.array_equal(T["ctx_scales"], s2)
+        assert np.array_equal(T["acc_o"], orc.gemm_i32_i8(T["ctx_codes"], W["wo"], S, h, h))
+        assert np.array_equal(T["acc_1"], orc.gemm_i32_i8(T["h1_codes"], W["w1"], S, f, h))
+        r2 = orc.w8a8_linear(T["h1_codes"], T["h1_scales"], W["w1"], W["s1"], S, f, h, orc.EPI_GELU_Q4, bias=p["b1"])
+        assert_f16_close(T["ffn1"], r2["f16"], "ffn1")
+        assert np.array_equal(T["acc_2"], orc.gemm_i32_i8(T["f_codes"], W["w2"], S, h, f))
+        r3 = orc.w8a8_linear(T["f_codes"], T["f_scales"], W["w2"], W["s2"], S, h, f, orc.EPI_RESLN_Q4,
+                             bias=p["b2"], residual=T["h1"], gamma=p["ln2_g"], beta=p["ln2_b"])
+        assert_f16_close(T["h_out"], r3["f16"], "h_out")
+        c2, s2 = orc.quantize_rows_i8(T["h_out"])
+        assert np.array_equal(T["hq_out"], c2) and np.array_equal(T["hs_out"], s2)
