@@ -279,6 +279,20 @@ Q4_API q4_status q4_encoder_stack(const q4_layer_cfg* cfg, const q4_layer_weight
                            void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------
+ * Pipelined serving over host buffers (the end-to-end path): nbatch batches, each B x S
+ * tokens, h_in[i] / h_out[i] host pointers (pinned for overlap) of [B*S, hidden] fp16.
+ * Batch i's upload (copy-in stream), forward (the caller's stream, = q4_encoder_stack) and
+ * download (copy-out stream) overlap the neighbouring batches through two device input and
+ * two device output buffers inside `workspace` (q4_encoder_pipeline_workspace).  The
+ * caller's stream completes after the last download.  Streams/events are created on the
+ * first call per device and reused; not CUDA-graph capturable. */
+Q4_API size_t q4_encoder_pipeline_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S);
+Q4_API q4_status q4_encoder_pipeline(const q4_layer_cfg* cfg, const q4_layer_weights* layers, int32_t L,
+                                     int64_t B, int64_t S, const uint16_t* const* h_in,
+                                     uint16_t* const* h_out, int32_t nbatch, void* workspace,
+                                     size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
  * W8A8 baseline of a7 / a8 (the paper's end-to-end INT8 comparison,
  * "i8-qall", Fig. e2e_i4_i8): the same layer and stack with 8-bit
  * codes throughout -- q4_quantize_rows_i8 for the layer-0 input, q4_w8a8_linear for the

@@ -24,6 +24,7 @@ EXPORTS = (
     "q4_attention_f16_q8", "q4_encoder_layer_w8a8_workspace", "q4_encoder_layer_w8a8",
     "q4_encoder_stack_w8a8_workspace", "q4_encoder_stack_w8a8", "q4_f16_linear_workspace", "q4_f16_linear",
     "q4_quantize_rows_asym", "q4_weight_code_sums", "q4_w4a4_asym_linear",
+    "q4_encoder_pipeline_workspace", "q4_encoder_pipeline",
 )
 
 
@@ -100,6 +101,10 @@ def lib():
         L.q4_f16_linear_workspace.restype = SZ
         L.q4_f16_linear.argtypes = [P, P, I64, I64, I64, C.POINTER(Epilogue), P, SZ, P]
         L.q4_quantize_rows_asym.argtypes = [P, I64, I64, I64, P, P, P, P]
+        L.q4_encoder_pipeline_workspace.argtypes = [C.POINTER(LayerCfg), I64, I64]
+        L.q4_encoder_pipeline_workspace.restype = SZ
+        L.q4_encoder_pipeline.argtypes = [C.POINTER(LayerCfg), C.POINTER(LayerWeights), I32, I64, I64, P, P, I32,
+                                          P, SZ, P]
         L.q4_weight_code_sums.argtypes = [P, I64, I64, P, P]
         L.q4_w4a4_asym_linear.argtypes = [P, P, P, P, P, P, I64, I64, I64, C.POINTER(Epilogue), P]
         L.q4_encoder_layer_w8a8_workspace.argtypes = [C.POINTER(LayerCfg), I64, I64]
@@ -113,7 +118,8 @@ def lib():
                 "q4_last_error", "q4_version", "q4_launch_count", "q4_w4a4_linear_workspace",
                 "q4_encoder_layer_workspace", "q4_encoder_stack_workspace",
                 "q4_w8a8_linear_workspace", "q4_encoder_layer_w8a8_workspace",
-                "q4_encoder_stack_w8a8_workspace", "q4_f16_linear_workspace") else C.c_int
+                "q4_encoder_stack_w8a8_workspace", "q4_f16_linear_workspace",
+                "q4_encoder_pipeline_workspace") else C.c_int
         _lib = L
     return _lib
 

@@ -718,4 +718,84 @@ q4_status q4_encoder_stack_w8a8(const q4_layer_cfg* cfg, const q4_layer_weights*
   return encoder_stack_impl(cfg, layers, L, B, S, h_in, h_out, workspace, ws_bytes, stream, true);
 }
 
+// ------------------------------------------------------------------ pipelined host-buffer serving
+// nbatch batches of host (pinned) inputs -> host outputs.  Batch i's H2D copy runs on a copy-in
+// stream, its forward on the caller's stream, its D2H copy on a copy-out stream; two device
+// input and two device output buffers (slot = i % 2) let batch i+1's upload and batch i-1's
+// download overlap batch i's forward.  Streams and events are created once per device and
+// reused (the call itself allocates nothing on the device).
+size_t q4_encoder_pipeline_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S) {
+  if (!cfg) return 0;
+  const size_t hb = align_up((size_t)(B * S) * cfg->hidden * 2);
+  return stack_ws(cfg, B * S, nullptr).bytes + 4 * hb;
+}
+
+q4_status q4_encoder_pipeline(const q4_layer_cfg* cfg, const q4_layer_weights* layers, int32_t L, int64_t B, int64_t S,
+                              const uint16_t* const* h_in, uint16_t* const* h_out, int32_t nbatch, void* workspace,
+                              size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  q4_status st = check_cfg(cfg, "q4_encoder_pipeline");
+  if (st) return st;
+  if (nbatch < 0 || (nbatch > 0 && (!h_in || !h_out))) return fail(Q4_EINVAL, "q4_encoder_pipeline: nbatch=%d h_in/h_out", nbatch);
+  const size_t need = q4_encoder_pipeline_workspace(cfg, B, S);
+  if (!workspace || ws_bytes < need)
+    return fail(Q4_EINVAL, "q4_encoder_pipeline: workspace %zu bytes < required %zu", ws_bytes, need);
+  if (nbatch == 0 || B * S == 0) return Q4_OK;
+  const size_t stack_bytes = stack_ws(cfg, B * S, nullptr).bytes;
+  const size_t hbytes = (size_t)(B * S) * cfg->hidden * 2, hb = align_up(hbytes);
+  uint8_t* base = (uint8_t*)workspace;
+  uint16_t* din[2] = {(uint16_t*)(base + stack_bytes), (uint16_t*)(base + stack_bytes + hb)};
+  uint16_t* dout[2] = {(uint16_t*)(base + stack_bytes + 2 * hb), (uint16_t*)(base + stack_bytes + 3 * hb)};
+  struct Aux {
+    cudaStream_t cin = nullptr, cout = nullptr;
+    cudaEvent_t in_ready[2], in_free[2], done[2], out_free[2];
+  };
+  static Aux aux[64];
+  static std::atomic<bool> made[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(Q4_EUNSUPPORTED, "q4_encoder_pipeline: device %d", dev);
+  Aux& a = aux[dev];
+  if (!made[dev].load()) {
+    cudaError_t e = cudaStreamCreateWithFlags(&a.cin, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a.cout, cudaStreamNonBlocking);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+      e = cudaEventCreateWithFlags(&a.in_ready[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.in_free[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.done[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.out_free[k], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "q4_encoder_pipeline: stream/event creation");
+    made[dev].store(true);
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  // the auxiliary streams start after everything already queued on the caller's stream
+  cudaEvent_t start = a.done[0];
+  if ((e = cudaEventRecord(start, s)) != cudaSuccess) return cuda_fail(e, "q4_encoder_pipeline");
+  cudaStreamWaitEvent(a.cin, start, 0);
+  cudaStreamWaitEvent(a.cout, start, 0);
+  for (int32_t i = 0; i < nbatch; ++i) {
+    const int k = i & 1;
+    if (i >= 2) cudaStreamWaitEvent(a.cin, a.in_free[k], 0);  // batch i-2 has consumed din[k]
+    if ((e = cudaMemcpyAsync(din[k], h_in[i], hbytes, cudaMemcpyHostToDevice, a.cin)) != cudaSuccess)
+      return cuda_fail(e, "q4_encoder_pipeline: H2D");
+    cudaEventRecord(a.in_ready[k], a.cin);
+    cudaStreamWaitEvent(s, a.in_ready[k], 0);
+    if (i >= 2) cudaStreamWaitEvent(s, a.out_free[k], 0);  // batch i-2's download has read dout[k]
+    if ((st = encoder_stack_impl(cfg, layers, L, B, S, din[k], dout[k], workspace, stack_bytes, stream, false)))
+      return st;
+    cudaEventRecord(a.in_free[k], s);
+    cudaEventRecord(a.done[k], s);
+    cudaStreamWaitEvent(a.cout, a.done[k], 0);
+    if ((e = cudaMemcpyAsync(h_out[i], dout[k], hbytes, cudaMemcpyDeviceToHost, a.cout)) != cudaSuccess)
+      return cuda_fail(e, "q4_encoder_pipeline: D2H");
+    cudaEventRecord(a.out_free[k], a.cout);
+  }
+  // the caller's stream completes after the last download
+  cudaStreamWaitEvent(s, a.out_free[(nbatch - 1) & 1], 0);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_encoder_pipeline");
+}
+
 }  // extern "C"

@@ -50,6 +50,24 @@ class W4A4Encoder:
                                      C.c_void_p(torch.cuda.current_stream().cuda_stream)))
         return h_out
 
+    def serve(self, h_in: list, h_out: list, B: int, S: int):
+        """Pipelined end-to-end serving (q4_encoder_pipeline, W4A4 only): lists of host fp16
+        [B*S, hidden] tensors (pinned for overlap); batch i's upload and batch i-1's download
+        overlap batch i's forward.  Stream-ordered on the current stream."""
+        if self.bits != 4:
+            raise ValueError("serve(): the pipelined entry runs the W4A4 stack")
+        if len(h_in) != len(h_out):
+            raise ValueError("serve(): h_in and h_out lengths differ")
+        n = lib().q4_encoder_pipeline_workspace(C.byref(self._lc), B, S)
+        if getattr(self, "_pws", None) is None or self._pws.numel() < n:
+            self._pws = torch.zeros(max(n, 1), dtype=torch.uint8, device=self.device)
+        pin = (C.c_void_p * len(h_in))(*[t.data_ptr() for t in h_in])
+        pout = (C.c_void_p * len(h_out))(*[t.data_ptr() for t in h_out])
+        check(lib().q4_encoder_pipeline(C.byref(self._lc), self._lw, self.L, B, S, pin, pout, len(h_in),
+                                        C.c_void_p(self._pws.data_ptr()), self._pws.numel(),
+                                        C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return h_out
+
     def capture(self, h_in: torch.Tensor, h_out: torch.Tensor, B: int, S: int, warmup: int = 1):
         """Capture forward(h_in -> h_out) (device buffers) into a CUDA graph."""
         self.workspace(B, S)

@@ -381,3 +381,24 @@ def test_prepack_weights_layout(q4):
     q = orc.unpack_int4(w, K).astype(np.int64).reshape(N, K // 32, 32)
     ref = np.concatenate([q[:, :, 0::2], q[:, :, 1::2]], axis=2).reshape(N, K) * 16
     assert np.array_equal(got, ref)
+
+
+def test_encoder_pipeline_serving(q4):
+    """q4_encoder_pipeline over host buffers == per-batch device forward, for 1..5 batches
+    (slot reuse, first/last-batch edges)."""
+    cfg = synth.BERT["base"]
+    B, S, L = 2, 128, 2
+    enc = q4.W4A4Encoder(cfg, [synth.layer_params(cfg, l, "pipe") for l in range(L)])
+    xs = [synth.hidden(B * S, cfg["hidden"], "pipe_x", i) for i in range(5)]
+    refs = []
+    for x in xs:
+        o = torch.empty(B * S, cfg["hidden"], dtype=torch.float16, device="cuda")
+        enc.forward(dev(x), o, B, S)
+        refs.append(host(o))
+    for n in (1, 2, 5):
+        ins = [torch.from_numpy(x).pin_memory() for x in xs[:n]]
+        outs = [torch.empty(B * S, cfg["hidden"], dtype=torch.float16).pin_memory() for _ in range(n)]
+        enc.serve(ins, outs, B, S)
+        torch.cuda.synchronize()
+        for i in range(n):
+            assert np.array_equal(outs[i].numpy(), refs[i]), (n, i)
