@@ -865,22 +865,17 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
           if (row_ok && nb == 0 && sub == 0) p.out_scales[gm] = amax > 0.f ? __fdiv_rn(amax, 127.0f) : 1.0f;
         } else {
         const float r7 = amax > 0.f ? __fdiv_rn(7.0f, amax) : 0.f;
-        for (int k = 0; k < NSL; ++k) {
-#pragma unroll
-          for (int jj = 0; jj < 2; jj += NS) {
-            const int j = 2 * k + jj + sub;
-            uint32_t h[16];
-            tmem_ld16(tbase + 32 * j, h);
-            tmem_wait_ld();
-            const uint4 wq = requant32(h, amax, r7, clip);
-            // 32 codes = 16 bytes: chunk (j & 1) of the slab row (a 64-column slab row = 32 code bytes)
-            *reinterpret_cast<uint4*>(stg + slab_off(lane, j & 1)) = wq;
-          }
-          slab_sync();
-          slab_store16(stg, p.out_codes, m0 + q * 32, RS * sub, RS, p.M, (size_t)N / 2, (size_t)(c0 + 64 * k) / 2, 32,
-                       lane);
-          slab_sync();
+        // the whole tile row's codes (TN / 2 <= 128 bytes) fit one slab row: chunk j -> slab
+        // chunk j, then one synchronised store of full row segments
+        for (int j = sub; j < NCH; j += NS) {
+          uint32_t h[16];
+          tmem_ld16(tbase + 32 * j, h);
+          tmem_wait_ld();
+          *reinterpret_cast<uint4*>(stg + slab_off(lane, j)) = requant32(h, amax, r7, clip);
         }
+        slab_sync();
+        slab_store16(stg, p.out_codes, m0 + q * 32, RS * sub, RS, p.M, (size_t)N / 2, (size_t)c0 / 2, TN / 2, lane);
+        slab_sync();
         if (row_ok && nb == 0 && sub == 0) p.out_scales[gm] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
         }
       }
