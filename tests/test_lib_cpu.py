@@ -71,3 +71,27 @@ def test_validation_errors_are_synchronous(L):
     # M = 0 is a no-op that succeeds without touching the device
     e = Epilogue(kind=1)
     assert L.q4_w4a4_linear(p, p, p, p, 0, 64, 64, C.byref(e), None, 0, None) == 0
+
+
+def test_strategy_names_follow_the_paper():
+    """fp16_parts bit i = part q(i+1) runs in FP16 (q4_layer_cfg); names list the quantized
+    parts as in PAPER.md:503-504 ("q3" = only the MLP intermediate quantized)."""
+    from paper_2301_12017_b200.tune import strategy_name
+    assert strategy_name(0) == "qall"
+    assert strategy_name(0xF) == "fp16"
+    assert strategy_name(0xB) == "q3"
+    assert strategy_name(0x5) == "q2q4"
+    assert len({strategy_name(m) for m in range(16)}) == 16
+
+
+def test_layer_structs_match_the_header():
+    """The ctypes mirrors of q4_layer_cfg / q4_layer_weights / q4_epilogue carry every field
+    the header declares, in order."""
+    import re
+    from paper_2301_12017_b200 import _lib
+    src = open(os.path.join(ROOT, "include", "q4.h")).read()
+    body = re.search(r"typedef struct \{(.*?)\} q4_layer_weights;", src, re.S).group(1)
+    names = re.findall(r"\*(\w+)", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
+    assert tuple(names) == _lib.WEIGHT_FIELDS
+    cfg = re.search(r"typedef struct \{(.*?)\} q4_layer_cfg;", src, re.S).group(1)
+    assert "fp16_parts" in cfg and [n for n, _ in _lib.LayerCfg._fields_][-1] == "fp16_parts"
