@@ -53,6 +53,7 @@ struct TcParams {
   float2* xstat;      // [mblocks][ntn][128] (mean, M2) partials
   float* xamax;       // [mblocks][ntn][128] max-abs partials
   unsigned* xcnt;     // [4][mblocks] arrival / departure counters (self-resetting; zero on entry)
+  int pair;           // CTA-pair (cta_group::2) mainloop: cluster of 2, CTA r owns m-block 2 c + r
   int dbg;            // profiling only (env Q4_DEBUG_SKIP): 1 skip TMA, 2 skip unpack, 4 skip MMA, 8 skip epilogue math
   unsigned long long* trace;  // profiling only (env Q4_TRACE): [grid][64 tiles][8] %globaltimer stamps
 };
@@ -81,12 +82,15 @@ template <int KIND> struct EpiCfg {
 // activation operand A is unpacked on chip.
 // A8 (W8A8 baseline, with BI8): A arrives as int8 codes too and is TMA'd straight into the
 // operand stage like B -- no packed ring, no on-chip unpack.
-template <int TN, bool BI8, bool A8 = false>
+// PAIR (with BI8): CTA-pair mainloop -- tcgen05.mma.cta_group::2 with M = 256; each CTA
+// stages its own 128 rows of A and half of the N tile of B, so the B stage halves and the
+// unpacked ring deepens to 4 stages.
+template <int TN, bool BI8, bool A8 = false, bool PAIR = false>
 struct TcCfg {
   static constexpr int BM = 128, BK = 128;  // BK in int8 elements = 64 packed bytes
-  static constexpr int SP = A8 ? 1 : BI8 ? 4 : 3, SU = BI8 ? 3 : 2;  // packed / unpacked smem stages
+  static constexpr int SP = A8 ? 1 : BI8 ? 4 : 3, SU = PAIR ? 4 : BI8 ? 3 : 2;  // packed / unpacked smem stages
   static constexpr int A_PK = A8 ? 0 : BM * 64, B_PK = BI8 ? 0 : TN * 64;
-  static constexpr int A_UN = BM * 128, B_UN = TN * 128;
+  static constexpr int A_UN = BM * 128, B_UN = (PAIR ? TN / 2 : TN) * 128;
   static constexpr int UN_STAGE = A_UN + B_UN, PK_STAGE = A_PK + B_PK;
   static constexpr int OFF_UN = 0;
   static constexpr int OFF_PK = SU * UN_STAGE;
@@ -106,15 +110,21 @@ struct TileIter {
   // The grid is `groups` x `ntn` CTAs; CTA (g, rank) owns n-block `rank` for the whole
   // kernel and walks m-blocks g, g + groups, ...  (fixed N-tile: column parameters are
   // staged once; row epilogues find the ntn CTAs of an m-block at the same step).
-  int cur, step, mblocks, rank;
-  __device__ TileIter(const TcParams& p) : mblocks(p.mblocks) {
-    rank = blockIdx.x % p.ntn;
-    cur = blockIdx.x / p.ntn;
+  // CTA pairs: cluster c = blockIdx.x / 2 plays the role of a CTA above over m-block pairs;
+  // CTA r of the pair owns m-block 2 * pair + r (M % 256 == 0).
+  int cur, step, mblocks, rank, sub, pair;
+  __device__ TileIter(const TcParams& p) {
+    pair = p.pair;
+    const int c = pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    sub = pair ? (int)(blockIdx.x & 1) : 0;
+    mblocks = pair ? p.mblocks / 2 : p.mblocks;
+    rank = c % p.ntn;
+    cur = c / p.ntn;
     step = p.groups;
   }
   __device__ bool next(int& mb, int& nb) {
     if (cur >= mblocks) return false;
-    mb = cur;
+    mb = pair ? 2 * cur + sub : cur;
     nb = rank;
     cur += step;
     return true;
@@ -392,12 +402,14 @@ Q4_DEV void slab_load16(uint8_t* stg, const uint8_t* gbase, int row0, int r0, in
 // strategy).  The byte-level staging is the A8 path unchanged (a 128-byte
 // k-block row = 64 fp16), the MMA is kind::f16 with fp32 accumulators, and the epilogue
 // reads the accumulator as fp32 with unit scales.
-template <int TN, int KIND, bool BI8, bool A8, bool H16 = false>
+template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false>
 __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     w4a4_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
   static_assert(!A8 || BI8, "W8A8 takes int8 weights through the BI8 path");
   static_assert(!H16 || A8, "fp16 operands use the A8 staging");
-  using C = TcCfg<TN, BI8, A8>;
+  static_assert(!PAIR || (BI8 && !A8 && KIND != EPI_GELU_Q4), "pair mainloop: prepacked weights, F16/I32/RESLN");
+  // (RESLN instantiations compile but are not dispatched: measured slower)
+  using C = TcCfg<TN, BI8, A8, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full_p = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -421,14 +433,31 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int i = 0; i < C::SP; ++i) { mbar_init(&full_p[i], 1); mbar_init(&empty_p[i], 4); }
-    for (int i = 0; i < C::SU; ++i) { mbar_init(&full_u[i], A8 ? 1 : BI8 ? 5 : 4); mbar_init(&empty_u[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EpiCfg<KIND>::EPW); }
+    // pair: the leader's full_u counts both CTAs' unpack warps (8) + its producer; its tempty
+    // counts both CTAs' epilogue warps
+    for (int i = 0; i < C::SU; ++i) { mbar_init(&full_u[i], A8 ? 1 : PAIR ? 9 : BI8 ? 5 : 4); mbar_init(&empty_u[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], (PAIR ? 2 : 1) * EpiCfg<KIND>::EPW); }
     fence_mbar_init();
   }
-  if (warp == WM) tmem_alloc(tmem_slot, C::TMEM_COLS);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
+  if constexpr (PAIR) {
+    if (warp == WM) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();  // both CTAs' barriers initialised before any remote arrive
+    tc_fence_after();
+  } else {
+    if (warp == WM) tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+  // pair: shared::cluster address of a barrier in the leader CTA (rank 0)
+  auto lead = [&](uint64_t* bar) -> uint32_t { return PAIR ? mapa(smem_u32(bar), 0) : smem_u32(bar); };
   const uint32_t tmem = *tmem_slot;
   TileIter it(p);
   int mb, nb;
@@ -473,8 +502,18 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
             const int su = g % C::SU;
             mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
             uint8_t* ub = smem + C::OFF_UN + su * C::UN_STAGE + C::A_UN;
-            mbar_arrive_expect_tx(&full_u[su], (uint32_t)C::B_UN);
-            tma_load_2d(ub, &tmB, &full_u[su], kb * 128, nb * TN);
+            if constexpr (PAIR) {
+              // this CTA's half of the N tile; completion counted on the leader's barrier
+              if (crank == 0) mbar_arrive_expect_tx(&full_u[su], (uint32_t)(2 * C::B_UN));
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(ub)), "l"(reinterpret_cast<uint64_t>(&tmB)),
+                  "r"(lead(&full_u[su])), "r"(kb * 128), "r"(nb * TN + (int)crank * (TN / 2))
+                  : "memory");
+            } else {
+              mbar_arrive_expect_tx(&full_u[su], (uint32_t)C::B_UN);
+              tma_load_2d(ub, &tmB, &full_u[su], kb * 128, nb * TN);
+            }
           }
         }
       }
@@ -482,17 +521,19 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     __syncwarp();
   } else if (warp == WM) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && (!PAIR || crank == 0)) {  // pair: the leader issues for both CTAs
       // asymmetric activations: unsigned A codes (a_format bit 7 = 0: u8 x s8)
       const uint32_t idesc = H16 ? umma_idesc_f16kk(128, TN)
-                                 : (p.a_zeros ? umma_idesc_i8(128, TN) & ~(1u << 7) : umma_idesc_i8(128, TN));
+                                 : (p.a_zeros ? umma_idesc_i8(PAIR ? 256 : 128, TN) & ~(1u << 7)
+                                              : umma_idesc_i8(PAIR ? 256 : 128, TN));
       uint32_t g = 0, tcount = 0;
       // profiling only (Q4_TRACE): per-tile (wait tempty, wait full_u total, issue span), slot 62
       unsigned long long* mtr = p.trace ? p.trace + ((size_t)blockIdx.x * 64 + 62) * 8 : nullptr;
       while (it.next(mb, nb)) {
         const uint32_t b = tcount & 1u;
         const unsigned long long m0 = mtr ? gtimer() : 0;
-        mbar_wait(&tempty[b], ((tcount >> 1) & 1u) ^ 1u);
+        if constexpr (PAIR) mbar_wait_cluster(&tempty[b], ((tcount >> 1) & 1u) ^ 1u);
+        else mbar_wait(&tempty[b], ((tcount >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const unsigned long long m1 = mtr ? gtimer() : 0;
         unsigned long long mw = 0;
@@ -500,7 +541,8 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
         for (int kb = 0; kb < KB; ++kb, ++g) {
           const int su = g % C::SU;
           const unsigned long long w0 = mtr ? gtimer() : 0;
-          mbar_wait(&full_u[su], (g / C::SU) & 1u);
+          if constexpr (PAIR) mbar_wait_cluster(&full_u[su], (g / C::SU) & 1u);
+          else mbar_wait(&full_u[su], (g / C::SU) & 1u);
           if (mtr) mw += gtimer() - w0;
           tc_fence_after();
           const uint32_t ua = smem_u32(smem + C::OFF_UN + su * C::UN_STAGE);
@@ -508,7 +550,14 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
           if (!(p.dbg & 4)) {
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
-              if constexpr (H16)
+              if constexpr (PAIR)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
+                    "l"(umma_smem_desc(ua + ks * 32, 1024, 2)), "l"(umma_smem_desc(ub + ks * 32, 1024, 2)),
+                    "r"(idesc), "r"((uint32_t)((kb | ks) != 0))
+                    : "memory");
+              else if constexpr (H16)
                 umma_f16kk(dt, umma_smem_desc(ua + ks * 32, 1024, 2), umma_smem_desc(ub + ks * 32, 1024, 2), idesc,
                            (kb | ks) != 0);
               else
@@ -516,9 +565,17 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
                         (kb | ks) != 0);
             }
           }
-          umma_commit(&empty_u[su]);
+          if constexpr (PAIR)
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                         ::"r"(smem_u32(&empty_u[su])), "h"((uint16_t)3) : "memory");
+          else
+            umma_commit(&empty_u[su]);
         }
-        umma_commit(&tfull[b]);
+        if constexpr (PAIR)
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                       ::"r"(smem_u32(&tfull[b])), "h"((uint16_t)3) : "memory");
+        else
+          umma_commit(&tfull[b]);
         if (mtr && tcount >= 2) {
           const unsigned long long m2 = gtimer();
           mtr[0] += m1 - m0; mtr[1] += mw; mtr[2] += m2 - m1; mtr[3] += 1;
@@ -559,7 +616,10 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&full_u[su]);
+          if constexpr (PAIR)
+            asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(lead(&full_u[su])) : "memory");
+          else
+            mbar_arrive(&full_u[su]);
           mbar_arrive(&empty_p[s]);
         }
         if (utr && g >= 16 && g < 16 + 256) {  // (wait_full, wait_empty, unpack, fence+arrive), 256 k-blocks
@@ -595,7 +655,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     const float clip = p.clip;
     float* prm = reinterpret_cast<float*>(smem + C::OFF_PRM);  // sw | bias | gamma | beta of this n-block
     {
-      const int c0 = (blockIdx.x % p.ntn) * TN;
+      const int c0 = it.rank * TN;  // this CTA's fixed n-block (pairs: per cluster)
       for (int i = ew * 32 + lane; i < TN; i += 2 * GT) {
         prm[i] = p.w_scales ? p.w_scales[c0 + i] : 1.0f;
         prm[TN + i] = p.bias ? __half2float(p.bias[c0 + i]) : 0.f;
@@ -883,14 +943,26 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
       // accumulator buffer b may be overwritten by the MMA of tile tcount + 2
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[b]);
+      if (lane == 0) {
+        if constexpr (PAIR)
+          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(lead(&tempty[b])) : "memory");
+        else
+          mbar_arrive(&tempty[b]);
+      }
       ++tcount;
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == WM) tmem_dealloc(tmem, C::TMEM_COLS);
+  if constexpr (PAIR) {
+    cluster_sync();  // the leader's MMAs write this CTA's TMEM and read its smem until the end
+    if (warp == WM)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+  } else {
+    if (warp == WM) tmem_dealloc(tmem, C::TMEM_COLS);
+  }
 }
 
 // ====================================================================== host side
@@ -941,10 +1013,10 @@ int num_sms() {
   return n;
 }
 
-template <int TN, int KIND, bool BI8, bool A8, bool H16 = false>
+template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false>
 cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {
-  using C = TcCfg<TN, BI8, A8>;
-  auto kern = w4a4_tc_kernel<TN, KIND, BI8, A8, H16>;
+  using C = TcCfg<TN, BI8, A8, PAIR>;
+  auto kern = w4a4_tc_kernel<TN, KIND, BI8, A8, H16, PAIR>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -953,7 +1025,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   }
   CUtensorMap ta, tb;
   const uint64_t kb = (uint64_t)g.K / 2;
-  const bool okb = BI8 ? make_tmap(&tb, g.w_i8, (uint64_t)g.N, (uint64_t)g.K, TN, 128, true)
+  const bool okb = BI8 ? make_tmap(&tb, g.w_i8, (uint64_t)g.N, (uint64_t)g.K, PAIR ? TN / 2 : TN, 128, true)
                        : make_tmap(&tb, g.w_codes, (uint64_t)g.N, kb, TN, 64);
   const bool oka = A8 ? make_tmap(&ta, g.a_i8, (uint64_t)g.M, (uint64_t)g.K, 128, 128, true)
                      : make_tmap(&ta, g.a_codes, (uint64_t)g.M, kb, 128, 64);
@@ -967,6 +1039,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.mblocks = (g.M + 127) / 128;
   p.a_scales = g.a_scales; p.w_scales = g.w_scales;
   p.a_zeros = g.a_zeros; p.w_sums = g.w_sums;
+  p.pair = PAIR ? 1 : 0;
   p.bias = g.bias; p.residual = g.residual; p.gamma = g.gamma; p.beta = g.beta;
   p.ln_eps = g.ln_eps; p.clip = g.clip;
   p.out_i32 = g.out_i32; p.out_f16 = g.out_f16; p.out_codes = g.out_codes; p.out_scales = g.out_scales;
@@ -982,11 +1055,13 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     p.trace = trace_buf;
   }
   const int sms = num_sms();
-  // groups of ntn co-resident CTAs (one per SM); a group walks the m-blocks
-  if (p.ntn > sms) { *why = "N/TN exceeds the number of SMs"; return cudaErrorNotSupported; }
-  p.groups = sms / p.ntn;
-  if (p.groups > p.mblocks) p.groups = p.mblocks;
-  const int grid = p.groups * p.ntn;
+  // groups of ntn co-resident CTAs (one per SM); a group walks the m-blocks.  Pairs: the unit
+  // is a 2-CTA cluster (two SMs) walking m-block pairs.
+  const int units = PAIR ? sms / 2 : sms, mwalk = PAIR ? p.mblocks / 2 : p.mblocks;
+  if (p.ntn > units) { *why = "N/TN exceeds the number of SMs"; return cudaErrorNotSupported; }
+  p.groups = units / p.ntn;
+  if (p.groups > mwalk) p.groups = mwalk;
+  const int grid = p.groups * p.ntn * (PAIR ? 2 : 1);
   if (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4) {
     const size_t need = tc_workspace_bytes(g.M, g.N, TN);
     if (!ws || ws_bytes < need) { *why = "workspace too small for the row-epilogue exchange"; return cudaErrorInvalidValue; }
@@ -998,7 +1073,24 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   }
   note_launch();
   {
-    const cudaError_t le = launch_pdl(g.M <= kPdlMaxRows, kern, dim3(grid), dim3(EpiCfg<KIND>::THREADS), C::SMEM, s, ta, tb, p);
+    cudaError_t le;
+    if constexpr (PAIR) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(EpiCfg<KIND>::THREADS);
+      cfg.dynamicSmemBytes = C::SMEM;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      le = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+    } else {
+      le = launch_pdl(g.M <= kPdlMaxRows, kern, dim3(grid), dim3(EpiCfg<KIND>::THREADS), C::SMEM, s, ta, tb, p);
+    }
     if (le != cudaSuccess) return le;
   }
   if (trace_path) {  // profiling only: dump the stamps of this launch (synchronous)
@@ -1015,6 +1107,13 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   return cudaGetLastError();
 }
 
+// The CTA-pair mainloop is on by default where it measured faster; Q4_PAIR=0 disables it
+// (profiling / A-B only).
+bool tc_pair_enabled() {
+  static const int env = [] { const char* e = getenv("Q4_PAIR"); return e ? atoi(e) : -1; }();
+  return env != 0;
+}
+
 template <int TN, bool BI8, bool A8 = false>
 cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s, const char** why) {
   if constexpr (A8) {
@@ -1026,6 +1125,15 @@ cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s
       }
       *why = "fp16 operands: no such epilogue";
       return cudaErrorInvalidValue;
+    }
+  }
+  if constexpr (BI8 && !A8 && TN == 256) {
+    // CTA-pair mainloop (cta_group::2) for large problems with prepacked weights
+    // (F16 / I32 only: measured QKV 105.8 -> 95.4 us at M = 32768; the RESLN row epilogue
+    // measured slower on pairs, 151 -> 160 us for FFN2, so it stays on the 1-CTA mainloop)
+    if (g.M % 256 == 0 && g.M >= 8192 && (g.kind == EPI_F16 || g.kind == EPI_I32) && tc_pair_enabled()) {
+      if (g.kind == EPI_I32) return run_tc<TN, EPI_I32, true, false, false, true>(g, ws, wsb, s, why);
+      return run_tc<TN, EPI_F16, true, false, false, true>(g, ws, wsb, s, why);
     }
   }
   switch (g.kind) {

@@ -402,3 +402,22 @@ def test_encoder_pipeline_serving(q4):
         torch.cuda.synchronize()
         for i in range(n):
             assert np.array_equal(outs[i].numpy(), refs[i]), (n, i)
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 3072, 1024), (8448, 2304, 768)])
+def test_linear_f16_cta_pair(q4, M, N, K):
+    """M % 256 == 0 and M >= 8192 with prepacked weights runs the CTA-pair mainloop
+    (tcgen05.mma.cta_group::2, M = 256): sampled 128-row slices (both CTAs of a pair, first and
+    last pairs) against the oracle; INT32 bit-exact, fp16 within tolerance."""
+    x, wt, b = synth.hidden(M, K, f"cp{M}"), synth.weight(N, K, f"cpw{N}_{K}"), synth.bias(N, f"cpb{N}")
+    a, sa = orc.quantize_rows(x)
+    w, sw = orc.quantize_rows(wt)
+    wd = dev(w)
+    w8 = q4.prepack_weights(wd)
+    i32 = host(q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_I32, w_i8=w8)["i32"])
+    f16 = host(q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_F16, bias=dev(b), w_i8=w8)["f16"])
+    for m0 in (0, 128, M // 2 - 128, M - 256, M - 128):
+        rows = slice(m0, m0 + 128)
+        assert np.array_equal(i32[rows], orc.gemm_i32(a[rows], w, 128, N, K)), m0
+        ref = orc.w4a4_linear(a[rows], sa[rows], w, sw, 128, N, K, orc.EPI_F16, bias=b)["f16"]
+        assert_f16_close(f16[rows], ref, f"pair F16 rows {m0}")
