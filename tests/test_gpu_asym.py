@@ -67,3 +67,25 @@ def test_w4a4_asym_linear(q4, M, N, K, w8):
     ref = orc.w4a4_asym_linear(a, sa, za, w, sw, M, N, K, orc.EPI_F16, bias=b)["f16"]
     g, r = host(out).astype(np.float64), ref.astype(np.float64)
     assert (np.abs(g - r) <= 1e-3 + 2e-3 * np.abs(r)).all()
+
+
+def test_w4a4_asym_linear_cta_pair(q4):
+    """M % 256 == 0, M >= 8192, prepacked weights: the asymmetric GEMM on the CTA-pair mainloop
+    (u8 x s8 with M = 256); sampled row slices against O-16."""
+    M, N, K = 8192, 1024, 1024
+    x = synth.hidden(M, K, "tap_x") + np.float16(0.5)
+    wt, b = synth.weight(N, K, "tap_w"), synth.bias(N, "tap_b")
+    a, sa, za = orc.quantize_rows_asym(x)
+    w, sw = orc.quantize_rows(wt)
+    wd = dev(w)
+    ws = q4.weight_code_sums(wd)
+    kw = {"w_i8": q4.prepack_weights(wd)}
+    i32 = host(q4.w4a4_asym_linear(dev(a), dev(sa), dev(za), wd, dev(sw), ws, q4.EPI_I32, **kw)["i32"])
+    f16 = host(q4.w4a4_asym_linear(dev(a), dev(sa), dev(za), wd, dev(sw), ws, q4.EPI_F16, bias=dev(b), **kw)["f16"])
+    for m0 in (0, 128, M - 128):
+        rows = slice(m0, m0 + 128)
+        assert np.array_equal(i32[rows], orc.w4a4_asym_linear(a[rows], sa[rows], za[rows], w, sw, 128, N, K,
+                                                               orc.EPI_I32)["i32"])
+        r = orc.w4a4_asym_linear(a[rows], sa[rows], za[rows], w, sw, 128, N, K, orc.EPI_F16, bias=b)["f16"]
+        g = f16[rows].astype(np.float64)
+        assert (np.abs(g - r) <= 1e-3 + 2e-3 * np.abs(r.astype(np.float64))).all()
