@@ -1131,7 +1131,8 @@ cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s
     // CTA-pair mainloop (cta_group::2) for large problems with prepacked weights
     // (F16 / I32 only: measured QKV 105.8 -> 95.4 us at M = 32768; the RESLN row epilogue
     // measured slower on pairs, 151 -> 160 us for FFN2, so it stays on the 1-CTA mainloop)
-    if (g.M % 256 == 0 && g.M >= 8192 && (g.kind == EPI_F16 || g.kind == EPI_I32) && tc_pair_enabled()) {
+    if (g.M % 256 == 0 && g.M >= 8192 && (g.kind == EPI_F16 || g.kind == EPI_I32) && g.N / TN <= num_sms() / 2 &&
+        tc_pair_enabled()) {
       if (g.kind == EPI_I32) return run_tc<TN, EPI_I32, true, false, false, true>(g, ws, wsb, s, why);
       return run_tc<TN, EPI_F16, true, false, false, true>(g, ws, wsb, s, why);
     }

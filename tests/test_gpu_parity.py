@@ -421,3 +421,14 @@ def test_linear_f16_cta_pair(q4, M, N, K):
         assert np.array_equal(i32[rows], orc.gemm_i32(a[rows], w, 128, N, K)), m0
         ref = orc.w4a4_linear(a[rows], sa[rows], w, sw, 128, N, K, orc.EPI_F16, bias=b)["f16"]
         assert_f16_close(f16[rows], ref, f"pair F16 rows {m0}")
+
+
+def test_linear_f16_wide_n_falls_back_from_pairs(q4):
+    """N / 256 > SMs / 2: the CTA-pair grid would not fit, the 1-CTA path takes it."""
+    M, N, K = 8192, 256 * 80, 256
+    a = synth.random_packed(M, K, "wn_a")
+    w = synth.random_packed(N, K, "wn_w")
+    sa, sw = synth.random_scales(M, "wn_sa"), synth.random_scales(N, "wn_sw")
+    wd = dev(w)
+    i32 = host(q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_I32, w_i8=q4.prepack_weights(wd))["i32"])
+    assert np.array_equal(i32[:128], orc.gemm_i32(a[:128], w, 128, N, K))
