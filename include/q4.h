@@ -127,9 +127,12 @@ typedef struct {
                                 same codes as w_codes; NULL = unpack w_codes on chip       */
 } q4_epilogue;
 
-/* Requirements: M >= 0; N % 32 == 0; K % 32 == 0; K <= 8192 (the INT32 accumulator
- * bound |acc| <= 64 K); all pointers 16-byte aligned.  Workspace: none today
- * (returns 0); pass any pointer. */
+/* Requirements: M >= 0; N % 32 == 0 (row epilogues N % 64 == 0); K % 32 == 0; K <= 8192
+ * (the INT32 accumulator bound |acc| <= 64 K); N / tile_n <= #SMs (every CTA owns one n-block,
+ * tile_n = 256 for M > 512, 64 below: N <= 37,888 resp. 9,472 on B200; larger N returns
+ * Q4_EUNSUPPORTED); all pointers 16-byte aligned.  Workspace: q4_w4a4_linear_workspace bytes
+ * (row epilogues: the cross-CTA exchange slots and self-resetting counters; zero-filled once
+ * before first use, left zeroed by every launch); 0 for I32 / F16. */
 Q4_API size_t q4_w4a4_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind);
 Q4_API q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, /* [M,K/2], [M] */
                          const uint8_t* w_codes, const float* w_scales, /* [N,K/2], [N] */
