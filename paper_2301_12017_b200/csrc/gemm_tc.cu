@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     w4a4_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
   static_assert(!A8 || BI8, "W8A8 takes int8 weights through the BI8 path");
   static_assert(!H16 || A8, "fp16 operands use the A8 staging");
-  static_assert(!PAIR || (BI8 && !A8 && KIND != EPI_GELU_Q4), "pair mainloop: prepacked weights, F16/I32/RESLN");
+  static_assert(!PAIR || (BI8 && !H16 && KIND != EPI_GELU_Q4), "pair mainloop: int8 weights, F16/I32/RESLN");
   // (RESLN instantiations compile but are not dispatched: measured slower)
   using C = TcCfg<TN, BI8, A8, PAIR>;
   extern __shared__ uint8_t smem_raw[];
@@ -480,9 +480,24 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
             const int su = g % C::SU;
             mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
             uint8_t* ub = smem + C::OFF_UN + su * C::UN_STAGE;
-            mbar_arrive_expect_tx(&full_u[su], (uint32_t)C::UN_STAGE);
-            tma_load_2d(ub, &tmA, &full_u[su], kb * 128, mb * C::BM);
-            tma_load_2d(ub + C::A_UN, &tmB, &full_u[su], kb * 128, nb * TN);
+            if constexpr (PAIR) {
+              // W8A8 pair: this CTA's A rows and half of the B tile, counted on the leader's barrier
+              if (crank == 0) mbar_arrive_expect_tx(&full_u[su], (uint32_t)(2 * C::UN_STAGE));
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(ub)), "l"(reinterpret_cast<uint64_t>(&tmA)),
+                  "r"(lead(&full_u[su])), "r"(kb * 128), "r"(mb * C::BM)
+                  : "memory");
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(ub + C::A_UN)), "l"(reinterpret_cast<uint64_t>(&tmB)),
+                  "r"(lead(&full_u[su])), "r"(kb * 128), "r"(nb * TN + (int)crank * (TN / 2))
+                  : "memory");
+            } else {
+              mbar_arrive_expect_tx(&full_u[su], (uint32_t)C::UN_STAGE);
+              tma_load_2d(ub, &tmA, &full_u[su], kb * 128, mb * C::BM);
+              tma_load_2d(ub + C::A_UN, &tmB, &full_u[su], kb * 128, nb * TN);
+            }
           }
           continue;
         }
@@ -1117,6 +1132,11 @@ bool tc_pair_enabled() {
 template <int TN, bool BI8, bool A8 = false>
 cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s, const char** why) {
   if constexpr (A8) {
+    if (!g.f16_ops && TN == 256 && g.M % 256 == 0 && g.M >= 8192 && (g.kind == EPI_F16 || g.kind == EPI_I32) &&
+        g.N / TN <= num_sms() / 2 && tc_pair_enabled()) {  // W8A8 on the CTA-pair mainloop
+      if (g.kind == EPI_I32) return run_tc<TN, EPI_I32, true, true, false, true>(g, ws, wsb, s, why);
+      return run_tc<TN, EPI_F16, true, true, false, true>(g, ws, wsb, s, why);
+    }
     if (g.f16_ops) {  // fp16 operands (q4_f16_linear): no I32 epilogue
       switch (g.kind) {
         case EPI_F16: return run_tc<TN, EPI_F16, true, true, true>(g, ws, wsb, s, why);

@@ -325,3 +325,17 @@ def test_w8a8_full_size_layer_sampled(q4):
         assert_f16_close(T["h_out"], r3["f16"], "h_out")
         c2, s2 = orc.quantize_rows_i8(T["h_out"])
         assert np.array_equal(T["hq_out"], c2) and np.array_equal(T["hs_out"], s2)
+
+
+def test_w8a8_cta_pair(q4):
+    """W8A8 at M % 256 == 0, M >= 8192 runs on the CTA-pair mainloop: sampled slices exact."""
+    M, N, K = 8192, 3072, 1024
+    a = synth.random_i8(M, K, "w8p_a")
+    w = synth.random_i8(N, K, "w8p_w")
+    sa, sw = synth.random_scales(M, "w8p_sa"), synth.random_scales(N, "w8p_sw")
+    i32 = host(q4.w8a8_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_I32)["i32"])
+    f16 = host(q4.w8a8_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_F16)["f16"])
+    for m0 in (0, 128, M - 128):
+        rows = slice(m0, m0 + 128)
+        assert np.array_equal(i32[rows], orc.gemm_i32_i8(a[rows], w, 128, N, K)), m0
+        assert_f16_close(f16[rows], orc.w8a8_linear(a[rows], sa[rows], w, sw, 128, N, K, orc.EPI_F16)["f16"], "pair")
