@@ -339,3 +339,33 @@ def test_w8a8_cta_pair(q4):
         rows = slice(m0, m0 + 128)
         assert np.array_equal(i32[rows], orc.gemm_i32_i8(a[rows], w, 128, N, K)), m0
         assert_f16_close(f16[rows], orc.w8a8_linear(a[rows], sa[rows], w, sw, 128, N, K, orc.EPI_F16)["f16"], "pair")
+
+
+@pytest.mark.slow
+def test_quantize_i8_exhaustive_fp16_pairs(q4):
+    """Every (x, amax) fp16 pair with 0 <= x <= amax through the 8-bit CUDA quantizer equals
+    the exact rational rounding rhe(127 x / amax) (O-11), computed here in int64 on the
+    fp16 values as integers in units of 2^-24.  (At 8 bits the IEEE-division form is not a
+    valid reference: the quotient can land within half an ulp of a half-integer.)"""
+    bits = np.arange(1, 0x7C00, dtype=np.uint16)
+    allpos = bits.view(np.float16)
+    ival = (allpos.astype(np.float64) * 2.0 ** 24).astype(np.int64)  # exact
+    n = allpos.size
+    chunk = 512
+    for s in range(0, n, chunk):
+        idx = np.arange(s, min(n, s + chunk))
+        width = ((idx[-1] + 1 + 7) // 8) * 8
+        X = np.zeros((idx.size, width), np.float16)
+        for r, i in enumerate(idx):
+            X[r, : i + 1] = allpos[: i + 1]
+        c, sc = q4.quantize_rows_i8(dev(X))
+        q = host(c).astype(np.int64)
+        Xi = (X.astype(np.float64) * 2.0 ** 24).astype(np.int64)
+        A = ival[idx][:, None]
+        num, den = 254 * Xi + A, 2 * A  # rhe(127 X / A) = floor((254 X + A) / 2A), ties to even
+        ref = num // den
+        tie = (num % den == 0) & (ref % 2 == 1)
+        ref = ref - tie
+        mask = np.arange(width)[None, :] <= idx[:, None]
+        assert np.array_equal(q[mask], ref[mask]), f"chunk {s}"
+        assert np.array_equal(host(sc), allpos[idx].astype(np.float32) / np.float32(127))
