@@ -95,3 +95,21 @@ def test_layer_structs_match_the_header():
     assert tuple(names) == _lib.WEIGHT_FIELDS
     cfg = re.search(r"typedef struct \{(.*?)\} q4_layer_cfg;", src, re.S).group(1)
     assert "fp16_parts" in cfg and [n for n, _ in _lib.LayerCfg._fields_][-1] == "fp16_parts"
+
+
+def test_workspace_sizes(L):
+    """Host-side sizing (no GPU): the row epilogues need exchange slots + counters that grow
+    with M and N / tile_n; F16 / I32 need none; the layer / stack workspaces cover them."""
+    from paper_2301_12017_b200 import _lib
+    ws = L.q4_w4a4_linear_workspace
+    assert ws(32768, 3072, 1024, _lib.EPI_F16) == 0 and ws(32768, 3072, 1024, _lib.EPI_I32) == 0
+    g = ws(32768, 4096, 1024, _lib.EPI_GELU_Q4)
+    r = ws(32768, 1024, 4096, _lib.EPI_RESLN_Q4)
+    # [mblocks][ntn][128] x (8 B stats + 4 B max) + counters: 256 m-blocks, 16 resp. 4 n-blocks
+    assert g >= 256 * 16 * 128 * 12 and r >= 256 * 4 * 128 * 12
+    assert ws(1024, 4096, 1024, _lib.EPI_GELU_Q4) < g
+    cfg = _lib.LayerCfg(1024, 16, 64, 4096, 1e-12, 0)
+    lw = L.q4_encoder_layer_workspace(C.byref(cfg), 256, 128)
+    sw = L.q4_encoder_stack_workspace(C.byref(cfg), 256, 128)
+    assert lw > g and sw > lw
+    assert L.q4_encoder_pipeline_workspace(C.byref(cfg), 256, 128) >= sw + 4 * 256 * 128 * 1024 * 2
