@@ -19,8 +19,12 @@
  *     A workspace must be ZERO-FILLED before its first use (cudaMemset): the row
  *     epilogues keep self-resetting cross-CTA rendezvous counters in it, and every
  *     completed call leaves them zero again, so no per-call reset (and no memset node
- *     in a captured graph) is needed.  A counter left non-zero (e.g. by a kernel fault)
- *     makes the next row-epilogue call trap with Q4_ECUDA instead of hanging.
+ *     in a captured graph) is needed.  The counters sit at the start of the workspace at
+ *     an offset that depends on M only, so one linear workspace serves row-epilogue calls
+ *     of the same M and any N / K (an encoder layer's N = hidden and N = ffn launches);
+ *     a call with a different M needs its own zero-filled workspace.  A counter left
+ *     non-zero (e.g. by a kernel fault) makes the next row-epilogue call trap with
+ *     Q4_ECUDA instead of hanging.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *     Calls are stream-ordered and asynchronous: no host synchronisation, no
  *     allocation, no host-side state change, so they can be captured in CUDA graphs
@@ -104,11 +108,15 @@ typedef enum { Q4_EPI_I32 = 0, Q4_EPI_F16 = 1, Q4_EPI_GELU_Q4 = 2, Q4_EPI_RESLN_
  *   MMA_SYNC_S4 legacy: cp.async -> ldmatrix -> mma.sync m16n8k64 .s4 (emulated on sm_100a)
  *   TCGEN05_W8  as TCGEN05, but the weights come prepacked (epi->w_i8, q4_prepack_weights):
  *               TMA'd straight into the swizzled operand stage; only A is unpacked on chip
+ *   TCGEN05_W8_1CTA  as TCGEN05_W8, never the CTA-pair (cta_group::2) mainloop that
+ *               TCGEN05_W8 / AUTO pick for F16 / I32 at M % 256 == 0, M >= 8192 (the row
+ *               epilogues always run 1-CTA; this reproduces their accumulators in an I32 tap)
  * AUTO uses TCGEN05_W8 when epi->w_i8 is given (faster at every measured M, 128..32768:
  * profiles/r1_gemm_sweep.jsonl), else TCGEN05.
  * The legacy variants implement Q4_EPI_I32 and Q4_EPI_F16 only. */
 typedef enum { Q4_MAINLOOP_AUTO = 0, Q4_MAINLOOP_TCGEN05 = 1, Q4_MAINLOOP_MMA_SYNC_S8 = 2,
-               Q4_MAINLOOP_MMA_SYNC_S4 = 3, Q4_MAINLOOP_TCGEN05_W8 = 4 } q4_mainloop;
+               Q4_MAINLOOP_MMA_SYNC_S4 = 3, Q4_MAINLOOP_TCGEN05_W8 = 4,
+               Q4_MAINLOOP_TCGEN05_W8_1CTA = 5 } q4_mainloop;
 
 typedef struct {
   int32_t kind;              /* q4_epi_kind                                              */
@@ -287,8 +295,9 @@ Q4_API q4_status q4_encoder_stack(const q4_layer_cfg* cfg, const q4_layer_weight
  * Batch i's upload (copy-in stream), forward (the caller's stream, = q4_encoder_stack) and
  * download (copy-out stream) overlap the neighbouring batches through two device input and
  * two device output buffers inside `workspace` (q4_encoder_pipeline_workspace).  The
- * caller's stream completes after the last download.  Streams/events are created on the
- * first call per device and reused; not CUDA-graph capturable. */
+ * caller's stream completes after the last download.  The two copy streams and their events
+ * are created per call and released when the enqueued work completes, so concurrent calls
+ * (distinct workspaces) are independent; not CUDA-graph capturable. */
 Q4_API size_t q4_encoder_pipeline_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S);
 Q4_API q4_status q4_encoder_pipeline(const q4_layer_cfg* cfg, const q4_layer_weights* layers, int32_t L,
                                      int64_t B, int64_t S, const uint16_t* const* h_in,

@@ -13,7 +13,8 @@ LIB_PATH = os.environ.get("Q4_LIB_PATH") or os.path.join(HERE, "libq4.so")
 
 Q4_OK, Q4_EINVAL, Q4_ESHAPE, Q4_EALIGN, Q4_EUNSUPPORTED, Q4_ECUDA = range(6)
 EPI_I32, EPI_F16, EPI_GELU_Q4, EPI_RESLN_Q4 = range(4)
-MAINLOOP_AUTO, MAINLOOP_TCGEN05, MAINLOOP_MMA_SYNC_S8, MAINLOOP_MMA_SYNC_S4, MAINLOOP_TCGEN05_W8 = range(5)
+(MAINLOOP_AUTO, MAINLOOP_TCGEN05, MAINLOOP_MMA_SYNC_S8, MAINLOOP_MMA_SYNC_S4, MAINLOOP_TCGEN05_W8,
+ MAINLOOP_TCGEN05_W8_1CTA) = range(6)
 STATUS_NAMES = ["Q4_OK", "Q4_EINVAL", "Q4_ESHAPE", "Q4_EALIGN", "Q4_EUNSUPPORTED", "Q4_ECUDA"]
 
 EXPORTS = (

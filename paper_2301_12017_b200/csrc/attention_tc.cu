@@ -461,8 +461,8 @@ cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __ha
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  static const char* trace_path = getenv("Q4_TRACE");
-  static const int dbg = getenv("Q4_ATTN_DBG") ? atoi(getenv("Q4_ATTN_DBG")) : 0;  // profiling only
+  static const char* trace_path = prof_env("Q4_TRACE");
+  static const int dbg = prof_env("Q4_ATTN_DBG") ? atoi(prof_env("Q4_ATTN_DBG")) : 0;  // profiling only
   static unsigned long long* trace_buf = nullptr;
   if (trace_path && !trace_buf) cudaMalloc(&trace_buf, sizeof(unsigned long long) * 512 * 16 * 16);
   // Small batches: split each sequence's heads over a cluster of G CTAs so the grid fills
@@ -485,7 +485,7 @@ cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __ha
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see launch_pdl)
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  static const bool no_pdl = getenv("Q4_NO_PDL") != nullptr;  // profiling only
+  static const bool no_pdl = prof_env("Q4_NO_PDL") != nullptr;  // profiling only
   cfg.numAttrs = (no_pdl || (int64_t)B * S > kPdlMaxRows) ? 1 : 2;
   cudaError_t le = cudaLaunchKernelEx(&cfg, attention_tc_kernel, tq, S, heads, ctx_f16, ctx_codes, ctx_scales,
                                       trace_path ? trace_buf : nullptr, dbg, G, i8 ? 1 : 0);

@@ -33,6 +33,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "../../include/q4.h"
 #include "kernels.h"
 
 namespace q4 {
@@ -1066,10 +1067,10 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.ln_eps = g.ln_eps; p.clip = g.clip;
   p.out_i32 = g.out_i32; p.out_f16 = g.out_f16; p.out_codes = g.out_codes; p.out_scales = g.out_scales;
   p.xstat = nullptr; p.xamax = nullptr; p.xcnt = nullptr;
-  static const int dbg = [] { const char* e = getenv("Q4_DEBUG_SKIP"); return e ? atoi(e) : 0; }();
+  static const int dbg = [] { const char* e = prof_env("Q4_DEBUG_SKIP"); return e ? atoi(e) : 0; }();
   p.dbg = dbg;
   p.trace = nullptr;
-  static const char* trace_path = getenv("Q4_TRACE");
+  static const char* trace_path = prof_env("Q4_TRACE");
   static unsigned long long* trace_buf = nullptr;
   if (trace_path) {
     if (!trace_buf) cudaMalloc(&trace_buf, sizeof(unsigned long long) * 148 * 64 * 8);
@@ -1087,11 +1088,14 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   if (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4) {
     const size_t need = tc_workspace_bytes(g.M, g.N, TN);
     if (!ws || ws_bytes < need) { *why = "workspace too small for the row-epilogue exchange"; return cudaErrorInvalidValue; }
+    // counters first, at an offset that depends on M only: row-epilogue launches of the same M
+    // and any N (a layer's RESLN N = hidden and GELU N = ffn) share one workspace, and one
+    // launch's float partials never land on another launch's counters
     uint8_t* w = reinterpret_cast<uint8_t*>(ws);
-    const size_t nslot = (size_t)p.mblocks * p.ntn * 128;
-    p.xstat = reinterpret_cast<float2*>(w);
-    p.xamax = reinterpret_cast<float*>(w + nslot * 8);
-    p.xcnt = reinterpret_cast<unsigned*>(w + nslot * 12);
+    const size_t nslot = (size_t)p.mblocks * p.ntn * 128, cnt_bytes = tc_counter_bytes(g.M);
+    p.xcnt = reinterpret_cast<unsigned*>(w);
+    p.xstat = reinterpret_cast<float2*>(w + cnt_bytes);
+    p.xamax = reinterpret_cast<float*>(w + cnt_bytes + nslot * 8);
   }
   note_launch();
   {
@@ -1132,7 +1136,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
 // The CTA-pair mainloop is on by default where it measured faster; Q4_PAIR=0 disables it
 // (profiling / A-B only).
 bool tc_pair_enabled() {
-  static const int env = [] { const char* e = getenv("Q4_PAIR"); return e ? atoi(e) : -1; }();
+  static const int env = [] { const char* e = prof_env("Q4_PAIR"); return e ? atoi(e) : -1; }();
   return env != 0;
 }
 
@@ -1140,7 +1144,7 @@ template <int TN, bool BI8, bool A8 = false>
 cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s, const char** why) {
   if constexpr (A8) {
     if (!g.f16_ops && TN == 256 && g.M % 256 == 0 && g.M >= 8192 && (g.kind == EPI_F16 || g.kind == EPI_I32) &&
-        g.N / TN <= num_sms() / 2 && tc_pair_enabled()) {  // W8A8 on the CTA-pair mainloop
+        g.N / TN <= num_sms() / 2 && g.mainloop != Q4_MAINLOOP_TCGEN05_W8_1CTA && tc_pair_enabled()) {  // W8A8 on the CTA-pair mainloop
       if (g.kind == EPI_I32) return run_tc<TN, EPI_I32, true, true, false, true>(g, ws, wsb, s, why);
       return run_tc<TN, EPI_F16, true, true, false, true>(g, ws, wsb, s, why);
     }
@@ -1158,7 +1162,7 @@ cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s
     // CTA-pair mainloop (cta_group::2) for large problems with prepacked weights
     // (F16 / I32 only: measured QKV 105.8 -> 95.4 us at M = 32768; the RESLN row epilogue
     // measured slower on pairs, 151 -> 160 us for FFN2, so it stays on the 1-CTA mainloop)
-    if (g.M % 256 == 0 && g.M >= 8192 && (g.kind == EPI_F16 || g.kind == EPI_I32) && g.N / TN <= num_sms() / 2 &&
+    if (g.M % 256 == 0 && g.M >= 8192 && (g.kind == EPI_F16 || g.kind == EPI_I32) && g.N / TN <= num_sms() / 2 && g.mainloop != Q4_MAINLOOP_TCGEN05_W8_1CTA &&
         tc_pair_enabled()) {
       if (g.kind == EPI_I32) return run_tc<TN, EPI_I32, true, false, false, true>(g, ws, wsb, s, why);
       return run_tc<TN, EPI_F16, true, false, false, true>(g, ws, wsb, s, why);
@@ -1189,7 +1193,7 @@ int tc_tile_n(int M, int N, int kind) {
   // Small M (latency configs): narrower tiles spread the work over more SMs.  Row
   // epilogues need >= 64 columns per tile (>= 16 code bytes per row per half).
   const bool row = kind == EPI_GELU_Q4 || kind == EPI_RESLN_Q4;
-  static const int env_tn = getenv("Q4_TN") ? atoi(getenv("Q4_TN")) : 0;  // profiling only
+  static const int env_tn = prof_env("Q4_TN") ? atoi(prof_env("Q4_TN")) : 0;  // profiling only
   const int pref = env_tn ? env_tn : M <= 512 ? 64 : 256;
   static const int cand[] = {256, 128, 64, 32};
   for (int c : cand)
@@ -1199,10 +1203,15 @@ int tc_tile_n(int M, int N, int kind) {
   return 0;
 }
 
+size_t tc_counter_bytes(int M) {
+  const size_t mblocks = (size_t)(M + 127) / 128;
+  return (4 * mblocks * sizeof(unsigned) + 255) & ~(size_t)255;
+}
+
 size_t tc_workspace_bytes(int M, int N, int TN) {
   if (TN <= 0) return 0;
   const size_t mblocks = (size_t)(M + 127) / 128, ntn = (size_t)N / TN;
-  return mblocks * ntn * 128 * 12 + 4 * mblocks * sizeof(unsigned) + 256;
+  return tc_counter_bytes(M) + mblocks * ntn * 128 * 12;
 }
 
 cudaError_t launch_w4a4_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {

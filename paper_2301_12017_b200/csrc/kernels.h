@@ -12,6 +12,15 @@ namespace q4 {
 
 void note_launch(int n = 1);  // counts kernels launched (q4_launch_count)
 
+// Profiling knobs (Q4_DEBUG_SKIP, Q4_TRACE, Q4_TN, Q4_PAIR, Q4_NO_PDL, Q4_ATTN_DBG) exist only in
+// a build compiled with -DQ4_PROFILING (build.py --profiling -> libq4_prof.so, selected with
+// Q4_LIB_PATH).  The shipped libq4.so reads no environment variable: prof_env() is nullptr.
+#ifdef Q4_PROFILING
+inline const char* prof_env(const char* name) { return getenv(name); }
+#else
+inline const char* prof_env(const char*) { return nullptr; }
+#endif
+
 // Launch with programmatic stream serialization (PDL) when `pdl`: the kernel may start
 // while its predecessor in the stream drains (it calls pdl_wait() before dependent
 // accesses; without the attribute that wait is a no-op).  Callers enable it for small
@@ -31,7 +40,7 @@ cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, siz
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  static const bool off = getenv("Q4_NO_PDL") != nullptr;  // profiling only: plain launches
+  static const bool off = prof_env("Q4_NO_PDL") != nullptr;  // profiling only: plain launches
   cfg.numAttrs = (pdl && !off) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
@@ -75,9 +84,8 @@ cudaError_t launch_quantize_rows_i8(const __half* x, int64_t rows, int cols, int
 cudaError_t launch_w4a4_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why);
 int tc_tile_n(int M, int N, int kind);
 size_t tc_workspace_bytes(int M, int N, int TN);
+size_t tc_counter_bytes(int M);  // the rendezvous counters at the start of a row-epilogue workspace
 cudaError_t launch_w4a4_legacy(const GemmArgs& g, bool s4, cudaStream_t s, const char** why);
-cudaError_t launch_attention(const __half* qkv, int B, int S, int heads, __half* ctx_f16,
-                             uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s);
 // i8: W8A8 baseline -- int8 ctx codes [B*S, h] with scale amax/127 instead of packed INT4
 cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __half* ctx_f16,
                                 uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s, bool i8 = false);

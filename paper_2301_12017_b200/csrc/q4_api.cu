@@ -198,12 +198,20 @@ q4_status q4_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales, con
   if (!a_zeros || (epi->kind == Q4_EPI_F16 && !w_sums))
     return fail(Q4_EINVAL, "q4_w4a4_asym_linear: NULL a_zeros / w_sums");
   if (epi->kind == Q4_EPI_F16 && !al16(w_sums)) return fail(Q4_EALIGN, "q4_w4a4_asym_linear: w_sums 16-byte aligned");
-  // the shared validation / dispatch of q4_w4a4_linear with the asymmetric fields set
-  if (M < 0 || N <= 0 || K <= 0 || N % 32 || K % 32 || K > 8192)
-    return fail(Q4_ESHAPE, "q4_w4a4_asym_linear: M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
+  // the validation of q4_w4a4_linear with the asymmetric fields set
+  if (M < 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1 << 24) || N % 32 || K % 32 || K > 8192)
+    return fail(Q4_ESHAPE, "q4_w4a4_asym_linear: M=%lld N=%lld K=%lld (N %% 32 == 0, K %% 32 == 0, K <= 8192)",
+                (long long)M, (long long)N, (long long)K);
   if (M == 0) return Q4_OK;
-  if (!a_codes || !a_scales || !w_codes || !w_scales || !al16(a_codes) || !al16(w_codes) || !al16(w_scales))
-    return fail(Q4_EALIGN, "q4_w4a4_asym_linear: NULL or misaligned operand");
+  if (!a_codes || !a_scales || !w_codes || !w_scales)
+    return fail(Q4_EINVAL, "q4_w4a4_asym_linear: NULL operand (a_codes/a_scales/w_codes/w_scales)");
+  if (!al16(a_codes) || !al16(w_codes) || !al16(w_scales) || !al4(a_scales) || !al4(a_zeros))
+    return fail(Q4_EALIGN, "q4_w4a4_asym_linear: codes / w_scales 16-byte aligned, a_scales / a_zeros 4-byte aligned");
+  if (epi->bias && !al4(epi->bias)) return fail(Q4_EALIGN, "q4_w4a4_asym_linear: bias must be 4-byte aligned");
+  if (epi->mainloop == Q4_MAINLOOP_TCGEN05_W8 && (!epi->w_i8 || !al16(epi->w_i8)))
+    return fail(Q4_EINVAL, "q4_w4a4_asym_linear: TCGEN05_W8 needs 16-byte aligned epi->w_i8 (q4_prepack_weights)");
+  if (epi->mainloop == Q4_MAINLOOP_AUTO && epi->w_i8 && !al16(epi->w_i8))
+    return fail(Q4_EALIGN, "q4_w4a4_asym_linear: epi->w_i8 must be 16-byte aligned");
   if ((epi->kind == Q4_EPI_F16 && (!epi->out_f16 || !al16(epi->out_f16))) ||
       (epi->kind == Q4_EPI_I32 && (!epi->out_i32 || !al16(epi->out_i32))))
     return fail(Q4_EINVAL, "q4_w4a4_asym_linear: output NULL or not 16-byte aligned");
@@ -351,7 +359,8 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
   g.out_i32 = epi->out_i32; g.out_f16 = reinterpret_cast<__half*>(epi->out_f16);
   g.out_codes = epi->out_codes; g.out_scales = epi->out_scales;
   g.w_i8 = nullptr;
-  if (epi->mainloop == Q4_MAINLOOP_TCGEN05_W8 || (epi->mainloop == Q4_MAINLOOP_AUTO && epi->w_i8)) {
+  if (epi->mainloop == Q4_MAINLOOP_TCGEN05_W8 || epi->mainloop == Q4_MAINLOOP_TCGEN05_W8_1CTA ||
+      (epi->mainloop == Q4_MAINLOOP_AUTO && epi->w_i8)) {
     if (!epi->w_i8 || !al16(epi->w_i8))
       return fail(Q4_EINVAL, "q4_w4a4_linear: TCGEN05_W8 needs 16-byte aligned epi->w_i8 (q4_prepack_weights)");
     g.w_i8 = epi->w_i8;
@@ -361,7 +370,8 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
   switch (epi->mainloop) {
     case Q4_MAINLOOP_AUTO:
     case Q4_MAINLOOP_TCGEN05:
-    case Q4_MAINLOOP_TCGEN05_W8: e = q4::launch_w4a4_tc(g, workspace, ws_bytes, (cudaStream_t)stream, &why); break;
+    case Q4_MAINLOOP_TCGEN05_W8:
+    case Q4_MAINLOOP_TCGEN05_W8_1CTA: e = q4::launch_w4a4_tc(g, workspace, ws_bytes, (cudaStream_t)stream, &why); break;
     case Q4_MAINLOOP_MMA_SYNC_S8: e = q4::launch_w4a4_legacy(g, false, (cudaStream_t)stream, &why); break;
     case Q4_MAINLOOP_MMA_SYNC_S4: e = q4::launch_w4a4_legacy(g, true, (cudaStream_t)stream, &why); break;
     default: return fail(Q4_EINVAL, "q4_w4a4_linear: unknown mainloop %d", epi->mainloop);
@@ -393,12 +403,9 @@ q4_status q4_attention_f16_q4(const uint16_t* qkv, int64_t B, int64_t S, int32_t
     return fail(Q4_EINVAL, "q4_attention_f16_q4: NULL qkv/ctx_f16/ctx_codes/ctx_scales");
   if (!al16(qkv) || !al4(ctx_codes) || !al16(ctx_f16))
     return fail(Q4_EALIGN, "q4_attention_f16_q4: qkv/ctx_f16 must be 16-byte aligned, codes 4-byte");
-  // tcgen05 kernel by default; the mma.sync kernel stays as the measured baseline (Q4_ATTN_LEGACY=1)
-  static const bool legacy = [] { const char* e = getenv("Q4_ATTN_LEGACY"); return e && atoi(e) != 0; }();
   const __half* q = reinterpret_cast<const __half*>(qkv);
   __half* cf = reinterpret_cast<__half*>(ctx_f16);
-  cudaError_t e = legacy ? q4::launch_attention(q, (int)B, (int)S, heads, cf, ctx_codes, ctx_scales, (cudaStream_t)stream)
-                         : q4::launch_attention_tc(q, (int)B, (int)S, heads, cf, ctx_codes, ctx_scales, (cudaStream_t)stream);
+  cudaError_t e = q4::launch_attention_tc(q, (int)B, (int)S, heads, cf, ctx_codes, ctx_scales, (cudaStream_t)stream);
   return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_attention_f16_q4");
 }
 
@@ -531,13 +538,20 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
     }
     return q4_w4a4_linear(ac, as, wc, wsc, M, N, K, &e, ws.gemm_ws, ws.gemm_ws_bytes, stream);
   };
+  // INT32 tap of a part: the same operands through the mainloop its production launch runs
+  // (prepacked weights when present; the 1-CTA mainloop for the row-epilogue parts, which the
+  // pair mainloop does not take), so the tap sees the accumulators the epilogue consumed.
   auto acc_tap = [&](const uint8_t* ac, const float* as, const uint8_t* wc, const float* wsc, int64_t N, int64_t K,
-                     int32_t* out) -> q4_status {
+                     int32_t* out, const int8_t* w8, bool row_epi) -> q4_status {
     if (!out) return Q4_OK;
     q4_epilogue e;
     memset(&e, 0, sizeof e);
     e.kind = Q4_EPI_I32;
     e.out_i32 = out;
+    if (w8) {
+      e.w_i8 = w8;
+      e.mainloop = row_epi ? Q4_MAINLOOP_TCGEN05_W8_1CTA : Q4_MAINLOOP_TCGEN05_W8;
+    }
     if (i8)
       return q4_w8a8_linear(reinterpret_cast<const int8_t*>(ac), as, reinterpret_cast<const int8_t*>(wc), wsc, M, N, K,
                             &e, nullptr, 0, stream);
@@ -558,7 +572,7 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
     if ((st = f16lin(h_in, w->fqkv, 3 * h, h, e))) return st;
   } else {
     if ((st = lin(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, e))) return st;
-    if ((st = acc_tap(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, tp.acc_qkv))) return st;
+    if ((st = acc_tap(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, tp.acc_qkv, w->wqkv8, false))) return st;
   }
   // FP16 attention + fused per-token ctx quantize
   if ((st = i8 ? q4_attention_f16_q8(qkv, B, S, cfg->heads, cfg->head_dim, ctx_f16,
@@ -573,7 +587,7 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
     if ((st = f16lin(ctx_f16, w->fo, h, h, e))) return st;
   } else {
     if ((st = lin(ctx_codes, ctx_scales, w->wo, w->so, h, h, e))) return st;
-    if ((st = acc_tap(ctx_codes, ctx_scales, w->wo, w->so, h, h, tp.acc_o))) return st;
+    if ((st = acc_tap(ctx_codes, ctx_scales, w->wo, w->so, h, h, tp.acc_o, w->wo8, true))) return st;
   }
   // MLP intermediate: dequant + bias + GELU + requant (+ fp16 output for an FP16 MLP output)
   memset(&e, 0, sizeof e);
@@ -583,7 +597,7 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
     if ((st = f16lin(h1, w->f1, f, h, e))) return st;
   } else {
     if ((st = lin(h1_codes, h1_scales, w->w1, w->s1, f, h, e))) return st;
-    if ((st = acc_tap(h1_codes, h1_scales, w->w1, w->s1, f, h, tp.acc_1))) return st;
+    if ((st = acc_tap(h1_codes, h1_scales, w->w1, w->s1, f, h, tp.acc_1, w->w18, true))) return st;
   }
   // MLP output: dequant + bias + residual(h1) + LN2 + requant
   memset(&e, 0, sizeof e);
@@ -593,7 +607,7 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
     if ((st = f16lin(ffn1, w->f2, h, f, e))) return st;
   } else {
     if ((st = lin(f_codes, f_scales, w->w2, w->s2, h, f, e))) return st;
-    if ((st = acc_tap(f_codes, f_scales, w->w2, w->s2, h, f, tp.acc_2))) return st;
+    if ((st = acc_tap(f_codes, f_scales, w->w2, w->s2, h, f, tp.acc_2, w->w28, true))) return st;
   }
   return Q4_OK;
 }
@@ -722,8 +736,8 @@ q4_status q4_encoder_stack_w8a8(const q4_layer_cfg* cfg, const q4_layer_weights*
 // nbatch batches of host (pinned) inputs -> host outputs.  Batch i's H2D copy runs on a copy-in
 // stream, its forward on the caller's stream, its D2H copy on a copy-out stream; two device
 // input and two device output buffers (slot = i % 2) let batch i+1's upload and batch i-1's
-// download overlap batch i's forward.  Streams and events are created once per device and
-// reused (the call itself allocates nothing on the device).
+// download overlap batch i's forward.  The copy streams and events are created per call (the
+// call allocates no device memory) so concurrent calls on one device share no state.
 size_t q4_encoder_pipeline_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S) {
   if (!cfg) return 0;
   const size_t hb = align_up((size_t)(B * S) * cfg->hidden * 2);
@@ -746,54 +760,55 @@ q4_status q4_encoder_pipeline(const q4_layer_cfg* cfg, const q4_layer_weights* l
   uint8_t* base = (uint8_t*)workspace;
   uint16_t* din[2] = {(uint16_t*)(base + stack_bytes), (uint16_t*)(base + stack_bytes + hb)};
   uint16_t* dout[2] = {(uint16_t*)(base + stack_bytes + 2 * hb), (uint16_t*)(base + stack_bytes + 3 * hb)};
+  // Streams and events belong to this call (re-entrant: concurrent calls share nothing).  They
+  // are destroyed before returning; CUDA releases them once the enqueued work that uses them
+  // has completed (cudaStreamDestroy / cudaEventDestroy on pending work return immediately).
   struct Aux {
     cudaStream_t cin = nullptr, cout = nullptr;
-    cudaEvent_t in_ready[2], in_free[2], done[2], out_free[2];
-  };
-  static Aux aux[64];
-  static std::atomic<bool> made[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return fail(Q4_EUNSUPPORTED, "q4_encoder_pipeline: device %d", dev);
-  Aux& a = aux[dev];
-  if (!made[dev].load()) {
+    cudaEvent_t ev[9] = {};  // in_ready[2], in_free[2], done[2], out_free[2], start
+    ~Aux() {
+      for (cudaEvent_t x : ev)
+        if (x) cudaEventDestroy(x);
+      if (cin) cudaStreamDestroy(cin);
+      if (cout) cudaStreamDestroy(cout);
+    }
+  } a;
+  {
     cudaError_t e = cudaStreamCreateWithFlags(&a.cin, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a.cout, cudaStreamNonBlocking);
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
-      e = cudaEventCreateWithFlags(&a.in_ready[k], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.in_free[k], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.done[k], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.out_free[k], cudaEventDisableTiming);
-    }
+    for (int k = 0; k < 9 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&a.ev[k], cudaEventDisableTiming);
     if (e != cudaSuccess) return cuda_fail(e, "q4_encoder_pipeline: stream/event creation");
-    made[dev].store(true);
   }
+  cudaEvent_t* in_ready = a.ev;
+  cudaEvent_t* in_free = a.ev + 2;
+  cudaEvent_t* done = a.ev + 4;
+  cudaEvent_t* out_free = a.ev + 6;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
   // the auxiliary streams start after everything already queued on the caller's stream
-  cudaEvent_t start = a.done[0];
+  cudaEvent_t start = a.ev[8];
   if ((e = cudaEventRecord(start, s)) != cudaSuccess) return cuda_fail(e, "q4_encoder_pipeline");
   cudaStreamWaitEvent(a.cin, start, 0);
   cudaStreamWaitEvent(a.cout, start, 0);
   for (int32_t i = 0; i < nbatch; ++i) {
     const int k = i & 1;
-    if (i >= 2) cudaStreamWaitEvent(a.cin, a.in_free[k], 0);  // batch i-2 has consumed din[k]
+    if (i >= 2) cudaStreamWaitEvent(a.cin, in_free[k], 0);  // batch i-2 has consumed din[k]
     if ((e = cudaMemcpyAsync(din[k], h_in[i], hbytes, cudaMemcpyHostToDevice, a.cin)) != cudaSuccess)
       return cuda_fail(e, "q4_encoder_pipeline: H2D");
-    cudaEventRecord(a.in_ready[k], a.cin);
-    cudaStreamWaitEvent(s, a.in_ready[k], 0);
-    if (i >= 2) cudaStreamWaitEvent(s, a.out_free[k], 0);  // batch i-2's download has read dout[k]
+    cudaEventRecord(in_ready[k], a.cin);
+    cudaStreamWaitEvent(s, in_ready[k], 0);
+    if (i >= 2) cudaStreamWaitEvent(s, out_free[k], 0);  // batch i-2's download has read dout[k]
     if ((st = encoder_stack_impl(cfg, layers, L, B, S, din[k], dout[k], workspace, stack_bytes, stream, false)))
       return st;
-    cudaEventRecord(a.in_free[k], s);
-    cudaEventRecord(a.done[k], s);
-    cudaStreamWaitEvent(a.cout, a.done[k], 0);
+    cudaEventRecord(in_free[k], s);
+    cudaEventRecord(done[k], s);
+    cudaStreamWaitEvent(a.cout, done[k], 0);
     if ((e = cudaMemcpyAsync(h_out[i], dout[k], hbytes, cudaMemcpyDeviceToHost, a.cout)) != cudaSuccess)
       return cuda_fail(e, "q4_encoder_pipeline: D2H");
-    cudaEventRecord(a.out_free[k], a.cout);
+    cudaEventRecord(out_free[k], a.cout);
   }
   // the caller's stream completes after the last download
-  cudaStreamWaitEvent(s, a.out_free[(nbatch - 1) & 1], 0);
+  cudaStreamWaitEvent(s, out_free[(nbatch - 1) & 1], 0);
   e = cudaGetLastError();
   return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_encoder_pipeline");
 }

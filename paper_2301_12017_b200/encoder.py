@@ -29,16 +29,16 @@ class W4A4Encoder:
         self.L = len(self.weights)
         self._lw = (LayerWeights * self.L)(*[ops.layer_weights(w) for w in self.weights])
         self._lc = ops.layer_cfg(self.cfg)
-        self._ws = None
-        self._ws_shape = None
+        self._ws = {}  # (B, S) -> workspace; kept alive: a captured graph holds raw pointers into it
         self.graph = None
+        self._graph_key = None
 
     def workspace(self, B: int, S: int) -> torch.Tensor:
-        if self._ws_shape != (B, S):
+        ws = self._ws.get((B, S))
+        if ws is None:
             n = self._ws_fn(C.byref(self._lc), B, S)
-            self._ws = torch.zeros(max(n, 1), dtype=torch.uint8, device=self.device)
-            self._ws_shape = (B, S)
-        return self._ws
+            ws = self._ws[(B, S)] = torch.zeros(max(n, 1), dtype=torch.uint8, device=self.device)
+        return ws
 
     def forward(self, h_in: torch.Tensor, h_out: torch.Tensor, B: int, S: int):
         """h_in / h_out: fp16 [B*S, hidden], CUDA tensors or (pinned) CPU tensors -- with
@@ -58,13 +58,17 @@ class W4A4Encoder:
             raise ValueError("serve(): the pipelined entry runs the W4A4 stack")
         if len(h_in) != len(h_out):
             raise ValueError("serve(): h_in and h_out lengths differ")
-        n = lib().q4_encoder_pipeline_workspace(C.byref(self._lc), B, S)
-        if getattr(self, "_pws", None) is None or self._pws.numel() < n:
-            self._pws = torch.zeros(max(n, 1), dtype=torch.uint8, device=self.device)
+        # one zero-filled workspace per shape (the row-epilogue counters sit at M-dependent offsets)
+        pws = getattr(self, "_pws", {})
+        self._pws = pws
+        if (B, S) not in pws:
+            n = lib().q4_encoder_pipeline_workspace(C.byref(self._lc), B, S)
+            pws[(B, S)] = torch.zeros(max(n, 1), dtype=torch.uint8, device=self.device)
+        ws = pws[(B, S)]
         pin = (C.c_void_p * len(h_in))(*[t.data_ptr() for t in h_in])
         pout = (C.c_void_p * len(h_out))(*[t.data_ptr() for t in h_out])
         check(lib().q4_encoder_pipeline(C.byref(self._lc), self._lw, self.L, B, S, pin, pout, len(h_in),
-                                        C.c_void_p(self._pws.data_ptr()), self._pws.numel(),
+                                        C.c_void_p(ws.data_ptr()), ws.numel(),
                                         C.c_void_p(torch.cuda.current_stream().cuda_stream)))
         return h_out
 
@@ -81,9 +85,13 @@ class W4A4Encoder:
         with torch.cuda.graph(g):
             self.forward(h_in, h_out, B, S)
         self.graph = g
+        # the graph replays into this shape's workspace and these buffers: keep them alive
+        self._graph_key = (B, S, h_in, h_out)
         return g
 
     def replay(self):
+        if self.graph is None:
+            raise RuntimeError("replay(): no graph captured (call capture() first)")
         self.graph.replay()
 
 

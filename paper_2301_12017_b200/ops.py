@@ -274,6 +274,13 @@ def quantize_layer(params: dict, device="cuda", prepack: bool = True, bits: int 
     return w
 
 
+def encoder_layer_workspace_bytes(cfg: dict, B: int, S: int, bits: int = 4) -> int:
+    """q4_encoder_layer_workspace (bits=8: the W8A8 layer's)."""
+    lc = layer_cfg(cfg)
+    fn = lib().q4_encoder_layer_w8a8_workspace if bits == 8 else lib().q4_encoder_layer_workspace
+    return int(fn(C.byref(lc), B, S))
+
+
 def encoder_layer(cfg: dict, w: dict, B: int, S: int, h_in, hq_in, hs_in, taps: bool = False,
                   workspace=None, bits: int = 4):
     """a8: one post-LN BERT layer (qall).  Returns dict(h_out, hq_out, hs_out[, taps...]).

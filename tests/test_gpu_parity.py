@@ -220,6 +220,23 @@ def test_attention(q4, B, S, H):
     assert np.array_equal(host(codes), c2) and np.array_equal(host(scales), s2)
 
 
+@pytest.mark.parametrize("B,S,H", [(160, 128, 16), (150, 77, 16), (160, 128, 12)])
+def test_attention_one_cta_per_sequence(q4, B, S, H):
+    """B >= 148: one CTA per sequence (no head cluster), the bench's launch shape -- the
+    cp.async-staged quantize tail and (h = 1024) its fast requant.  Every sequence's codes
+    and scales are checked bit-exactly against O-1 of the GPU's fp16 ctx; the fp16 ctx
+    against O-8 on a sample of sequences (first, last and inner)."""
+    qkv = synth.hidden(B * S, 3 * H * 64, f"aqb{B}_{S}_{H}")
+    codes, scales, ctx = q4.attention_f16_q4(dev(qkv), B, S, H, 64, f16_tap=True)
+    c = host(ctx)
+    c2, s2 = orc.quantize_rows(c)
+    assert np.array_equal(host(codes), c2) and np.array_equal(host(scales), s2)
+    for b in (0, 1, B // 2, B - 2, B - 1):
+        rows = slice(b * S, (b + 1) * S)
+        rctx, _, _ = orc.attention(qkv[rows], 1, S, H, 64)
+        assert_f16_close(c[rows], rctx, f"ctx seq {b}")
+
+
 # ------------------------------------------------------------------ a8 encoder layer
 def _layer_setup(cfg, B, S, seed="enc"):
     p = synth.layer_params(cfg, 0, seed)
@@ -329,7 +346,78 @@ def test_full_size_layer_sampled(q4):
         assert np.array_equal(T["acc_o"], orc.gemm_i32(T["ctx_codes"], W["wo"], S, h, h))
         assert np.array_equal(T["acc_1"], orc.gemm_i32(T["h1_codes"], W["w1"], S, f, h))
         assert np.array_equal(T["acc_2"], orc.gemm_i32(T["f_codes"], W["w2"], S, h, f))
+        # every requantized intermediate at the bench geometry: codes == O-1(GPU fp16) (R13),
+        # fp16 outputs within tolerance of the oracle step on the GPU's own inputs
+        c2, s2 = orc.quantize_rows(T["ctx"])
+        assert np.array_equal(T["ctx_codes"], c2) and np.array_equal(T["ctx_scales"], s2), f"ctx codes seq {bsel}"
+        r1 = orc.w4a4_linear(T["ctx_codes"], T["ctx_scales"], W["wo"], W["so"], S, h, h, orc.EPI_RESLN_Q4,
+                             bias=p["bo"], residual=x[rows], gamma=p["ln1_g"], beta=p["ln1_b"])
+        assert_f16_close(T["h1"], r1["f16"], f"h1 seq {bsel}")
+        c2, s2 = orc.quantize_rows(T["h1"])
+        assert np.array_equal(T["h1_codes"], c2) and np.array_equal(T["h1_scales"], s2), f"h1 codes seq {bsel}"
+        r2 = orc.w4a4_linear(T["h1_codes"], T["h1_scales"], W["w1"], W["s1"], S, f, h, orc.EPI_GELU_Q4, bias=p["b1"])
+        assert_f16_close(T["ffn1"], r2["f16"], f"ffn1 seq {bsel}")
+        c2, s2 = orc.quantize_rows(T["ffn1"])
+        assert np.array_equal(T["f_codes"], c2) and np.array_equal(T["f_scales"], s2), f"f codes seq {bsel}"
         r3 = orc.w4a4_linear(T["f_codes"], T["f_scales"], W["w2"], W["s2"], S, h, f, orc.EPI_RESLN_Q4,
+                             bias=p["b2"], residual=T["h1"], gamma=p["ln2_g"], beta=p["ln2_b"])
+        assert_f16_close(T["h_out"], r3["f16"], "h_out")
+        c2, s2 = orc.quantize_rows(T["h_out"])
+        assert np.array_equal(T["hq_out"], c2) and np.array_equal(T["hs_out"], s2)
+    # the bench runs the layer without taps (no fp16 MLP tap, no INT32 tap GEMMs): its outputs
+    # equal the tapped run's bit for bit, so the checks above cover the untapped launches too
+    o2 = q4.encoder_layer(cfg, w, B, S, dev(x), xq, xs, taps=False)
+    for k in ("h_out", "hq_out", "hs_out"):
+        assert torch.equal(o2[k], out[k]), k
+
+
+@pytest.mark.parametrize("kind", ["pair", "1cta"])
+def test_full_size_i32_production_mainloops(q4, kind):
+    """The accumulators the production epilogues consume, at the bench's M = 32768: the
+    prepacked-weight mainloop on CTA pairs (QKV's F16 launch) and on single CTAs (the row
+    epilogues), sampled 128-row slices bit-exact against O-4 (first, second, middle, last)."""
+    M, N, K = 32768, (3072 if kind == "pair" else 4096), 1024
+    a = synth.random_packed(M, K, f"fi_a{kind}", full_range=True)
+    w = synth.random_packed(N, K, f"fi_w{kind}", full_range=True)
+    sa, sw = synth.random_scales(M, "fi_sa"), synth.random_scales(N, "fi_sw")
+    wd = dev(w)
+    ml = q4.MAINLOOP_TCGEN05_W8 if kind == "pair" else q4.MAINLOOP_TCGEN05_W8_1CTA
+    i32 = host(q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_I32, w_i8=q4.prepack_weights(wd),
+                              mainloop=ml)["i32"])
+    for m0 in (0, 128, 256, M // 2 + 128, M - 256, M - 128):
+        rows = slice(m0, m0 + 128)
+        assert np.array_equal(i32[rows], orc.gemm_i32(a[rows], w, 128, N, K)), m0
+
+
+@pytest.mark.parametrize("hidden,ffn", [(768, 1024), (1024, 512), (768, 3072)])
+def test_encoder_layer_odd_ffn(q4, hidden, ffn):
+    """Layers whose N = hidden (RESLN) and N = ffn (GELU) row-epilogue launches share one
+    workspace with n-tile counts that are not in the BERT ratio (ffn < hidden, ffn/hidden <
+    1.5): teacher-forced parity of every step, at a size with several m-blocks per CTA."""
+    cfg = {"hidden": hidden, "heads": hidden // 64, "head_dim": 64, "ffn": ffn, "ln_eps": 1e-12}
+    B, S = 8, 128
+    M, h, f = B * S, hidden, ffn
+    p = synth.layer_params(cfg, 0, f"odd{hidden}_{ffn}")
+    x = synth.hidden(M, h, f"odd_x{hidden}")
+    w = q4.quantize_layer(p)
+    xq, xs = q4.quantize_rows(dev(x))
+    for rep in range(2):  # the second call reuses the workspace the first one left
+        ws = torch.zeros(q4.encoder_layer_workspace_bytes(cfg, B, S), dtype=torch.uint8, device="cuda") \
+            if rep == 0 else ws
+        out = q4.encoder_layer(cfg, w, B, S, dev(x), xq, xs, taps=True, workspace=ws)
+        T = {k: host(v) for k, v in out.items()}
+        W = {k: host(v) for k, v in w.items()}
+        r1 = orc.w4a4_linear(T["ctx_codes"], T["ctx_scales"], W["wo"], W["so"], M, h, h, orc.EPI_RESLN_Q4,
+                             bias=p["bo"], residual=x, gamma=p["ln1_g"], beta=p["ln1_b"])
+        assert_f16_close(T["h1"], r1["f16"], "h1")
+        c2, s2 = orc.quantize_rows(T["h1"])
+        assert np.array_equal(T["h1_codes"], c2) and np.array_equal(T["h1_scales"], s2)
+        assert np.array_equal(T["acc_1"], orc.gemm_i32(T["h1_codes"], W["w1"], M, f, h))
+        r2 = orc.w4a4_linear(T["h1_codes"], T["h1_scales"], W["w1"], W["s1"], M, f, h, orc.EPI_GELU_Q4, bias=p["b1"])
+        assert_f16_close(T["ffn1"], r2["f16"], "ffn1")
+        c2, s2 = orc.quantize_rows(T["ffn1"])
+        assert np.array_equal(T["f_codes"], c2) and np.array_equal(T["f_scales"], s2)
+        r3 = orc.w4a4_linear(T["f_codes"], T["f_scales"], W["w2"], W["s2"], M, h, f, orc.EPI_RESLN_Q4,
                              bias=p["b2"], residual=T["h1"], gamma=p["ln2_g"], beta=p["ln2_b"])
         assert_f16_close(T["h_out"], r3["f16"], "h_out")
         c2, s2 = orc.quantize_rows(T["h_out"])
@@ -368,6 +456,11 @@ def test_quantize_exhaustive_fp16_pairs(q4):
         ref = np.rint((np.float32(7.0) * X.astype(np.float32)) / a).astype(np.int64)
         mask = np.arange(width)[None, :] <= idx[:, None]
         assert np.array_equal(q[mask], ref[mask]), f"chunk {s}"
+        assert np.array_equal(host(sc), allpos[idx].astype(np.float32) / np.float32(7))
+        # the negated half: -x with the same amax (round half to even is odd-symmetric)
+        c, sc = q4.quantize_rows(dev(-X))
+        qn = orc.unpack_int4(host(c), width).astype(np.int64)
+        assert np.array_equal(qn[mask], -ref[mask]), f"chunk {s} (negated)"
         assert np.array_equal(host(sc), allpos[idx].astype(np.float32) / np.float32(7))
 
 

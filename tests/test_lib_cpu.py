@@ -40,6 +40,18 @@ def test_version(L):
     assert b"sm_100a" in L.q4_version()
 
 
+def test_shipped_library_has_no_profiling_knobs(L):
+    """The profiling environment knobs (skip TMA / unpack / MMA / epilogue math, zero codes,
+    trace stamps, tile / pair overrides) exist only in the -DQ4_PROFILING build: the shipped
+    libq4.so does not even contain their names, so no stray variable can change its results."""
+    from paper_2301_12017_b200 import _lib
+    blob = open(_lib.LIB_PATH if not os.environ.get("Q4_LIB_PATH") else
+                os.path.join(ROOT, "paper_2301_12017_b200", "libq4.so"), "rb").read()
+    for k in (b"Q4_DEBUG_SKIP", b"Q4_TRACE", b"Q4_PAIR", b"Q4_TN", b"Q4_NO_PDL", b"Q4_ATTN_DBG",
+              b"Q4_ATTN_LEGACY"):
+        assert k not in blob, k
+
+
 def _dummy(n=64):
     buf = (C.c_uint8 * (n + 64))()
     a = C.addressof(buf)
