@@ -1,11 +1,16 @@
 #!/usr/bin/env python
 """bench.py -- W4A4 BERT encoder throughput on B200 (BASELINE.json configs[3]):
-BERT-large, 24 layers, batch 256 per GPU, seq 128, all four linears W4A4 ("qall"),
-batch-sharded data parallel over N GPUs (weak scaling: each rank runs its own 256
-sequences; no collective in the data path).
+BERT-large, 24 layers, global batch 256, seq 128, all four linears W4A4 ("qall"),
+batch-sharded data parallel over N GPUs (strong scaling at the fixed global
+batch of 256 -- rank r runs sequences [r*256/N, (r+1)*256/N) -- with weak scaling, 256
+sequences per GPU, measured as a secondary figure; no collective in the data path beyond
+the NCCL all-gather of the outputs).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   torchrun --nproc-per-node N ... bench.py --gpus N ...
+
+With --gpus N > 1 and no torchrun environment, bench.py launches itself under
+torch.distributed.run with N ranks (127.0.0.1); under torchrun, WORLD_SIZE must equal N.
 
 One step = one pass of the whole hot path: initial activation
 quantize + 24 x [QKV W4A4 GEMM, FP16 attention + ctx quantize, attn-out W4A4 GEMM +
@@ -36,7 +41,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="large", choices=["base", "large"])
-    ap.add_argument("--batch", type=int, default=256, help="sequences per GPU")
+    ap.add_argument("--batch", type=int, default=256,
+                    help="global batch (strong scaling) or sequences per GPU (--scaling weak)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1: fixed global batch (strong, SURVEY 8(e) primary) or fixed per-GPU batch")
     ap.add_argument("--seq", type=int, default=128)
     ap.add_argument("--layers", type=int, default=0, help="0 = the model's own depth")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -44,7 +52,20 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip latency / GEMM side measurements")
     ap.add_argument("--gather", default="cls", choices=["cls", "full", "none"],
                     help="N>1: NCCL all-gather of the outputs inside every timed step (SURVEY 8(e))")
+    ap.add_argument("--oracle-worker", default=None, help=argparse.SUPPRESS)
     return ap.parse_args()
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 without a torchrun environment: re-launch this script as N ranks."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -135,25 +156,83 @@ def attention_work(B, S, H, d=64):
 _ORACLE_W = {}
 
 
-def oracle_sample(cfg, n_seq, S, threads=0):
-    """Time the CPU oracle (as it stands) on one encoder layer over n_seq sequences.
-    Weight generation / quantization (offline in the product path too) is not timed."""
-    import numpy as np
-    import oracle as orc
-    from paper_2301_12017_b200 import synth
-    key = (cfg["hidden"], cfg["ffn"])
+def _oracle_layer_weights(orc, synth, cfg, layer=0, threads=0):
+    key = (cfg["hidden"], cfg["ffn"], layer)
     if key not in _ORACLE_W:
-        p = synth.layer_params(cfg, 0, "bert")
+        p = synth.layer_params(cfg, layer, "bert")
         w = dict(p)
         for k in ("wqkv", "wo", "w1", "w2"):
             w[k], w["s" + k[1:]] = orc.quantize_rows(p[k], threads=threads)
         _ORACLE_W[key] = w
-    w = _ORACLE_W[key]
+    return _ORACLE_W[key]
+
+
+def oracle_sample(cfg, n_seq, S, threads=0, layers=1):
+    """Time the CPU oracle (as it stands) on `layers` encoder layers over n_seq sequences:
+    the initial quantize + L x O-9.  Weight generation / quantization (offline in the
+    product path too) is not timed."""
+    import numpy as np
+    import oracle as orc
+    from paper_2301_12017_b200 import synth
+    ws = [_oracle_layer_weights(orc, synth, cfg, l, threads) for l in range(layers)]
     x = np.concatenate([synth.hidden(S, cfg["hidden"], "input", b) for b in range(n_seq)])
     t0 = time.perf_counter()
     xq, xs = orc.quantize_rows(x, threads=threads)
-    orc.encoder_layer(cfg, w, n_seq, S, x, xq, xs, threads=threads)
+    for w in ws:
+        o = orc.encoder_layer(cfg, w, n_seq, S, x, xq, xs, threads=threads)
+        x, xq, xs = o["h_out"], o["hq_out"], o["hs_out"]
     return time.perf_counter() - t0
+
+
+def oracle_linear_sample(M, N, K, threads=0):
+    """BASELINE configs[0]: one W4A4 linear (F16 epilogue) through the oracle."""
+    import oracle as orc
+    from paper_2301_12017_b200 import synth
+    x = synth.hidden(M, K, "c1_x")
+    w = synth.layer_params(synth.BERT["base"], 0, "bert")["wo"]
+    wc, wsc = orc.quantize_rows(w, threads=threads)
+    t0 = time.perf_counter()
+    xc, xsc = orc.quantize_rows(x, threads=threads)
+    orc.w4a4_linear(xc, xsc, wc, wsc, M, N, K, orc.EPI_F16, threads=threads)
+    return time.perf_counter() - t0
+
+
+def oracle_worker(spec: str) -> int:
+    """Child process of the cpu_baseline leg: time the oracle, print one JSON object.
+    Runs apart from the product process, so the GPU arm never loads liboracle.so."""
+    from paper_2301_12017_b200 import synth
+    sp = json.loads(spec)
+    out = {}
+    large, base = dict(synth.BERT["large"]), dict(synth.BERT["base"])
+    th_all = cpu_cores()  # explicit: torchrun exports OMP_NUM_THREADS=1
+    # BASELINE configs[3] slice (SURVEY 8(d)): one BERT-large layer over 16 sequences (M = 2048),
+    # all host threads; and a 1-thread run on a 2-sequence slice
+    t = [oracle_sample(large, 16, 128, th_all) for _ in range(sp.get("reps", 2))]
+    out["large_layer_m2048_s"] = statistics.median(t)
+    out["large_layer_m256_1thread_s"] = oracle_sample(large, 2, 128, 1)
+    if sp.get("configs", True):
+        # configs[0..2] timed in full: linear M=128 K=N=768; BERT-base layer bs 1; 12 layers bs 1
+        out["c1_linear_m128_s"] = statistics.median(oracle_linear_sample(128, 768, 768) for _ in range(5))
+        out["c2_base_layer_bs1_s"] = statistics.median(oracle_sample(base, 1, 128, th_all) for _ in range(5))
+        out["c3_base_12layer_bs1_s"] = statistics.median(oracle_sample(base, 1, 128, th_all, 12) for _ in range(2))
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def cpu_baseline_subprocess(L: int, reps: int = 2):
+    """cpu_baseline of our arm (rank 0, N=1): the oracle timed in a child process."""
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-worker",
+                        json.dumps({"reps": reps})], capture_output=True, text=True, timeout=600)
+    if r.returncode != 0:
+        raise RuntimeError(f"oracle worker failed: {r.stderr[-2000:]}")
+    o = json.loads(r.stdout.strip().splitlines()[-1])
+    t = o["large_layer_m2048_s"]
+    return {"value": 16 / (t * L), "unit": "seq/s", "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"1 BERT-large layer x 16 seq x 128 tok (M = 2048, one slice of the workload), "
+                      f"median of {reps}, all host threads, extrapolated x{L} layers (x16 slices = the "
+                      f"256-seq batch at the same seq/s)",
+            "one_thread_seq_per_s": 2 / (o["large_layer_m256_1thread_s"] * L),
+            "configs_full_s": {k: v for k, v in o.items() if k.startswith("c")}}
 
 
 def cpu_cores():
@@ -171,20 +250,22 @@ def run_reference(args):
     cfg = dict(synth.BERT[args.model])
     L = args.layers or cfg["layers"]
     cores = cpu_cores()
-    n_seq = 1
+    n_seq = 16  # one M = 2048 slice of the batch per step
     times = []
     for i in range(args.warmup + args.steps):
-        t = oracle_sample(cfg, n_seq, args.seq)
+        t = oracle_sample(cfg, n_seq, args.seq, threads=cores)  # explicit: torchrun sets OMP_NUM_THREADS=1
         if i >= args.warmup:
             times.append(t)
     t = statistics.median(times)
     value = n_seq / (t * L)  # seq/s of the full L-layer encoder (layers are identical work)
-    sample = f"1 {args.model} encoder layer x {n_seq} seq x {args.seq} tok per step, extrapolated x{L} layers"
+    sample = (f"1 {args.model} encoder layer x {n_seq} seq x {args.seq} tok (M = {n_seq * args.seq}) per step, "
+              f"all host threads, extrapolated x{L} layers")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "seq/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64 (CPU oracle)", "data": "synthetic",
+            "scaling": args.scaling if args.gpus > 1 else "strong", "vs_baseline": None,
+            "dtype": "int64/f64 (CPU oracle)", "data": "synthetic",
             "config": {"workload": WORKLOAD, "model": f"bert-{args.model}", "layers": L,
-                       "batch_per_gpu": args.batch, "seq_len": args.seq},
+                       "global_batch": args.batch, "seq_len": args.seq},
             "cpu_baseline": {"value": value, "unit": "seq/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "seq/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -194,6 +275,10 @@ def run_reference(args):
 # ----------------------------------------------------------------------------- our arm
 def main():
     args = parse()
+    if args.oracle_worker is not None:
+        return oracle_worker(args.oracle_worker)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     import numpy as np
@@ -208,6 +293,8 @@ def main():
     rank, world, local = qd.env_ranks()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     N = world
@@ -218,14 +305,16 @@ def main():
 
     cfg = dict(synth.BERT[args.model])
     L = args.layers or cfg["layers"]
-    B, S, h = args.batch, args.seq, cfg["hidden"]
+    S, h = args.seq, cfg["hidden"]
+    GB = args.batch if args.scaling == "strong" else args.batch * N  # global batch
+    if GB % N:
+        raise SystemExit(f"bench.py: global batch {GB} does not split evenly over {N} ranks")
+    start, B = qd.shard(GB, rank, N)  # this rank's contiguous slice of the global batch
     M = B * S
     layers = [synth.layer_params(cfg, l, "bert") for l in range(L)]
     enc = q4.W4A4Encoder(cfg, layers, device=dev)
     del layers
-    # this rank's shard of the global batch (B sequences per GPU, weak scaling)
-    start, count = qd.shard(B * N, rank, N)
-    x = np.concatenate([synth.hidden(S, h, "input", b) for b in range(start, start + count)])
+    x = np.concatenate([synth.hidden(S, h, "input", b) for b in range(start, start + B)])
     xd = torch.from_numpy(x).to(dev)
     out = torch.empty_like(xd)
 
@@ -264,7 +353,7 @@ def main():
     total_ms = ev[0].elapsed_time(ev[-1])
     ms_per_step = max_over_ranks(total_ms / args.steps)
     p50 = max_over_ranks(statistics.median(step_ms))
-    value = N * B / (ms_per_step / 1e3)
+    value = GB / (ms_per_step / 1e3)
     clocks = clk.summary()
     gather_info = None
     if gather is not None:
@@ -318,10 +407,10 @@ def main():
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
         ok = ok and torch.equal(os_h[(args.steps - 1) % 2], out.cpu())
-        e2e = {"value": N * B / (e2e_ms / 1e3), "unit": "seq/s", "h2d_bytes_per_step": M * h * 2,
+        e2e = {"value": GB / (e2e_ms / 1e3), "unit": "seq/s", "h2d_bytes_per_step": M * h * 2,
                "d2h_bytes_per_step": M * h * 2, "ms_per_step": e2e_ms, "matches_device_path": ok,
                "api": "W4A4Encoder.serve -> q4_encoder_pipeline (copies overlapped across steps)",
-               "serial_ms_per_step": serial_ms, "serial_value": N * B / (serial_ms / 1e3)}
+               "serial_ms_per_step": serial_ms, "serial_value": GB / (serial_ms / 1e3)}
 
     # ------------------------------------------------------------------ per-kernel breakdown
     # One instrumented forward: the same launches as the graph, issued one by one with CUDA
@@ -395,37 +484,92 @@ def main():
     extras = {}
     if not args.no_extras and rank == 0:
         extras = side_measurements(q4, synth, torch, np, dev, args)
+        if N == 1:
+            extras["strong_scaling_model"] = strong_scaling_model(enc, synth, torch, np, dev, args, ms_per_step)
+
+    # ------------------------------------------------------------------ weak scaling (N > 1, secondary)
+    weak = None
+    if N > 1 and args.scaling == "strong":
+        # 256 sequences per rank (the global batch grows with N): same graph at M = 256 * S
+        Bw = args.batch
+        sw0, _ = qd.shard(Bw * N, rank, N)
+        xw = torch.from_numpy(np.concatenate([synth.hidden(S, h, "input", b) for b in range(sw0, sw0 + Bw)])).to(dev)
+        ow = torch.empty_like(xw)
+        encw = enc.sibling()
+        encw.capture(xw, ow, Bw, S)
+        gw = qd.OutputGather(Bw, S, h, args.gather, dev) if args.gather != "none" else None
+        for _ in range(args.warmup):
+            encw.replay()
+            if gw is not None:
+                gw(ow)
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            encw.replay()
+            if gw is not None:
+                gw(ow)
+        b.record(stream)
+        torch.cuda.synchronize()
+        wms = max_over_ranks(a.elapsed_time(b) / args.steps)
+        weak = {"value": Bw * N / (wms / 1e3), "unit": "seq/s", "ms_per_step": wms, "batch_per_gpu": Bw,
+                "global_batch": Bw * N}
+        del encw, xw, ow, gw
 
     # ------------------------------------------------------------------ CPU baseline (rank 0, N=1)
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
-        n_seq = 1
-        t1 = oracle_sample(cfg, n_seq, S)
-        reps = max(1, min(8, int(15.0 / max(t1, 1e-3))))  # ~15 s of CPU work
-        ts = [oracle_sample(cfg, n_seq, S) for _ in range(reps)]
-        t = statistics.median(ts)
-        cpu = {"value": n_seq / (t * L), "unit": "seq/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": f"1 {args.model} layer x {n_seq} seq x {S} tok, median of {reps}, extrapolated x{L} layers"}
+        cpu = cpu_baseline_subprocess(L)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "seq/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "p50_ms": p50, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int4 (W4A4, s8 tensor-core MMA, s32 acc)",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int4 (W4A4, s8 tensor-core MMA, s32 acc)",
             "data": "synthetic (seeded, random-init weights)",
             "config": {"workload": WORKLOAD, "model": f"bert-{args.model}", "layers": L, "batch_per_gpu": B,
-                       "global_batch": B * N, "seq_len": S, "parallelism": f"dp{N} (batch-sharded replicas" + (
+                       "global_batch": GB, "seq_len": S, "parallelism": f"dp{N} (batch-sharded replicas" + (
                            f", NCCL all-gather of the {args.gather} outputs per step)" if gather is not None else ", no collective)"),
                        "l2": f"no flush: per-step working set {(M * h * 2 * 6 + M * cfg['ffn'] / 2) / 1e9:.2f} GB "
                              f"of activations + {sum(v.numel() for w in enc.weights for v in w.values()) / 1e6:.0f} MB "
                              f"weights >> 126 MB L2", "cuda_graph": True},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks, "gather": gather_info, "kernels": breakdown, "extras": extras, "lib": q4.version(),
+            "clocks": clocks, "gather": gather_info, "weak_scaling": weak, "kernels": breakdown, "extras": extras, "lib": q4.version(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def strong_scaling_model(enc, synth, torch, np, dev, args, ms_n1):
+    """SURVEY 8(e) on one GPU: the per-rank step of an N-way strong-scaled run is this model at
+    batch 256/N (M = 16384 / 8192 / 4096).  Predicted N-GPU seq/s = 256 / t(256/N), before
+    the [CLS] gather (0.5 MB; NCCL is not measurable on one GPU)."""
+    S, h = args.seq, enc.cfg["hidden"]
+    stream = torch.cuda.current_stream()
+    out = {"n1_ms": ms_n1}
+    for n in (2, 4, 8):
+        B = args.batch // n
+        x = torch.from_numpy(np.concatenate([synth.hidden(S, h, "input", b) for b in range(B)])).to(dev)
+        o = torch.empty_like(x)
+        e = enc.sibling()
+        e.capture(x, o, B, S)
+        for _ in range(5):
+            e.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(20):
+            e.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) / 20
+        out[f"n{n}"] = {"batch_per_gpu": B, "M": B * S, "ms": t, "pred_seq_per_s": args.batch / (t * 1e-3),
+                        "pred_efficiency": ms_n1 / (n * t)}
+        del e, x, o
+    return out
 
 
 def side_measurements(q4, synth, torch, np, dev, args):

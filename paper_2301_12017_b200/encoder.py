@@ -33,6 +33,15 @@ class W4A4Encoder:
         self.graph = None
         self._graph_key = None
 
+    def sibling(self):
+        """A second encoder over the same device weights, with its own workspaces and graph
+        (e.g. the same model captured at another batch size)."""
+        other = object.__new__(type(self))
+        other.__dict__.update(self.__dict__)
+        other._ws, other.graph, other._graph_key = {}, None, None
+        other._pws = {}
+        return other
+
     def workspace(self, B: int, S: int) -> torch.Tensor:
         ws = self._ws.get((B, S))
         if ws is None:

@@ -104,3 +104,45 @@ def test_output_gather_single_process():
     assert torch.equal(qd.OutputGather(B, S, h, "cls")(x), x[::S])
     with pytest.raises(ValueError):
         qd.OutputGather(B, S, h, "rows")
+
+
+def _strong_worker(rank, world, port, q):
+    """bench.py's strong-scaling data path with a stub forward: global batch GB split over the
+    ranks (qd.shard), a per-sequence forward (mixes tokens within a sequence, so a shard that
+    split a sequence or misordered them would show), the [CLS] / full gather in rank order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        GB, S, h = 8, 4, 8
+        start, B = qd.shard(GB, rank, world)
+        x = torch.from_numpy(np.concatenate([synth.hidden(S, h, "input", b) for b in range(start, start + B)]))
+        y = _stub_forward(x, B, S, h)
+        q.put((rank, {m: qd.OutputGather(B, S, h, m)(y).clone().numpy() for m in ("cls", "full")},
+                  qd.max_over_ranks(float(B))))
+    finally:
+        dist.destroy_process_group()
+
+
+def _stub_forward(x, B, S, h):
+    xs = x.float().view(B, S, h)
+    return (xs.cumsum(1) * 0.5 + xs.mean(1, keepdim=True)).half().view(B * S, h)
+
+
+def test_two_rank_gloo_strong_scaling_stub_forward():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_strong_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    GB, S, h = 8, 4, 8
+    x = torch.from_numpy(np.concatenate([synth.hidden(S, h, "input", b) for b in range(GB)]))
+    ref = _stub_forward(x, GB, S, h).numpy()
+    for _, got, m in res:
+        assert np.array_equal(got["full"], ref)  # sharded + gathered == one process, whole batch
+        assert np.array_equal(got["cls"], ref[::S])
+        assert m == GB // world
