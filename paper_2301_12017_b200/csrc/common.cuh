@@ -472,4 +472,61 @@ Q4_DEV float2 gelu2(float2 t) {
   return ffma2(tn, qv, make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f)));
 }
 
+// tcgen05.wait::ld that also carries the loaded registers as operands, so no use of them can be
+// scheduled above the wait (software-pipelined TMEM loads)
+Q4_DEV void tmem_wait_ld_dep(uint32_t (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+               :
+               : "memory");
+}
+
+// GELU (erf form, reading R11) of 16 dequantized accumulators, t = acc sa sw + b, as 8 packed fp16
+// pairs.  GELU(x) = max(x,0) + tn Q(|x|)-ish with tn = -min(|x|, 4.5): Q(t) = exp(-t^2/2) R(u),
+// R a degree-6 polynomial in u = tn + 2.25 (scripts/fit_gelu.py 4.5 6: |err| <= 4.1e-5 against
+// the fp64 erf form in this float32 evaluation order, 1/24 of the 1e-3 absolute parity budget).
+// The 8 pairs advance in lockstep, one Horner step for all of them at a time: 8 independent
+// chains per step instead of the compiler's register-bound interleave.
+template <bool FACC>
+Q4_DEV void gelu16(const uint32_t (&v)[16], float2 sa2, const float* sw, const float* bs, uint32_t (&h)[8]) {
+  constexpr float HI = 4.5f, H2 = 2.25f;
+  const float4* pw = reinterpret_cast<const float4*>(sw);
+  const float4* pb = reinterpret_cast<const float4*>(bs);
+  float2 t[8], u[8], r[8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 w = pw[j], bb = pb[j];
+    const float2 a0 = FACC ? make_float2(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]))
+                           : make_float2((float)(int)v[4 * j], (float)(int)v[4 * j + 1]);
+    const float2 a1 = FACC ? make_float2(__uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]))
+                           : make_float2((float)(int)v[4 * j + 2], (float)(int)v[4 * j + 3]);
+    t[2 * j] = ffma2(fmul2(a0, sa2), make_float2(w.x, w.y), make_float2(bb.x, bb.y));
+    t[2 * j + 1] = ffma2(fmul2(a1, sa2), make_float2(w.z, w.w), make_float2(bb.z, bb.w));
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    u[j] = fadd2(make_float2(fmaxf(-fabsf(t[j].x), -HI), fmaxf(-fabsf(t[j].y), -HI)), f2(H2));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = ffma2(f2(2.548979828e-04f), u[j], f2(4.253684019e-04f));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = ffma2(r[j], u[j], f2(7.912631845e-04f));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = ffma2(r[j], u[j], f2(5.301531870e-03f));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = ffma2(r[j], u[j], f2(1.732770912e-02f));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = ffma2(r[j], u[j], f2(5.303432420e-02f));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = ffma2(r[j], u[j], f2(1.536411792e-01f));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 tn = fadd2(u[j], f2(-H2));
+    const float2 ea = fmul2(fmul2(tn, tn), f2(-0.72134752044448170f));  // -t^2/2 * log2(e)
+    const float2 qv = fmul2(make_float2(ex2_approx(ea.x), ex2_approx(ea.y)), r[j]);
+    const float2 y = ffma2(tn, qv, make_float2(fmaxf(t[j].x, 0.f), fmaxf(t[j].y, 0.f)));
+    h[j] = pack_half2(y.x, y.y);
+  }
+}
+
 }  // namespace q4

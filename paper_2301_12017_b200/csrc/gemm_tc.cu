@@ -39,6 +39,11 @@
 namespace q4 {
 
 enum { EPI_I32 = 0, EPI_F16 = 1, EPI_GELU_Q4 = 2, EPI_RESLN_Q4 = 3 };
+// GELU_Q4 epilogue variant: true = y parked in L2, TMEM released after pass A (gelu_epilogue);
+// false = y parked in TMEM, pass B from TMEM after the rendezvous (the shared row-epilogue path)
+#ifndef Q4_GELU_DECOUPLED
+#define Q4_GELU_DECOUPLED 0
+#endif
 
 struct TcParams {
   int M, N, K;
@@ -61,6 +66,7 @@ struct TcParams {
   float2* xstat;      // [mblocks][ntn][128] (mean, M2) partials
   float* xamax;       // [mblocks][ntn][128] max-abs partials
   unsigned* xcnt;     // [4][mblocks] arrival / departure counters (self-resetting; zero on entry)
+  __half* yscr;       // GELU_Q4 without an fp16 tap: [grid][2 groups][2 slots][128][TN] y parking (L2)
   int pair;           // CTA-pair (cta_group::2) mainloop: cluster of 2, CTA r owns m-block 2 c + r
   int dbg;            // profiling only (env Q4_DEBUG_SKIP): 1 skip TMA, 2 skip unpack, 4 skip MMA, 8 skip epilogue math
   unsigned long long* trace;  // profiling only (env Q4_TRACE): [grid][64 tiles][8] %globaltimer stamps
@@ -80,9 +86,9 @@ Q4_DEV unsigned long long gtimer() {
 template <int KIND> struct EpiCfg {
   static constexpr bool ROW = KIND == 2 || KIND == 3;
   static constexpr int EPW = ROW ? 8 : 4;
-  static constexpr int PAD = KIND == 3 ? 2 : 0;  // idle warps completing the mainloop warpgroup
+  static constexpr int PAD = (KIND == 3 || (KIND == 2 && Q4_GELU_DECOUPLED)) ? 2 : 0;  // idle warps completing the mainloop warpgroup
   static constexpr int THREADS = (6 + PAD + 2 * EPW) * 32;
-  static constexpr int MAINLOOP_REGS = 48, EPI_REGS = 96;
+  static constexpr int MAINLOOP_REGS = KIND == 2 ? 56 : 48, EPI_REGS = KIND == 2 ? 88 : 96;
 };
 
 // BI8: B (weights) arrives prepacked as int8 "16*q" in the MMA's K order
@@ -406,6 +412,198 @@ Q4_DEV void slab_load16(uint8_t* stg, const uint8_t* gbase, int row0, int r0, in
   }
 }
 
+// ------------------------------------------------------------------ GELU_Q4 epilogue
+// Decoupled from the accumulator (DESIGN.md 4.3 "GELU_Q4: y parked in L2"):
+//   pass A (thread = row, TMEM lane quarter): y = fp16(GELU(acc sa sw + b)) -> global (the
+//     fp16 tap if the caller asked for it, else a per-CTA L2 parking slot) through the swizzled
+//     slab; per-row partial max-abs.  The TMEM buffer is released right after pass A, so the
+//     MMA of tile t + 2 overlaps the rest of tile t's epilogue.
+//   publish the partials (red.release) -- no wait here;
+//   pass B of the group's PREVIOUS tile t - 2 (warp = 16 rows, lane = 8 columns of a row:
+//     coalesced y loads from L2 and coalesced code stores), whose exchange completed while
+//     pass A of tile t ran.  The group never idles in the rendezvous.
+// Two parking slots per group: y(t) is written before y(t - 2) is consumed.
+// Pass B of one tile (m-block pmb, n-block pnb): warp gw of the group codes rows
+// [16 gw, 16 gw + 16) of the tile; lane l holds columns [8 l, 8 l + 8) of a row (TN / 8 lanes).
+// `ys` is row 0 of the tile's y (ld `ldy` halves), written by this group's pass A.
+template <int TN, bool A8, bool H16>
+Q4_DEV void gelu_pass_b(const TcParams& p, int pmb, int pnb, const __half* ys, int ldy, int gw, int lane, int gbar,
+                        int GT, bool leader) {
+  const int ntn = p.ntn;
+  if (leader && !(p.dbg & 1024)) {  // rendezvous of m-block pmb (published one group cycle ago)
+    unsigned* cnt = p.xcnt + p.mblocks + pmb;
+    unsigned polls = 0;
+    while (ld_acquire_gpu(cnt) < (unsigned)ntn) {
+      __nanosleep(32);
+      if (++polls > (1u << 26)) __trap();
+    }
+    if (atomicAdd(cnt + 2 * (size_t)p.mblocks, 1u) == (unsigned)ntn - 1) {
+      cnt[0] = 0u;
+      cnt[2 * (size_t)p.mblocks] = 0u;
+    }
+  }
+  named_bar(gbar, GT);
+  if (p.dbg & 256) return;
+  const int r0 = gw * 16, row0 = pmb * 128 + r0;
+  const int nr = p.M - row0 < 16 ? p.M - row0 : 16;  // valid rows of this warp
+  const bool act = lane < TN / 8;  // lanes holding columns (all lanes take part in the shuffles)
+  // every L2 load of the warp is issued before the first use (one round trip): the 16 y rows
+  // (16 B per lane per row), then the ntn max-abs partials of the rows (lanes l and l ^ 16:
+  // row l % 16)
+  const uint4* yp = reinterpret_cast<const uint4*>(ys + (size_t)r0 * ldy) + lane;
+  const int ystep = ldy / 8;
+  uint4 y[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u)
+    if (act && u < nr) y[u] = __ldcg(yp + u * ystep);
+  float am = 0.f;
+  {
+    const float* xp = p.xamax + (size_t)pmb * ntn * 128 + r0 + (lane & 15);
+    for (int kk = lane >> 4; kk < ntn; kk += 2) am = fmaxf(am, __ldcg(xp + (size_t)kk * 128));
+    am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 16));
+  }
+  // lanes 0-15 derive their row's requant multiplier and scale (IEEE divisions) once
+  constexpr bool I8 = A8 && !H16;
+  constexpr float QMAX = I8 ? 127.0f : 7.0f;
+  const float rq_l = am > 0.f ? __fdiv_rn(QMAX, am) : 0.f;
+  if (pnb == 0 && lane < nr) p.out_scales[row0 + lane] = am > 0.f ? __fdiv_rn(am, QMAX) : 1.0f;
+  // rows whose codes take the exact path (clip, all-zero row)
+  const uint32_t exact = __ballot_sync(0xffffffffu, lane < 16 && (p.clip > 0.f || !(am > 0.f)));
+  uint8_t* cp = p.out_codes + (size_t)row0 * (I8 ? p.N : p.N / 2) + (I8 ? pnb * TN + 8 * lane : pnb * TN / 2 + 4 * lane);
+  const size_t cstep = I8 ? (size_t)p.N : (size_t)p.N / 2;
+  const float clip = p.clip;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const float amax = __shfl_sync(0xffffffffu, am, u);
+    const float rq = __shfl_sync(0xffffffffu, rq_l, u);
+    if (u >= nr) break;
+    if (!act) continue;
+    const uint32_t hk[4] = {y[u].x, y[u].y, y[u].z, y[u].w};
+    if constexpr (I8) {
+      *reinterpret_cast<uint2*>(cp + u * cstep) = requant8_i8(hk, amax, rq, clip);
+    } else {
+      float dm = 0.f;
+      uint32_t w = requant8_nofix(hk, rq, dm);
+      if (dm > 0.499998f || ((exact >> u) & 1u)) w = requant8(hk, amax, rq, clip);
+      *reinterpret_cast<uint32_t*>(cp + u * cstep) = w;
+    }
+  }
+}
+
+// Pass A's y slab (32 rows x 64 fp16, swizzled) -> global: this warp's RS rows from r_first;
+// `gq` is row 0 of the slab's 32 rows at the slab's column, `nvalid` the rows < M.
+template <int RS>
+Q4_DEV void slab_store_y(const uint8_t* stg, uint8_t* gq, int ldb, int r_first, int nvalid, int lane) {
+  const int c = lane & 7;
+  int r = r_first + (lane >> 3);
+  uint8_t* g = gq + r * ldb + c * 16;
+#pragma unroll
+  for (int i = 0; i < RS / 4; ++i, r += 4, g += 4 * ldb)
+    if (r < nvalid) *reinterpret_cast<uint4*>(g) = *reinterpret_cast<const uint4*>(stg + slab_off(r, c));
+}
+
+template <int TN, bool A8, bool H16>
+Q4_DEV void gelu_epilogue(const TcParams& p, TileIter& it, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
+                          uint8_t* stg, float4* rowp, const float* prm, int ew, int lane) {
+  constexpr int EPW = EpiCfg<EPI_GELU_Q4>::EPW, NS = EPW / 4, GT = EPW * 32;
+  constexpr int NSL = TN / 64, RS = 32 / NS;
+  const int grp = ew / EPW, sub = (ew >> 2) % NS, q = ew & 3, r = q * 32 + lane;
+  const int gw = ew % EPW;  // warp within the group
+  const int gbar = 1 + grp, pbar = 4 + grp * 4 + q;
+  const bool leader = gw == 0 && lane == 0;
+  const float clip = p.clip;
+  const bool tap = p.out_f16 != nullptr;
+  // y of a tile: the caller's fp16 tap, else this group's two L2 parking slots (alternating)
+  const int ldy = tap ? p.N : TN;
+  __half* const slot0 = tap ? nullptr : p.yscr + ((size_t)blockIdx.x * 2 + grp) * 2 * 128 * TN;
+  auto ybase = [&](int mb, int nb, uint32_t slot) -> __half* {
+    return tap ? p.out_f16 + (size_t)mb * 128 * p.N + nb * TN : slot0 + slot * (128 * TN);
+  };
+  auto slab_sync = [&]() {
+    if constexpr (NS > 1) named_bar(pbar, 32 * NS); else __syncwarp();
+  };
+  // profiling only (Q4_TRACE): per tile [0] acc wait start, [1] acc ready, [2] pass A done (TMEM
+  // released), [3] published, [4] pass B start, [6] pass B done
+  auto stamp = [&](uint32_t tc, int k) {
+    if (p.trace && leader && tc < 64) p.trace[((size_t)blockIdx.x * 64 + tc) * 8 + k] = gtimer();
+  };
+  uint32_t tcount = 0, slot = 0, ptc = 0;
+  int pmb = -1, pnb = 0, mb, nb;
+  while (it.next(mb, nb)) {
+    const uint32_t b = tcount & 1u;
+    if ((int)b != grp) { ++tcount; continue; }
+    const int m0 = mb * 128, gm = m0 + r;
+    const float sa = gm < p.M ? (H16 ? 1.0f : p.a_scales[gm] * (A8 ? 1.0f : 1.0f / 256.0f)) : 0.f;
+    const float2 sa2 = f2(sa);
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + b * TN + 32 * sub;
+    uint8_t* yq = reinterpret_cast<uint8_t*>(ybase(mb, nb, slot) + (size_t)(q * 32) * ldy);
+    const int qrows = p.M - m0 - q * 32;  // valid rows of this lane quarter (may exceed 32)
+    stamp(tcount, 0);
+    if (gw == 0) mbar_wait(&tfull[b], (tcount >> 1) & 1u);
+    named_bar(gbar, GT);
+    tc_fence_after();
+    stamp(tcount, 1);
+    // pass A: this side's 32-column chunk of each 64-column slab, as two 16-column pieces
+    __half2 hmax = __float2half2_rn(0.f);
+#pragma unroll 1
+    for (int k = 0; k < NSL; ++k) {
+#pragma unroll
+      for (int hp = 0; hp < 2; ++hp) {
+        const int col = 64 * k + 32 * sub + 16 * hp;
+        uint32_t v[16], h[8];
+        tmem_ld16(tbase + 64 * k + 16 * hp, v);
+        tmem_wait_ld_dep(v);
+        gelu16<H16>(v, sa2, prm + col, prm + TN + col, h);
+        if (clip > 0.f) {
+          const __half2 cl = __float2half2_rn(clip);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) hmax = __hmax2(hmax, __hmin2(__habs2(*reinterpret_cast<const __half2*>(&h[u])), cl));
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) hmax = __hmax2(hmax, __habs2(*reinterpret_cast<const __half2*>(&h[u])));
+        }
+        const int c16 = 4 * sub + 2 * hp;  // 16-byte chunk of the slab row
+        *reinterpret_cast<uint4*>(stg + slab_off(lane, c16)) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(stg + slab_off(lane, c16 + 1)) = make_uint4(h[4], h[5], h[6], h[7]);
+      }
+      slab_sync();
+      if (!(p.dbg & 512)) slab_store_y<RS>(stg, yq + 128 * k, 2 * ldy, RS * sub, qrows, lane);
+      slab_sync();
+    }
+    // the accumulator buffer is free: the MMA of tile tcount + 2 may start
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[b]);
+    stamp(tcount, 2);
+    float amax = fmaxf(__low2float(hmax), __high2float(hmax));
+    if constexpr (NS > 1) {
+      rowp[sub * 128 + r].z = amax;
+      named_bar(gbar, GT);
+      amax = fmaxf(rowp[r].z, rowp[128 + r].z);
+    }
+    if (sub == 0) p.xamax[((size_t)mb * p.ntn + nb) * 128 + r] = amax;
+    // publish: the group's partial stores (ordered by the bar.sync) become visible with the arrival
+    named_bar(gbar, GT);
+    if (leader) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.xcnt + p.mblocks + mb) : "memory");
+    stamp(tcount, 3);
+    if (pmb >= 0) {
+      stamp(ptc, 4);
+      gelu_pass_b<TN, A8, H16>(p, pmb, pnb, ybase(pmb, pnb, slot ^ 1u), ldy, gw, lane, gbar, GT, leader);
+      stamp(ptc, 6);
+    }
+    ptc = tcount;
+    pmb = mb;
+    pnb = nb;
+    slot ^= 1u;
+    ++tcount;
+  }
+  if (pmb >= 0) {
+    stamp(ptc, 4);
+    gelu_pass_b<TN, A8, H16>(p, pmb, pnb, ybase(pmb, pnb, slot ^ 1u), ldy, gw, lane, gbar, GT, leader);
+    stamp(ptc, 6);
+  }
+}
+
 // H16 (with A8, BI8): fp16 operands (the unquantized parts of a per-part quantization
 // strategy).  The byte-level staging is the A8 path unchanged (a 128-byte
 // k-block row = 64 fp16), the MMA is kind::f16 with fp32 accumulators, and the epilogue
@@ -702,6 +900,9 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     auto stamp = [&](int k) {
       if (tr && leader) tr[k] = gtimer();
     };
+    if constexpr (KIND == EPI_GELU_Q4 && Q4_GELU_DECOUPLED) {
+      gelu_epilogue<TN, A8, H16>(p, it, tmem, tfull, tempty, stg, rowp, prm, ew, lane);
+    } else
     while (it.next(mb, nb)) {
       const uint32_t b = tcount & 1u;
       if ((int)b != grp) { ++tcount; continue; }
@@ -882,7 +1083,13 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
                 h[2 * i4 + 1] = pack_half2(y1.x, y1.y);
               }
             } else {
-              dequant32<H16>(v, sa2, prm + 32 * j, prm + TN + 32 * j, h, true);
+              uint32_t v0[16], v1[16], h0[8], h1[8];
+#pragma unroll
+              for (int u = 0; u < 16; ++u) { v0[u] = v[u]; v1[u] = v[16 + u]; }
+              gelu16<H16>(v0, sa2, prm + 32 * j, prm + TN + 32 * j, h0);
+              gelu16<H16>(v1, sa2, prm + 32 * j + 16, prm + TN + 32 * j + 16, h1);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) { h[u] = h0[u]; h[8 + u] = h1[u]; }
             }
             if (clip > 0.f) {
               const __half2 cl = __float2half2_rn(clip);
@@ -1066,7 +1273,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.bias = g.bias; p.residual = g.residual; p.gamma = g.gamma; p.beta = g.beta;
   p.ln_eps = g.ln_eps; p.clip = g.clip;
   p.out_i32 = g.out_i32; p.out_f16 = g.out_f16; p.out_codes = g.out_codes; p.out_scales = g.out_scales;
-  p.xstat = nullptr; p.xamax = nullptr; p.xcnt = nullptr;
+  p.xstat = nullptr; p.xamax = nullptr; p.xcnt = nullptr; p.yscr = nullptr;
   static const int dbg = [] { const char* e = prof_env("Q4_DEBUG_SKIP"); return e ? atoi(e) : 0; }();
   p.dbg = dbg;
   p.trace = nullptr;
@@ -1086,7 +1293,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   if (p.groups > mwalk) p.groups = mwalk;
   const int grid = p.groups * p.ntn * (PAIR ? 2 : 1);
   if (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4) {
-    const size_t need = tc_workspace_bytes(g.M, g.N, TN);
+    const size_t need = tc_workspace_bytes(g.M, g.N, TN, KIND);
     if (!ws || ws_bytes < need) { *why = "workspace too small for the row-epilogue exchange"; return cudaErrorInvalidValue; }
     // counters first, at an offset that depends on M only: row-epilogue launches of the same M
     // and any N (a layer's RESLN N = hidden and GELU N = ffn) share one workspace, and one
@@ -1096,6 +1303,11 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     p.xcnt = reinterpret_cast<unsigned*>(w);
     p.xstat = reinterpret_cast<float2*>(w + cnt_bytes);
     p.xamax = reinterpret_cast<float*>(w + cnt_bytes + nslot * 8);
+    p.yscr = KIND == EPI_GELU_Q4 ? reinterpret_cast<__half*>(w + cnt_bytes + nslot * 12) : nullptr;
+    if (KIND == EPI_GELU_Q4 && (size_t)grid > tc_row_grid(g.M, g.N, TN)) {
+      *why = "row-epilogue grid larger than the workspace sizing assumed";
+      return cudaErrorInvalidValue;
+    }
   }
   note_launch();
   {
@@ -1208,10 +1420,21 @@ size_t tc_counter_bytes(int M) {
   return (4 * mblocks * sizeof(unsigned) + 255) & ~(size_t)255;
 }
 
-size_t tc_workspace_bytes(int M, int N, int TN) {
+// CTAs of a row-epilogue launch (the grid run_tc picks): groups of ntn co-resident CTAs
+size_t tc_row_grid(int M, int N, int TN) {
+  const size_t mblocks = (size_t)(M + 127) / 128, ntn = (size_t)N / TN;
+  size_t groups = ntn ? (size_t)num_sms() / ntn : 0;
+  if (groups > mblocks) groups = mblocks;
+  return groups * ntn;
+}
+
+size_t tc_workspace_bytes(int M, int N, int TN, int kind) {
   if (TN <= 0) return 0;
   const size_t mblocks = (size_t)(M + 127) / 128, ntn = (size_t)N / TN;
-  return tc_counter_bytes(M) + mblocks * ntn * 128 * 12;
+  size_t b = tc_counter_bytes(M) + mblocks * ntn * 128 * 12;
+  // GELU_Q4: two y parking slots per epilogue group (pass B of tile t runs after pass A of t + 2)
+  if (kind == EPI_GELU_Q4 && Q4_GELU_DECOUPLED) b += tc_row_grid(M, N, TN) * 4 * 128 * (size_t)TN * 2;
+  return b;
 }
 
 cudaError_t launch_w4a4_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {

@@ -83,7 +83,8 @@ cudaError_t launch_quantize_rows_i8(const __half* x, int64_t rows, int cols, int
 // Row epilogues (GELU_Q4 / RESLN_Q4) need `ws` of tc_workspace_bytes(M, N, tc_tile_n(...)).
 cudaError_t launch_w4a4_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why);
 int tc_tile_n(int M, int N, int kind);
-size_t tc_workspace_bytes(int M, int N, int TN);
+size_t tc_workspace_bytes(int M, int N, int TN, int kind);
+size_t tc_row_grid(int M, int N, int TN);  // CTAs of a 1-CTA row-epilogue launch
 size_t tc_counter_bytes(int M);  // the rendezvous counters at the start of a row-epilogue workspace
 cudaError_t launch_w4a4_legacy(const GemmArgs& g, bool s4, cudaStream_t s, const char** why);
 // i8: W8A8 baseline -- int8 ctx codes [B*S, h] with scale amax/127 instead of packed INT4

@@ -1,12 +1,19 @@
-"""Fit of the GELU tail polynomial used by gelu2() in csrc/common.cuh (offline tooling;
-not part of the product path).  GELU(x) = max(x,0) - |x| Q(|x|), Q(t) = exp(-t^2/2) R(t),
-R(v) a degree-8 polynomial in v = 2.75 - min(t, 5.5).  Weighted least squares on the GELU
-error, reweighted towards minimax; prints the coefficients and the max |error| of the
-float32 evaluation order the kernel uses against the fp64 erf form."""
+"""Fit of the GELU tail polynomials in csrc/common.cuh (offline tooling; not part of the
+product path).  GELU(x) = max(x,0) - |x| Q(|x|), Q(t) = exp(-t^2/2) R(t), R(v) a degree-DEG
+polynomial in v = HI/2 - min(t, HI).  Weighted least squares on the GELU error, reweighted
+towards minimax; prints the coefficients and the max |error| of the float32 evaluation order
+the kernel uses against the fp64 erf form.
+
+  python scripts/fit_gelu.py            # gelu16 (GELU_Q4 epilogue): HI 4.5, degree 6
+  python scripts/fit_gelu.py 5.5 8 old  # gelu2 (row-per-thread epilogues)"""
+import sys
+
 import numpy as np
 from scipy.special import erfc
 
-HI, DEG = 5.5, 8
+HI = float(sys.argv[1]) if len(sys.argv) > 1 else 4.5
+DEG = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+OLD = len(sys.argv) > 3  # gelu2: tn kept; gelu16: tn recovered as v - HI/2
 t = np.linspace(0, HI, 200001)
 R = 0.5 * erfc(t / np.sqrt(2)) * np.exp(t * t / 2)
 V = np.vander(HI / 2 - t, DEG + 1)
@@ -23,6 +30,8 @@ v = (tn + np.float32(HI / 2)).astype(np.float32)
 r = np.full_like(v, c32[0])
 for ci in c32[1:]:
     r = (r * v + ci).astype(np.float32)
+if not OLD:
+    tn = (v - np.float32(HI / 2)).astype(np.float32)
 ea = ((tn * tn).astype(np.float32) * np.float32(-0.72134752044448170)).astype(np.float32)
 q = (np.exp2(ea.astype(np.float64)).astype(np.float32) * r).astype(np.float32)
 y = (tn * q + np.maximum(x, 0)).astype(np.float32)
