@@ -68,6 +68,7 @@ struct TcParams {
   unsigned* xcnt;     // [4][mblocks] arrival / departure counters (self-resetting; zero on entry)
   __half* yscr;       // GELU_Q4 without an fp16 tap: [grid][2 groups][2 slots][128][TN] y parking (L2)
   int pair;           // CTA-pair (cta_group::2) mainloop: cluster of 2, CTA r owns m-block 2 c + r
+  int lin;            // linear tile schedule (R4): `groups` units walk the row-major tile order
   int dbg;            // profiling only (env Q4_DEBUG_SKIP): 1 skip TMA, 2 skip unpack, 4 skip MMA, 8 skip epilogue math
   unsigned long long* trace;  // profiling only (env Q4_TRACE): [grid][64 tiles][8] %globaltimer stamps
 };
@@ -83,12 +84,18 @@ Q4_DEV unsigned long long gtimer() {
 // so they form two aligned warpgroups) drop to
 // MAINLOOP_REGS and the 16 epilogue warps rise to EPI_REGS.  The pool is what the CTA was
 // launched with (768 threads x 80 = 61440): 8 x 48 + 16 x 96 = 1920 warp-registers x 32.
-template <int KIND> struct EpiCfg {
+// R4 (row epilogues on the CTA-pair mainloop): four 128-column TMEM accumulators drained by
+// four 4-warp groups (thread = row, all 128 columns of the tile), so four tiles are in flight
+// per CTA instead of two; the pair MMA (M = 256, N = 128) keeps the shared-memory traffic per
+// MAC of the 1-CTA N = 256 tile (each CTA stages half of B).
+template <int KIND, bool R4 = false> struct EpiCfg {
   static constexpr bool ROW = KIND == 2 || KIND == 3;
-  static constexpr int EPW = ROW ? 8 : 4;
-  static constexpr int PAD = (KIND == 3 || (KIND == 2 && Q4_GELU_DECOUPLED)) ? 2 : 0;  // idle warps completing the mainloop warpgroup
-  static constexpr int THREADS = (6 + PAD + 2 * EPW) * 32;
-  static constexpr int MAINLOOP_REGS = KIND == 2 ? 56 : 48, EPI_REGS = KIND == 2 ? 88 : 96;
+  static constexpr int NBUF = R4 ? 4 : 2;  // TMEM accumulator buffers = epilogue groups
+  static constexpr int EPW = R4 ? 4 : ROW ? 8 : 4;
+  static constexpr int PAD = (KIND == 3 || (KIND == 2 && (Q4_GELU_DECOUPLED || R4))) ? 2 : 0;  // idle warps completing the mainloop warpgroup
+  static constexpr int THREADS = (6 + PAD + NBUF * EPW) * 32;
+  static constexpr bool TIGHT = KIND == 2 && Q4_GELU_DECOUPLED && !R4;
+  static constexpr int MAINLOOP_REGS = TIGHT ? 56 : 48, EPI_REGS = TIGHT ? 88 : 96;
 };
 
 // BI8: B (weights) arrives prepacked as int8 "16*q" in the MMA's K order
@@ -99,7 +106,7 @@ template <int KIND> struct EpiCfg {
 // PAIR (with BI8): CTA-pair mainloop -- tcgen05.mma.cta_group::2 with M = 256; each CTA
 // stages its own 128 rows of A and half of the N tile of B, so the B stage halves and the
 // unpacked ring deepens to 4 stages.
-template <int TN, bool BI8, bool A8 = false, bool PAIR = false>
+template <int TN, bool BI8, bool A8 = false, bool PAIR = false, bool R4 = false>
 struct TcCfg {
   static constexpr int BM = 128, BK = 128;  // BK in int8 elements = 64 packed bytes
   static constexpr int SP = A8 ? 1 : BI8 ? 4 : 3, SU = PAIR ? 4 : BI8 ? 3 : 2;  // packed / unpacked smem stages
@@ -108,13 +115,15 @@ struct TcCfg {
   static constexpr int UN_STAGE = A_UN + B_UN, PK_STAGE = A_PK + B_PK;
   static constexpr int OFF_UN = 0;
   static constexpr int OFF_PK = SU * UN_STAGE;
-  static constexpr int OFF_STG = OFF_PK + SP * PK_STAGE;  // 8 warp pairs x 4 KB staging slabs
-  static constexpr int OFF_PRM = OFF_STG + 8 * 4096;      // [4][TN] fp32 column params
-  static constexpr int OFF_ROW = OFF_PRM + 4 * TN * 4;    // [2 groups][2 sides][128] float4 row partials
-  static constexpr int OFF_BAR = OFF_ROW + 2 * 2 * 128 * 16;
+  static constexpr int NSLAB = R4 ? 16 : 8;              // 4 KB staging slabs: per warp (R4) or warp pair
+  static constexpr int OFF_STG = OFF_PK + SP * PK_STAGE;
+  static constexpr int OFF_PRM = OFF_STG + NSLAB * 4096;  // [R4 ? 4 groups : 1][4][TN] fp32 column params
+  static constexpr int OFF_ROW = OFF_PRM + (R4 ? 4 : 1) * 4 * TN * 4;  // [2 groups][2 sides][128] float4 row partials
+  static constexpr int OFF_BAR = OFF_ROW + (R4 ? 0 : 2 * 2 * 128 * 16);
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int HW = TN / 2;  // columns per epilogue group
-  static constexpr int TMEM_COLS = 2 * TN <= 64 ? 64 : 2 * TN <= 128 ? 128 : 2 * TN <= 256 ? 256 : 512;
+  static constexpr int NBUF = R4 ? 4 : 2;
+  static constexpr int TMEM_COLS = NBUF * TN <= 64 ? 64 : NBUF * TN <= 128 ? 128 : NBUF * TN <= 256 ? 256 : 512;
+  static_assert(NBUF * TN <= 512, "TMEM");
   static_assert(TN % 32 == 0 && TN >= 32 && TN <= 256, "tile N");
   static_assert(SMEM <= 227 * 1024, "smem");
 };
@@ -126,17 +135,30 @@ struct TileIter {
   // staged once; row epilogues find the ntn CTAs of an m-block at the same step).
   // CTA pairs: cluster c = blockIdx.x / 2 plays the role of a CTA above over m-block pairs;
   // CTA r of the pair owns m-block 2 * pair + r (M % 256 == 0).
-  int cur, step, mblocks, rank, sub, pair;
+  // Linear schedule (R4): the `groups` units (pairs) take pair-tiles i = unit, unit + groups, ...
+  // in row-major (m-block pair, n-block) order, so the ntn tiles of an m-block run in the same
+  // or the next wave on consecutive units; every SM is used whatever ntn is.
+  int cur, step, mblocks, rank, sub, pair, lin, ntn;
   __device__ TileIter(const TcParams& p) {
     pair = p.pair;
+    lin = p.lin;
+    ntn = p.ntn;
     const int c = pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     sub = pair ? (int)(blockIdx.x & 1) : 0;
     mblocks = pair ? p.mblocks / 2 : p.mblocks;
-    rank = c % p.ntn;
-    cur = c / p.ntn;
+    rank = lin ? 0 : c % p.ntn;
+    cur = lin ? c : c / p.ntn;
     step = p.groups;
   }
   __device__ bool next(int& mb, int& nb) {
+    if (lin) {
+      if (cur >= mblocks * ntn) return false;
+      const int mp = cur / ntn;
+      nb = cur - mp * ntn;
+      mb = pair ? 2 * mp + sub : mp;
+      cur += step;
+      return true;
+    }
     if (cur >= mblocks) return false;
     mb = pair ? 2 * cur + sub : cur;
     nb = rank;
@@ -609,28 +631,32 @@ Q4_DEV void gelu_epilogue(const TcParams& p, TileIter& it, uint32_t tmem, uint64
 // k-block row = 64 fp16), the MMA is kind::f16 with fp32 accumulators, and the epilogue
 // reads the accumulator as fp32 with unit scales.
 template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false>
-__global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
+__global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>::THREADS, 1)
     w4a4_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
   static_assert(!A8 || BI8, "W8A8 takes int8 weights through the BI8 path");
   static_assert(!H16 || A8, "fp16 operands use the A8 staging");
-  static_assert(!PAIR || (BI8 && !H16 && KIND != EPI_GELU_Q4), "pair mainloop: int8 weights, F16/I32/RESLN");
-  // (RESLN instantiations compile but are not dispatched: measured slower)
-  using C = TcCfg<TN, BI8, A8, PAIR>;
+  static_assert(!PAIR || (BI8 && !H16), "pair mainloop: int8 weights");
+  // R4: row epilogues on the pair mainloop (four 128-column accumulators, linear schedule)
+  constexpr bool R4 = PAIR && (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4);
+  static_assert(!R4 || TN == 128, "R4 tiles are 256 x 128 per pair");
+  using E = EpiCfg<KIND, R4>;
+  using C = TcCfg<TN, BI8, A8, PAIR, R4>;
+  constexpr int NBUF = E::NBUF;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full_p = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* empty_p = full_p + C::SP;
   uint64_t* full_u = empty_p + C::SP;
   uint64_t* empty_u = full_u + C::SU;
-  uint64_t* tfull = empty_u + C::SU;   // [2]
-  uint64_t* tempty = tfull + 2;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty_u + C::SU;   // [NBUF]
+  uint64_t* tempty = tfull + NBUF;     // [NBUF]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (p.K + C::BK - 1) / C::BK;
   // Warp roles.  The issue arbiter favours higher warp ids, so the mainloop's critical
   // path (unpack, TMA producer, MMA issuer) sits above the epilogue warps.
-  constexpr int NE = 2 * EpiCfg<KIND>::EPW;  // epilogue warps 0 .. NE-1
+  constexpr int NE = NBUF * E::EPW;          // epilogue warps 0 .. NE-1
   constexpr int WU = NE;                     // unpack warps WU .. WU+3
   constexpr int WP = NE + 4;                 // TMA producer
   constexpr int WM = NE + 5;                 // MMA issuer (+ TMEM alloc / dealloc)
@@ -642,7 +668,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     // pair: the leader's full_u counts both CTAs' unpack warps (8) + its producer; its tempty
     // counts both CTAs' epilogue warps
     for (int i = 0; i < C::SU; ++i) { mbar_init(&full_u[i], A8 ? 1 : PAIR ? 9 : BI8 ? 5 : 4); mbar_init(&empty_u[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], (PAIR ? 2 : 1) * EpiCfg<KIND>::EPW); }
+    for (int i = 0; i < NBUF; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], (PAIR ? 2 : 1) * E::EPW); }
     fence_mbar_init();
   }
   if constexpr (PAIR) {
@@ -673,8 +699,8 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
   // Register rebalancing (row epilogues): one setmaxnreg per side, executed by whole
   // warpgroups at a single call site that dominates that side's code.
   if (warp >= NE) {
-  if constexpr (EpiCfg<KIND>::PAD > 0)
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(EpiCfg<KIND>::MAINLOOP_REGS));
+  if constexpr (E::PAD > 0)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(E::MAINLOOP_REGS));
   if (warp == WP) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
@@ -751,10 +777,10 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
       // profiling only (Q4_TRACE): per-tile (wait tempty, wait full_u total, issue span), slot 62
       unsigned long long* mtr = p.trace ? p.trace + ((size_t)blockIdx.x * 64 + 62) * 8 : nullptr;
       while (it.next(mb, nb)) {
-        const uint32_t b = tcount & 1u;
+        const uint32_t b = tcount % NBUF, ph = (tcount / NBUF) & 1u;
         const unsigned long long m0 = mtr ? gtimer() : 0;
-        if constexpr (PAIR) mbar_wait_cluster(&tempty[b], ((tcount >> 1) & 1u) ^ 1u);
-        else mbar_wait(&tempty[b], ((tcount >> 1) & 1u) ^ 1u);
+        if constexpr (PAIR) mbar_wait_cluster(&tempty[b], ph ^ 1u);
+        else mbar_wait(&tempty[b], ph ^ 1u);
         tc_fence_after();
         const unsigned long long m1 = mtr ? gtimer() : 0;
         unsigned long long mw = 0;
@@ -820,12 +846,12 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
         // Row epilogues: the first unpack warp polls both barriers and the other three block
         // in bar.sync (their spin would take issue slots from 16 busy epilogue warps).  With
         // the light F16 / I32 epilogues every warp polls (measured faster: no barrier hop).
-        if (!EpiCfg<KIND>::ROW || warp == WU) {
+        if (!E::ROW || warp == WU) {
           mbar_wait(&full_p[s], (g / C::SP) & 1u);
           mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
         }
         const unsigned long long u1 = utr ? gtimer() : 0;
-        if constexpr (EpiCfg<KIND>::ROW) named_bar(kUnpackBar, 128);
+        if constexpr (E::ROW) named_bar(kUnpackBar, 128);
         const unsigned long long u2 = utr ? gtimer() : 0;
         const uint8_t* pk = smem + C::OFF_PK + s * C::PK_STAGE;
         uint8_t* un = smem + C::OFF_UN + su * C::UN_STAGE;
@@ -852,42 +878,47 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
   }
   } else {
     // ---------------------------------------------------------------- epilogue
-    if constexpr (EpiCfg<KIND>::PAD > 0)
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EpiCfg<KIND>::EPI_REGS));
+    if constexpr (E::PAD > 0)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(E::EPI_REGS));
     // 2 groups (group g drains TMEM buffer g: tiles with tcount % 2 == g) x EPW warps.  In
     // a group, the warp with lane quarter q and side `sub` (EPW = 8: two sides) handles rows
     // 32q..32q+31 and the 32-column chunks j with j % NS == sub.  The NS warps of a
     // (group, q) set share a 32-row x 128-byte staging slab, so every 64-column slab leaves as
     // full 128-byte row segments.
-    constexpr int EPW = EpiCfg<KIND>::EPW;
+    // R4: 4 groups x 4 warps, group g drains buffer g (tcount % 4 == g); a warp covers its 32
+    // rows x all TN = 128 columns and owns a 4 KB slab; column parameters per tile and group.
+    constexpr int EPW = E::EPW;
     constexpr int NS = EPW / 4;            // sides per lane quarter
     constexpr int GT = EPW * 32;           // threads per group
-    const int ew = warp;                   // 0 .. 2*EPW-1
+    const int ew = warp;                   // 0 .. NBUF*EPW-1
     const int grp = ew / EPW;
     const int sub = (ew >> 2) % NS;
     const int q = warp & 3;                // TMEM lane quarter
     const int r = q * 32 + lane;           // row within the tile
-    const int pair = grp * 4 + q;
-    const int gbar = 1 + grp, pbar = 4 + pair;
+    const int pair = R4 ? ew : grp * 4 + q;  // staging slab
+    const int gbar = R4 ? 4 + grp : 1 + grp, pbar = 4 + pair;
     const bool leader = (ew % EPW) == 0 && lane == 0;
     uint8_t* stg = smem + C::OFF_STG + pair * 4096;
     float4* rowp = reinterpret_cast<float4*>(smem + C::OFF_ROW) + grp * 256;  // [2 sides][128]
     const int N = p.N;
     const float clip = p.clip;
-    float* prm = reinterpret_cast<float*>(smem + C::OFF_PRM);  // sw | bias | gamma | beta of this n-block
-    {
-      const int c0 = it.rank * TN;  // this CTA's fixed n-block (pairs: per cluster)
-      for (int i = ew * 32 + lane; i < TN; i += 2 * GT) {
-        prm[i] = p.w_scales ? p.w_scales[c0 + i] : 1.0f;
-        prm[TN + i] = p.bias ? __half2float(p.bias[c0 + i]) : 0.f;
-        if (KIND == EPI_F16 && p.a_zeros) prm[2 * TN + i] = p.w_sums[c0 + i];
-        if constexpr (KIND == EPI_RESLN_Q4) {
-          prm[2 * TN + i] = __half2float(p.gamma[c0 + i]);
-          prm[3 * TN + i] = __half2float(p.beta[c0 + i]);
-        }
+    // sw | bias | gamma | beta of this CTA's n-block (staged once) or, R4, of the group's tile
+    float* const prm0 = reinterpret_cast<float*>(smem + C::OFF_PRM) + (R4 ? grp * 4 * TN : 0);
+    auto load_prm = [&](int c0, int i) {
+      prm0[i] = p.w_scales ? p.w_scales[c0 + i] : 1.0f;
+      prm0[TN + i] = p.bias ? __half2float(p.bias[c0 + i]) : 0.f;
+      if (KIND == EPI_F16 && p.a_zeros) prm0[2 * TN + i] = p.w_sums[c0 + i];
+      if constexpr (KIND == EPI_RESLN_Q4) {
+        prm0[2 * TN + i] = __half2float(p.gamma[c0 + i]);
+        prm0[3 * TN + i] = __half2float(p.beta[c0 + i]);
       }
-      asm volatile("bar.sync 3, %0;" ::"r"(2 * GT) : "memory");  // all epilogue warps
+    };
+    if constexpr (!R4) {
+      const int c0 = it.rank * TN;  // this CTA's fixed n-block (pairs: per cluster)
+      for (int i = ew * 32 + lane; i < TN; i += NBUF * GT) load_prm(c0, i);
+      asm volatile("bar.sync 3, %0;" ::"r"(NBUF * GT) : "memory");  // all epilogue warps
     }
+    const float* prm = prm0;
     // sync of the NS warps sharing a slab (a warp alone needs only __syncwarp)
     auto slab_sync = [&]() {
       if constexpr (NS > 1) named_bar(pbar, 32 * NS); else __syncwarp();
@@ -900,13 +931,14 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
     auto stamp = [&](int k) {
       if (tr && leader) tr[k] = gtimer();
     };
-    if constexpr (KIND == EPI_GELU_Q4 && Q4_GELU_DECOUPLED) {
+    if constexpr (KIND == EPI_GELU_Q4 && Q4_GELU_DECOUPLED && !R4) {
       gelu_epilogue<TN, A8, H16>(p, it, tmem, tfull, tempty, stg, rowp, prm, ew, lane);
     } else
     while (it.next(mb, nb)) {
-      const uint32_t b = tcount & 1u;
+      const uint32_t b = tcount % NBUF;
       if ((int)b != grp) { ++tcount; continue; }
       tr = (p.trace && tcount < 64) ? p.trace + ((size_t)blockIdx.x * 64 + tcount) * 8 : nullptr;
+      if constexpr (R4) load_prm(nb * TN, ew % EPW * 32 + lane);  // GT == TN: one column per thread
       stamp(0);
       const int m0 = mb * C::BM;
       const int gm = m0 + r;
@@ -929,7 +961,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND>::THREADS, 1)
       }
       // one warp of the group polls the accumulator barrier; the others block in bar.sync
       // (a try_wait spin in all EPW warps costs issue slots the working group needs)
-      if (ew % EPW == 0) mbar_wait(&tfull[b], (tcount >> 1) & 1u);
+      if (ew % EPW == 0) mbar_wait(&tfull[b], (tcount / NBUF) & 1u);
       named_bar(gbar, GT);
       tc_fence_after();
       stamp(1);
@@ -1245,7 +1277,9 @@ int num_sms() {
 
 template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false>
 cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {
-  using C = TcCfg<TN, BI8, A8, PAIR>;
+  constexpr bool R4 = PAIR && (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4);
+  using C = TcCfg<TN, BI8, A8, PAIR, R4>;
+  constexpr int THREADS = EpiCfg<KIND, R4>::THREADS;
   auto kern = w4a4_tc_kernel<TN, KIND, BI8, A8, H16, PAIR>;
   static bool configured = false;
   if (!configured) {
@@ -1270,6 +1304,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.a_scales = g.a_scales; p.w_scales = g.w_scales;
   p.a_zeros = g.a_zeros; p.w_sums = g.w_sums;
   p.pair = PAIR ? 1 : 0;
+  p.lin = R4 ? 1 : 0;
   p.bias = g.bias; p.residual = g.residual; p.gamma = g.gamma; p.beta = g.beta;
   p.ln_eps = g.ln_eps; p.clip = g.clip;
   p.out_i32 = g.out_i32; p.out_f16 = g.out_f16; p.out_codes = g.out_codes; p.out_scales = g.out_scales;
@@ -1288,10 +1323,36 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   // groups of ntn co-resident CTAs (one per SM); a group walks the m-blocks.  Pairs: the unit
   // is a 2-CTA cluster (two SMs) walking m-block pairs.
   const int units = PAIR ? sms / 2 : sms, mwalk = PAIR ? p.mblocks / 2 : p.mblocks;
-  if (p.ntn > units) { *why = "N/TN exceeds the number of SMs"; return cudaErrorNotSupported; }
-  p.groups = units / p.ntn;
-  if (p.groups > mwalk) p.groups = mwalk;
-  const int grid = p.groups * p.ntn * (PAIR ? 2 : 1);
+  int grid;
+  if constexpr (R4) {
+    // linear schedule over every co-resident CTA pair (the row rendezvous spins, so all
+    // clusters must be resident at once: the occupancy query bounds the grid)
+    static const int max_clusters = [&] {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2 * units);
+      cfg.blockDim = dim3(THREADS);
+      cfg.dynamicSmemBytes = C::SMEM;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = 0;
+      return n;
+    }();
+    if (max_clusters <= 0) { *why = "no co-resident CTA pair for the R4 kernel"; return cudaErrorNotSupported; }
+    p.groups = max_clusters < units ? max_clusters : units;
+    if (p.groups > mwalk * p.ntn) p.groups = mwalk * p.ntn;
+    grid = 2 * p.groups;
+  } else {
+    if (p.ntn > units) { *why = "N/TN exceeds the number of SMs"; return cudaErrorNotSupported; }
+    p.groups = units / p.ntn;
+    if (p.groups > mwalk) p.groups = mwalk;
+    grid = p.groups * p.ntn * (PAIR ? 2 : 1);
+  }
   if (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4) {
     const size_t need = tc_workspace_bytes(g.M, g.N, TN, KIND);
     if (!ws || ws_bytes < need) { *why = "workspace too small for the row-epilogue exchange"; return cudaErrorInvalidValue; }
@@ -1304,7 +1365,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     p.xstat = reinterpret_cast<float2*>(w + cnt_bytes);
     p.xamax = reinterpret_cast<float*>(w + cnt_bytes + nslot * 8);
     p.yscr = KIND == EPI_GELU_Q4 ? reinterpret_cast<__half*>(w + cnt_bytes + nslot * 12) : nullptr;
-    if (KIND == EPI_GELU_Q4 && (size_t)grid > tc_row_grid(g.M, g.N, TN)) {
+    if (KIND == EPI_GELU_Q4 && Q4_GELU_DECOUPLED && (size_t)grid > tc_row_grid(g.M, g.N, TN)) {
       *why = "row-epilogue grid larger than the workspace sizing assumed";
       return cudaErrorInvalidValue;
     }
@@ -1315,7 +1376,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     if constexpr (PAIR) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(EpiCfg<KIND>::THREADS);
+      cfg.blockDim = dim3(THREADS);
       cfg.dynamicSmemBytes = C::SMEM;
       cfg.stream = s;
       cudaLaunchAttribute at[1];
@@ -1327,7 +1388,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
       cfg.numAttrs = 1;
       le = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
     } else {
-      le = launch_pdl(g.M <= kPdlMaxRows, kern, dim3(grid), dim3(EpiCfg<KIND>::THREADS), C::SMEM, s, ta, tb, p);
+      le = launch_pdl(g.M <= kPdlMaxRows, kern, dim3(grid), dim3(THREADS), C::SMEM, s, ta, tb, p);
     }
     if (le != cudaSuccess) return le;
   }
@@ -1344,6 +1405,15 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   }
   return cudaGetLastError();
 }
+
+// The R4 row kernel is off: measured slower (FFN1 253 vs 219 us, FFN2 243 vs 149 us at
+// M = 32768; the pair N = 128 mainloop is shared-memory bound on the A unpack).  Q4_R4=1 in
+// the profiling build selects it (A/B only).
+bool tc_r4_enabled() {
+  static const int env = [] { const char* e = prof_env("Q4_R4"); return e ? atoi(e) : 0; }();
+  return env == 1;
+}
+constexpr int kR4MinRows = 8192;
 
 // The CTA-pair mainloop is on by default where it measured faster; Q4_PAIR=0 disables it
 // (profiling / A-B only).
@@ -1430,7 +1500,8 @@ size_t tc_row_grid(int M, int N, int TN) {
 
 size_t tc_workspace_bytes(int M, int N, int TN, int kind) {
   if (TN <= 0) return 0;
-  const size_t mblocks = (size_t)(M + 127) / 128, ntn = (size_t)N / TN;
+  // partial slots for ntn = N / min(TN, 128): the R4 row kernel (TN = 128) may run instead
+  const size_t mblocks = (size_t)(M + 127) / 128, ntn = (size_t)N / (TN < 128 ? TN : 128);
   size_t b = tc_counter_bytes(M) + mblocks * ntn * 128 * 12;
   // GELU_Q4: two y parking slots per epilogue group (pass B of tile t runs after pass A of t + 2)
   if (kind == EPI_GELU_Q4 && Q4_GELU_DECOUPLED) b += tc_row_grid(M, N, TN) * 4 * 128 * (size_t)TN * 2;
@@ -1439,6 +1510,13 @@ size_t tc_workspace_bytes(int M, int N, int TN, int kind) {
 
 cudaError_t launch_w4a4_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {
   if (g.M == 0) return cudaSuccess;
+  // Row epilogues at large M with prepacked weights: the R4 pair kernel (four accumulators)
+  if ((g.kind == EPI_GELU_Q4 || g.kind == EPI_RESLN_Q4) && g.w_i8 && !g.a_i8 && !g.f16_ops && !g.a_zeros &&
+      g.M % 256 == 0 && g.M >= kR4MinRows && g.N % 128 == 0 && g.mainloop != Q4_MAINLOOP_TCGEN05_W8_1CTA &&
+      tc_pair_enabled() && tc_r4_enabled()) {
+    if (g.kind == EPI_GELU_Q4) return run_tc<128, EPI_GELU_Q4, true, false, false, true>(g, ws, ws_bytes, s, why);
+    return run_tc<128, EPI_RESLN_Q4, true, false, false, true>(g, ws, ws_bytes, s, why);
+  }
   const int tn = tc_tile_n(g.M, g.N, g.kind);
   if (!tn) {
     *why = "the tcgen05 path needs N % 32 == 0 (N % 64 == 0 for GELU_Q4 / RESLN_Q4)";

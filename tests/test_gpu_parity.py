@@ -525,3 +525,39 @@ def test_linear_f16_wide_n_falls_back_from_pairs(q4):
     wd = dev(w)
     i32 = host(q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), q4.EPI_I32, w_i8=q4.prepack_weights(wd))["i32"])
     assert np.array_equal(i32[:128], orc.gemm_i32(a[:128], w, 128, N, K))
+
+
+# ------------------------------------------------------------------ R4: row epilogues on the pair mainloop
+@pytest.mark.parametrize("M,N,K,kind", [(8192, 4096, 1024, "gelu"), (8448, 3072, 768, "gelu"),
+                                        (8192, 1024, 4096, "resln"), (8448, 768, 3072, "resln"),
+                                        (8192, 1024, 1024, "resln")])
+def test_r4_row_epilogues(q4, M, N, K, kind):
+    """M % 256 == 0, M >= 8192, prepacked weights: the R4 kernel (CTA-pair mainloop, four
+    128-column accumulators, linear tile schedule, per-tile column parameters).  Every element
+    against the oracle (O-6 / O-7), codes == O-1(GPU fp16); repeated launches reuse the
+    self-resetting rendezvous counters."""
+    x, wt, b = synth.hidden(M, K, f"r4x{M}_{K}"), synth.weight(N, K, f"r4w{N}_{K}"), synth.bias(N, f"r4b{N}")
+    a, sa = orc.quantize_rows(x)
+    w, sw = orc.quantize_rows(wt)
+    wd = dev(w)
+    w8 = q4.prepack_weights(wd)
+    if kind == "gelu":
+        args = dict(bias=dev(b), f16_tap=True, w_i8=w8)
+        ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, orc.EPI_GELU_Q4, bias=b)
+        epi = q4.EPI_GELU_Q4
+    else:
+        res = synth.hidden(M, N, f"r4r{M}_{N}")
+        gam, bet = synth.ln_params(N, f"r4ln{N}")
+        args = dict(bias=dev(b), residual=dev(res), gamma=dev(gam), beta=dev(bet), ln_eps=1e-12, w_i8=w8)
+        ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, orc.EPI_RESLN_Q4, bias=b, residual=res, gamma=gam,
+                              beta=bet, ln_eps=1e-12)
+        epi = q4.EPI_RESLN_Q4
+    out = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), epi, **args)
+    y = host(out["f16"])
+    assert_f16_close(y, ref["f16"], kind)
+    c2, s2 = orc.quantize_rows(y)
+    assert np.array_equal(host(out["codes"]), c2)
+    assert np.array_equal(host(out["scales"]), s2)
+    for _ in range(2):
+        o2 = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), epi, **args)
+        assert np.array_equal(host(o2["codes"]), c2) and np.array_equal(host(o2["f16"]), y)
