@@ -413,18 +413,32 @@ cluster_tail:
       if (g == 0 && r < S) ctx_scales[row0 + r] = a > 0.f ? __fdiv_rn(a, qm) : 1.0f;
     }
     __syncthreads();
-    // this CTA's columns [64 j0, 64 (j0 + hpc)): cpr 16-byte chunks (8 values) per row
-    const int cpr = hpc * 8;
-    for (int idx = threadIdx.x; idx < S * cpr; idx += AT_THREADS) {
-      const int rw = idx / cpr, c = idx - rw * cpr;
-      const float a = amx[rw];
-      const uint4 x = __ldcg(reinterpret_cast<const uint4*>(ctx_f16 + (size_t)(row0 + rw) * h + j0 * 64 + c * 8));
-      const uint32_t hh[4] = {x.x, x.y, x.z, x.w};
-      if (i8)
-        reinterpret_cast<uint2*>(ctx_codes + (size_t)(row0 + rw) * h + j0 * 64)[c] = requant8_i8(hh, a, rr7[rw], 0.f);
-      else
-        reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] =
-            a > 0.f ? requant8(hh, a, rr7[rw], 0.f) : 0u;
+    // this CTA's columns [64 j0, 64 (j0 + hpc)): cpr 16-byte chunks (8 values) per row; eight
+    // L2 loads in flight per thread before their codes are computed
+    const int cpr = hpc * 8, tot = S * cpr;
+    for (int base = threadIdx.x; base < tot; base += 8 * AT_THREADS) {
+      uint4 xs[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * AT_THREADS;
+        if (idx < tot) {
+          const int rw = idx / cpr, c = idx - rw * cpr;
+          xs[u] = __ldcg(reinterpret_cast<const uint4*>(ctx_f16 + (size_t)(row0 + rw) * h + j0 * 64 + c * 8));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * AT_THREADS;
+        if (idx >= tot) break;
+        const int rw = idx / cpr, c = idx - rw * cpr;
+        const float a = amx[rw];
+        const uint32_t hh[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
+        if (i8)
+          reinterpret_cast<uint2*>(ctx_codes + (size_t)(row0 + rw) * h + j0 * 64)[c] = requant8_i8(hh, a, rr7[rw], 0.f);
+        else
+          reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] =
+              a > 0.f ? requant8(hh, a, rr7[rw], 0.f) : 0u;
+      }
     }
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
@@ -471,6 +485,8 @@ cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __ha
   if (B < 148)
     for (int d = 8; d >= 2; --d)
       if (heads % d == 0 && B * d <= 296) { G = d; break; }
+  static const int g_env = prof_env("Q4_ATTN_G") ? atoi(prof_env("Q4_ATTN_G")) : 0;  // profiling only
+  if (g_env > 0 && heads % g_env == 0 && g_env <= 8) G = g_env;
   note_launch();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(B * G));

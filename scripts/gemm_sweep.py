@@ -4,8 +4,9 @@ timing of a CUDA graph of 20 back-to-back launches (inputs resident; the graph r
 host launch cost that would otherwise dominate at small M), for the tcgen05 mainloop with packed
 weights, with prepacked int8 weights (W8), the legacy mma.sync s8 baseline, and the W8A8
 baseline (int8 activations and weights, both TMA'd into the MMA stage).  TOPS =
-2*M*N*K / t; roofline = min(INT8 peak, HBM * ops/bytes) with the peaks of bench.peaks().
-Writes one JSON object per line (profiles/r1_gemm_sweep.jsonl when run by the round script)."""
+2*M*N*K / t; roofline = min(INT8 burst peak, HBM * ops/bytes) with the peaks of bench.peaks()
+(burst: every GEMM here runs alone, not inside the long step).
+Writes one JSON object per line (profiles/<round>/gemm_sweep.jsonl when run by the round script)."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -14,7 +15,7 @@ from paper_2301_12017_b200 import synth
 from bench import peaks
 
 pk = peaks()
-int8_peak, hbm = pk["int8_tops"], pk["hbm_gbs"]
+int8_peak, hbm = pk["int8_tops_burst"], pk["hbm_gbs"]  # each GEMM is timed alone: burst peak
 dev = torch.device("cuda")
 for (K, N) in ((768, 3072), (3072, 768), (1024, 4096), (4096, 1024)):
     w = torch.from_numpy(synth.random_packed(N, K, "sw%d" % N)).to(dev)

@@ -4,7 +4,7 @@
 #  2. one `ncu --set full` capture of the dominant kernel (FFN1 GELU_Q4 GEMM, W8 variant)
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
-R=${1:-r1}
+R=${1:-r2}
 B="python bench.py --steps 2 --warmup 1 --no-extras --no-cpu-baseline --no-e2e"
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv \
   --log-file gpurun_out/${R}_launches.csv $B > gpurun_out/${R}_ncu_list.log 2>&1
