@@ -604,6 +604,27 @@ def side_measurements(q4, synth, torch, np, dev, args):
         out[name] = t[100]
         out[name.replace("p50", "p10")] = t[20]
         out[name.replace("p50", "p90")] = t[180]
+    # Latency floor (SURVEY 8(d) configs[2]): a CUDA graph of as many empty PDL kernels as the
+    # 12-layer bs-1 forward launches (1 + 12 x 5), same launch attributes, p50 of 200 replays
+    for nk, nm in ((61, "latency_floor_61_empty_kernels_ms"), (6, "latency_floor_6_empty_kernels_ms")):
+        g = torch.cuda.CUDAGraph()
+        s2 = torch.cuda.Stream()
+        with torch.cuda.stream(s2):
+            q4.launch_floor(nk, 36)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            q4.launch_floor(nk, 36)
+        for _ in range(20):
+            g.replay()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(201)]
+        torch.cuda.synchronize()
+        evs[0].record(stream)
+        for i in range(200):
+            g.replay()
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        t = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(200))
+        out[nm] = t[100]
     # The paper's INT4-vs-INT8 comparison (Fig. e2e_i4_i8): the W8A8
     # baseline encoder (same kernels at 8 bits) on the bench workload and the latency config
     for size, L, B, name in (("large", 24, 256, "w8a8_bert_large_24l_bs256"), ("base", 12, 1, "w8a8_bert_base_12l_bs1")):

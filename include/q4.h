@@ -64,6 +64,12 @@ Q4_API const char* q4_last_error(void);
 Q4_API const char* q4_version(void);
 /* Number of kernels this process launched through the library (all threads). */
 Q4_API uint64_t q4_launch_count(void);
+/* Measurement only (the latency roofline of BASELINE configs[2]: "launch
+ * overhead non-negligible"): launch `n` empty kernels of `ctas` CTAs x 128 threads on `stream`
+ * with the same programmatic-dependent-launch attribute the encoder uses for small problems,
+ * so a CUDA graph of them gives the empty-graph floor for the encoder's kernel count.
+ * n in [0, 4096], ctas in [1, 1024]; Q4_EINVAL otherwise.  No memory is touched. */
+Q4_API q4_status q4_launch_floor(int32_t n, int32_t ctas, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * a1/a2  Symmetric per-row INT4 quantization + packing.

@@ -25,7 +25,7 @@ EXPORTS = (
     "q4_attention_f16_q8", "q4_encoder_layer_w8a8_workspace", "q4_encoder_layer_w8a8",
     "q4_encoder_stack_w8a8_workspace", "q4_encoder_stack_w8a8", "q4_f16_linear_workspace", "q4_f16_linear",
     "q4_quantize_rows_asym", "q4_weight_code_sums", "q4_w4a4_asym_linear",
-    "q4_encoder_pipeline_workspace", "q4_encoder_pipeline",
+    "q4_encoder_pipeline_workspace", "q4_encoder_pipeline", "q4_launch_floor",
 )
 
 
@@ -114,6 +114,7 @@ def lib():
         L.q4_encoder_stack_w8a8_workspace.argtypes = [C.POINTER(LayerCfg), I64, I64]
         L.q4_encoder_stack_w8a8_workspace.restype = SZ
         L.q4_encoder_stack_w8a8.argtypes = L.q4_encoder_stack.argtypes
+        L.q4_launch_floor.argtypes = [C.c_int32, C.c_int32, P]
         for name in EXPORTS:
             L[name].restype = L[name].restype if name in (
                 "q4_last_error", "q4_version", "q4_launch_count", "q4_w4a4_linear_workspace",

@@ -86,6 +86,7 @@ int tc_tile_n(int M, int N, int kind);
 size_t tc_workspace_bytes(int M, int N, int TN, int kind);
 size_t tc_row_grid(int M, int N, int TN);  // CTAs of a 1-CTA row-epilogue launch
 size_t tc_counter_bytes(int M);  // the rendezvous counters at the start of a row-epilogue workspace
+cudaError_t launch_floor_kernel(int ctas, cudaStream_t s);  // empty PDL kernel (measurement only)
 cudaError_t launch_w4a4_legacy(const GemmArgs& g, bool s4, cudaStream_t s, const char** why);
 // i8: W8A8 baseline -- int8 ctx codes [B*S, h] with scale amax/127 instead of packed INT4
 cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __half* ctx_f16,

@@ -48,6 +48,17 @@ const char* q4_last_error(void) { return g_err; }
 const char* q4_version(void) { return "q4-b200 0.1 (sm_100a; tcgen05 kind::i8 W4A4)"; }
 uint64_t q4_launch_count(void) { return q4::g_launches.load(); }
 
+q4_status q4_launch_floor(int32_t n, int32_t ctas, void* stream) {
+  g_err[0] = 0;
+  if (n < 0 || n > 4096 || ctas < 1 || ctas > 1024)
+    return fail(Q4_EINVAL, "q4_launch_floor: n=%d ctas=%d (need 0..4096, 1..1024)", n, ctas);
+  for (int i = 0; i < n; ++i) {
+    cudaError_t e = q4::launch_floor_kernel(ctas, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "q4_launch_floor");
+  }
+  return Q4_OK;
+}
+
 q4_status q4_quantize_rows(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x, float clip,
                            uint8_t* codes, float* scales, void* stream) {
   g_err[0] = 0;

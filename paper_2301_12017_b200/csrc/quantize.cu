@@ -260,4 +260,15 @@ cudaError_t launch_quantize_rows_i8(const __half* x, int64_t rows, int cols, int
   return launch_quantize_impl<true>(x, rows, cols, ld_x, clip, reinterpret_cast<uint8_t*>(codes), scales, s);
 }
 
+// Empty kernel with the encoder's launch attributes (q4_launch_floor, measurement only): the
+// same prologue handshake as the hot kernels (launch_dependents, then wait) and nothing else.
+__global__ void floor_kernel() {
+  pdl_launch_dependents();
+  pdl_wait();
+}
+cudaError_t launch_floor_kernel(int ctas, cudaStream_t s) {
+  note_launch();
+  return launch_pdl(true, floor_kernel, dim3(ctas), dim3(128), 0, s);
+}
+
 }  // namespace q4

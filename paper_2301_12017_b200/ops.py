@@ -233,6 +233,11 @@ def layer_cfg(cfg: dict) -> LayerCfg:
                     int(cfg.get("fp16_parts", 0)))
 
 
+def launch_floor(n: int, ctas: int = 32):
+    """Measurement only: n empty PDL kernels on the current stream (q4_launch_floor)."""
+    _lib.check(_lib.lib().q4_launch_floor(int(n), int(ctas), C.c_void_p(_stream())), "q4_launch_floor")
+
+
 def prepack_weights(w_codes: torch.Tensor) -> torch.Tensor:
     """a2': packed INT4 [N, K/2] -> MMA-ready int8 [N, K] (q4_prepack_weights)."""
     _need(w_codes, torch.uint8, "w_codes", 2)
