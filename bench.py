@@ -660,8 +660,8 @@ def side_measurements(q4, synth, torch, np, dev, args):
                                                        "q3_ms": r["times"]["q3"], "times": r["times"]}
     # GEMM TOPS at the BERT-large FFN shapes, M = 32768 (tcgen05 vs legacy mma.sync); each GEMM
     # is timed alone, so its fraction is against the burst INT8 peak
-    out["gemm_peak_int8_tops_burst"] = pk["int8_tops_burst"]
     pk = peaks()
+    out["gemm_peak_int8_tops_burst"] = pk["int8_tops_burst"]
     for (Nn, K) in ((4096, 1024), (1024, 4096)):
         M = 32768
         a = torch.from_numpy(synth.random_packed(M, K, f"sw_a{K}")).to(dev)

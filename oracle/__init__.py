@@ -67,7 +67,7 @@ def lib():
                                          P, P, P, P, I]
         L.oracle_f16_linear.argtypes = [P, P, I64, I64, I64, I, P, P, P, P, D, F, P, P, P, I]
         L.oracle_quantize_rows_asym.argtypes = [P, I64, I64, I64, P, P, P, I]
-        L.oracle_w4a4_asym_linear.argtypes = [P, P, P, P, P, I64, I64, I64, I, P, P, P, I]
+        L.oracle_w4a4_asym_linear.argtypes = [P, P, P, P, P, I64, I64, I64, I, P, P, P, P, D, P, P, P, P, P, I]
         _lib = L
     return _lib
 
@@ -245,19 +245,28 @@ def unpack_u4(packed: np.ndarray, cols: int) -> np.ndarray:
 
 
 def w4a4_asym_linear(a_codes, a_scales, a_zeros, w_codes, w_scales, M, N, K, epi=EPI_F16, bias=None,
-                     threads: int = 0):
-    """O-16: asymmetric-activation W4A4 linear, F16 or I32 epilogue."""
+                     residual=None, gamma=None, beta=None, ln_eps=1e-12, asym_out=True, threads: int = 0):
+    """O-16: asymmetric-activation W4A4 linear with the O-4..O-7 epilogues; the requantizing
+    kinds code their fp16 output asymmetrically (O-15: codes, scales, zeros) when asym_out,
+    else symmetrically (O-1: codes, scales)."""
     a_codes, w_codes = _c(a_codes, np.uint8), _c(w_codes, np.uint8)
     a_scales, a_zeros, w_scales = _c(a_scales, np.float32), _c(a_zeros, np.float32), _c(w_scales, np.float32)
-    bias = _c(bias, np.float16)
+    bias, residual = _c(bias, np.float16), _c(residual, np.float16)
+    gamma, beta = _c(gamma, np.float16), _c(beta, np.float16)
     out = {}
-    i32 = f16 = None
+    i32 = f16 = codes = scales = zeros = None
     if epi == EPI_I32:
         i32 = out["i32"] = np.zeros((M, N), np.int32)
     else:
         f16 = out["f16"] = np.zeros((M, N), np.float16)
+    if epi in (EPI_GELU_Q4, EPI_RESLN_Q4):
+        codes = out["codes"] = np.zeros((M, (N + 1) // 2), np.uint8)
+        scales = out["scales"] = np.zeros(M, np.float32)
+        if asym_out:
+            zeros = out["zeros"] = np.zeros(M, np.float32)
     rc = lib().oracle_w4a4_asym_linear(_p(a_codes), _p(a_scales), _p(a_zeros), _p(w_codes), _p(w_scales), M, N, K,
-                                       epi, _p(bias), _p(i32), _p(f16), threads)
+                                       epi, _p(bias), _p(residual), _p(gamma), _p(beta), float(ln_eps), _p(i32),
+                                       _p(f16), _p(codes), _p(scales), _p(zeros), threads)
     _check(rc, "w4a4_asym_linear")
     return out
 

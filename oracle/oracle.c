@@ -140,35 +140,37 @@ int oracle_quantize_rows_i8(const uint16_t* x, int64_t rows, int64_t cols, int64
  * units of 2^-24: 15 (X - Z) < 2^46), scale = fl32(fl64(D) / 15) (fp64 division, then fp32);
  * constant row -> scale 1, codes 0, zero = the constant.  Codes packed as
  * unsigned nibbles, low nibble = even index. */
+/* One row of O-15: codes packed two per byte (low nibble = even column), scale, zero. */
+static void quantize_row_asym(const uint16_t* xr, int64_t cols, uint8_t* out, float* scale, float* zero) {
+  int64_t pb = (cols + 1) / 2;
+  double mn = oracle_f16_to_f64(xr[0]), mx = mn;
+  for (int64_t j = 1; j < cols; ++j) {
+    double v = oracle_f16_to_f64(xr[j]);
+    if (v < mn) mn = v;
+    if (v > mx) mx = v;
+  }
+  *zero = (float)mn;
+  memset(out, 0, (size_t)pb);
+  if (mx == mn) {
+    *scale = 1.0f;
+    return;
+  }
+  int64_t Dq = (int64_t)ldexp(mx - mn, 24);  /* exact: fp16 values are multiples of 2^-24 */
+  for (int64_t j = 0; j < cols; ++j) {
+    int64_t Xq = (int64_t)ldexp(oracle_f16_to_f64(xr[j]) - mn, 24);
+    int64_t c = rhe_div(15 * Xq, Dq);
+    if (c > 15) c = 15;  /* clamp to [0, 2^b - 1] (R17); never binds */
+    out[j / 2] |= (uint8_t)((c & 0xF) << (4 * (j & 1)));
+  }
+  *scale = (float)((mx - mn) / 15.0);
+}
+
 int oracle_quantize_rows_asym(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x,
                               uint8_t* codes, float* scales, float* zeros, int threads) {
   if (rows < 0 || cols <= 0 || ld_x < cols) return -1;
   int64_t pb = (cols + 1) / 2;
 #pragma omp parallel for schedule(static) OMP_THREADS(threads)
-  for (int64_t r = 0; r < rows; ++r) {
-    const uint16_t* xr = x + r * ld_x;
-    double mn = oracle_f16_to_f64(xr[0]), mx = mn;
-    for (int64_t j = 1; j < cols; ++j) {
-      double v = oracle_f16_to_f64(xr[j]);
-      if (v < mn) mn = v;
-      if (v > mx) mx = v;
-    }
-    zeros[r] = (float)mn;
-    uint8_t* out = codes + r * pb;
-    memset(out, 0, (size_t)pb);
-    if (mx == mn) {
-      scales[r] = 1.0f;
-      continue;
-    }
-    int64_t Dq = (int64_t)ldexp(mx - mn, 24);  /* exact: fp16 values are multiples of 2^-24 */
-    for (int64_t j = 0; j < cols; ++j) {
-      int64_t Xq = (int64_t)ldexp(oracle_f16_to_f64(xr[j]) - mn, 24);
-      int64_t c = rhe_div(15 * Xq, Dq);
-      if (c > 15) c = 15;  /* clamp to [0, 2^b - 1] (R17); never binds */
-      out[j / 2] |= (uint8_t)((c & 0xF) << (4 * (j & 1)));
-    }
-    scales[r] = (float)((mx - mn) / 15.0);
-  }
+  for (int64_t r = 0; r < rows; ++r) quantize_row_asym(x + r * ld_x, cols, codes + r * pb, &scales[r], &zeros[r]);
   return 0;
 }
 
@@ -252,7 +254,7 @@ static int linear_epilogue(const int32_t* acc, const double* dacc, const float* 
                            const uint16_t* residual, const uint16_t* gamma, const uint16_t* beta,
                            double ln_eps, float clip, int32_t* out_i32, uint16_t* out_f16,
                            int qmax, uint8_t* out_codes4, int8_t* out_codes8, float* out_scales,
-                           int threads) {
+                           float* out_zeros, int threads) {
   int64_t pb = (N + 1) / 2;
 #pragma omp parallel for schedule(static) OMP_THREADS(threads)
   for (int64_t m = 0; m < M; ++m) {
@@ -274,6 +276,10 @@ static int linear_epilogue(const int32_t* acc, const double* dacc, const float* 
       case ORACLE_EPI_GELU_Q4:
         for (int64_t n = 0; n < N; ++n) y[n] = oracle_f64_to_f16(gelu_erf(t[n]));
         if (out_f16) memcpy(out_f16 + m * N, y, (size_t)N * sizeof(uint16_t));
+        if (out_zeros) { /* asymmetric requant (NEXT-3): O-15 on the fp16 row */
+          quantize_row_asym(y, N, out_codes4 + m * pb, &out_scales[m], &out_zeros[m]);
+          break;
+        }
         quantize_row_q(y, N, (double)clip, qmax, q, &out_scales[m]);
         if (qmax == 7) pack_row(q, N, out_codes4 + m * pb);
         else memcpy(out_codes8 + m * N, q, (size_t)N);
@@ -292,6 +298,10 @@ static int linear_epilogue(const int32_t* acc, const double* dacc, const float* 
           y[n] = oracle_f64_to_f16((t[n] - mu) * rstd * oracle_f16_to_f64(gamma[n]) +
                                    oracle_f16_to_f64(beta[n]));
         memcpy(out_f16 + m * N, y, (size_t)N * sizeof(uint16_t));
+        if (out_zeros) {
+          quantize_row_asym(y, N, out_codes4 + m * pb, &out_scales[m], &out_zeros[m]);
+          break;
+        }
         quantize_row_q(y, N, (double)clip, qmax, q, &out_scales[m]);
         if (qmax == 7) pack_row(q, N, out_codes4 + m * pb);
         else memcpy(out_codes8 + m * N, q, (size_t)N);
@@ -332,7 +342,7 @@ int oracle_w4a4_linear(const uint8_t* a_codes, const float* a_scales,
   int rc = oracle_gemm_i32(a_codes, w_codes, M, N, K, acc, threads);
   if (!rc)
     rc = linear_epilogue(acc, NULL, a_scales, w_scales, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, clip,
-                         out_i32, out_f16, 7, out_codes, NULL, out_scales, threads);
+                         out_i32, out_f16, 7, out_codes, NULL, out_scales, NULL, threads);
   free(acc);
   return rc;
 }
@@ -348,7 +358,7 @@ int oracle_w8a8_linear(const int8_t* a_codes, const float* a_scales, const int8_
   int rc = gemm_i32_q(a_codes, w_codes, M, N, K, acc, threads);
   if (!rc)
     rc = linear_epilogue(acc, NULL, a_scales, w_scales, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, clip,
-                         out_i32, out_f16, 127, NULL, out_codes, out_scales, threads);
+                         out_i32, out_f16, 127, NULL, out_codes, out_scales, NULL, threads);
   free(acc);
   return rc;
 }
@@ -371,47 +381,50 @@ int oracle_f16_linear(const uint16_t* a, const uint16_t* w, int64_t M, int64_t N
       dacc[m * N + n] = sacc;
     }
   int rc = linear_epilogue(NULL, dacc, NULL, NULL, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, clip, NULL,
-                           out_f16, 7, out_codes, NULL, out_scales, threads);
+                           out_f16, 7, out_codes, NULL, out_scales, NULL, threads);
   free(dacc);
   return rc;
 }
 
 /* O-16: W4A4 linear with asymmetric activations: the dequantized activation is
  * scale * qa + zero, so  t = sw[n] (sa[m] sum_k qa qw + za[m] sum_k qw[n,k]) + b[n]  (fp64),
- * qa unsigned [0, 15], qw signed (symmetric per output channel); F16 and I32 (acc = sum qa qw)
- * epilogues. */
+ * qa unsigned [0, 15], qw signed (symmetric per output channel).  Epilogues as O-4..O-7 (I32:
+ * acc = sum qa qw); the requantizing kinds (GELU_Q4, RESLN_Q4) code their fp16 output with the
+ * asymmetric quantizer O-15 (codes, scales, zeros) when out_zeros is given -- the activations
+ * of an asymmetric layer (NEXT-3) -- else with the symmetric O-1. */
 int oracle_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales, const float* a_zeros,
                             const uint8_t* w_codes, const float* w_scales, int64_t M, int64_t N, int64_t K,
-                            int epi_kind, const uint16_t* bias, int32_t* out_i32, uint16_t* out_f16,
-                            int threads) {
-  if (M < 0 || N <= 0 || K <= 0) return -1;
-  if (epi_kind != ORACLE_EPI_I32 && epi_kind != ORACLE_EPI_F16) return -1;
-  if ((epi_kind == ORACLE_EPI_I32 && !out_i32) || (epi_kind == ORACLE_EPI_F16 && !out_f16)) return -1;
+                            int epi_kind, const uint16_t* bias, const uint16_t* residual, const uint16_t* gamma,
+                            const uint16_t* beta, double ln_eps, int32_t* out_i32, uint16_t* out_f16,
+                            uint8_t* out_codes, float* out_scales, float* out_zeros, int threads) {
+  if (!epilogue_args_ok(M, N, K, epi_kind, residual, gamma, beta, 0.0f, out_i32, out_f16, out_codes, out_scales))
+    return -1;
   int64_t pb = (K + 1) / 2;
   uint8_t* qa = (uint8_t*)malloc((size_t)(M * K > 0 ? M * K : 1));
   int8_t* qw = (int8_t*)malloc((size_t)(N * K));
+  int32_t* acc = (int32_t*)malloc((size_t)(M * N > 0 ? M * N : 1) * sizeof(int32_t));
+  double* dacc = (double*)malloc((size_t)(M * N > 0 ? M * N : 1) * sizeof(double));
   for (int64_t m = 0; m < M; ++m)
     for (int64_t k = 0; k < K; ++k) qa[m * K + k] = (uint8_t)((a_codes[m * pb + k / 2] >> (4 * (k & 1))) & 0xF);
   oracle_unpack_int4(w_codes, N, K, qw);
 #pragma omp parallel for schedule(static) OMP_THREADS(threads)
   for (int64_t m = 0; m < M; ++m)
     for (int64_t n = 0; n < N; ++n) {
-      int64_t acc = 0, cs = 0;
+      int64_t s = 0, cs = 0;
       for (int64_t k = 0; k < K; ++k) {
-        acc += (int64_t)qa[m * K + k] * (int64_t)qw[n * K + k];
+        s += (int64_t)qa[m * K + k] * (int64_t)qw[n * K + k];
         cs += qw[n * K + k];
       }
-      if (epi_kind == ORACLE_EPI_I32) {
-        out_i32[m * N + n] = (int32_t)acc;
-      } else {
-        double t = (double)w_scales[n] * ((double)a_scales[m] * (double)acc + (double)a_zeros[m] * (double)cs) +
-                   (bias ? oracle_f16_to_f64(bias[n]) : 0.0);
-        out_f16[m * N + n] = oracle_f64_to_f16(t);
-      }
+      acc[m * N + n] = (int32_t)s;
+      dacc[m * N + n] = (double)w_scales[n] * ((double)a_scales[m] * (double)s + (double)a_zeros[m] * (double)cs);
     }
+  int rc = linear_epilogue(acc, dacc, NULL, NULL, M, N, epi_kind, bias, residual, gamma, beta, ln_eps, 0.0f, out_i32,
+                           out_f16, 7, out_codes, NULL, out_scales, out_zeros, threads);
   free(qa);
   free(qw);
-  return 0;
+  free(acc);
+  free(dacc);
+  return rc;
 }
 
 /* ------------------------------------------------------------------ O-8 attention */

@@ -153,8 +153,9 @@ int oracle_quantize_rows_asym(const uint16_t* x, int64_t rows, int64_t cols, int
                               uint8_t* codes, float* scales, float* zeros, int threads);
 int oracle_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales, const float* a_zeros,
                             const uint8_t* w_codes, const float* w_scales, int64_t M, int64_t N, int64_t K,
-                            int epi_kind, const uint16_t* bias, int32_t* out_i32, uint16_t* out_f16,
-                            int threads);
+                            int epi_kind, const uint16_t* bias, const uint16_t* residual, const uint16_t* gamma,
+                            const uint16_t* beta, double ln_eps, int32_t* out_i32, uint16_t* out_f16,
+                            uint8_t* out_codes, float* out_scales, float* out_zeros, int threads);
 
 #ifdef __cplusplus
 }

@@ -235,7 +235,7 @@ def layer_cfg(cfg: dict) -> LayerCfg:
 
 def launch_floor(n: int, ctas: int = 32):
     """Measurement only: n empty PDL kernels on the current stream (q4_launch_floor)."""
-    _lib.check(_lib.lib().q4_launch_floor(int(n), int(ctas), C.c_void_p(_stream())), "q4_launch_floor")
+    _lib.check(_lib.lib().q4_launch_floor(int(n), int(ctas), _stream()), "q4_launch_floor")
 
 
 def prepack_weights(w_codes: torch.Tensor) -> torch.Tensor:

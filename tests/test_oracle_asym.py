@@ -78,3 +78,66 @@ def test_asym_linear_vs_ints_and_torch(orc):
     dqw = torch.tensor(sw, dtype=torch.float64)[:, None] * torch.tensor(qw, dtype=torch.float64)
     ref = F.linear(dqa, dqw, torch.tensor(b, dtype=torch.float64)).numpy()
     assert f16ulp_close(out, ref.astype(np.float16), 1)
+
+
+def _asym_operands(orc, M, N, K, tag):
+    x = synth.hidden(M, K, f"ae_x{tag}") + np.float16(0.25)
+    a, sa, za = orc.quantize_rows_asym(x)
+    w, sw = orc.quantize_rows(synth.weight(N, K, f"ae_w{tag}"))
+    b = synth.bias(N, f"ae_b{tag}")
+    # dequantized operands in fp64: za + sa qa (unsigned) and sw qw (signed)
+    xd = za[:, None].astype(np.float64) + sa[:, None].astype(np.float64) * orc.unpack_u4(a, K)
+    wd = sw[:, None].astype(np.float64) * orc.unpack_int4(w, K)
+    t = torch.from_numpy(xd) @ torch.from_numpy(wd).T + torch.from_numpy(b.astype(np.float64))
+    return a, sa, za, w, sw, b, t
+
+
+def test_asym_gelu_requant_epilogue(orc):
+    """O-16 GELU_Q4 (NEXT-3 asymmetric layer): fp16 = GELU(t) of the torch fp64 linear on the
+    dequantized operands (<= 1 ulp), codes/scales/zeros = O-15 of that fp16 row (pinned above),
+    and the symmetric-output variant codes the same fp16 with O-1."""
+    M, N, K = 9, 96, 64
+    a, sa, za, w, sw, b, t = _asym_operands(orc, M, N, K, "g")
+    r = orc.w4a4_asym_linear(a, sa, za, w, sw, M, N, K, orc.EPI_GELU_Q4, bias=b)
+    ref = F.gelu(t).numpy().astype(np.float16)
+    assert f16ulp_close(r["f16"], ref)
+    c, s, z = orc.quantize_rows_asym(r["f16"])
+    assert np.array_equal(r["codes"], c) and np.array_equal(r["scales"], s) and np.array_equal(r["zeros"], z)
+    r2 = orc.w4a4_asym_linear(a, sa, za, w, sw, M, N, K, orc.EPI_GELU_Q4, bias=b, asym_out=False)
+    c2, s2 = orc.quantize_rows(r2["f16"])
+    assert np.array_equal(r2["f16"], r["f16"]) and np.array_equal(r2["codes"], c2) and "zeros" not in r2
+
+
+def test_asym_resln_requant_epilogue(orc):
+    """O-16 RESLN_Q4: fp16 = LayerNorm(t + residual) (torch fp64, biased variance, eps 1e-12)."""
+    M, N, K = 7, 128, 96
+    a, sa, za, w, sw, b, t = _asym_operands(orc, M, N, K, "r")
+    res = synth.hidden(M, N, "ae_res")
+    g, bt = synth.ln_params(N, "ae_ln")
+    r = orc.w4a4_asym_linear(a, sa, za, w, sw, M, N, K, orc.EPI_RESLN_Q4, bias=b, residual=res, gamma=g, beta=bt)
+    z = t + torch.from_numpy(res.astype(np.float64))
+    ref = F.layer_norm(z, (N,), torch.from_numpy(g.astype(np.float64)), torch.from_numpy(bt.astype(np.float64)),
+                       eps=1e-12).numpy().astype(np.float16)
+    assert f16ulp_close(r["f16"], ref)
+    c, s, zz = orc.quantize_rows_asym(r["f16"])
+    assert np.array_equal(r["codes"], c) and np.array_equal(r["scales"], s) and np.array_equal(r["zeros"], zz)
+
+
+def test_asym_epilogues_reduce_to_symmetric(orc):
+    """Zero points 0 and codes in [0, 7] are valid for both quantizers: the asymmetric linear
+    then equals the symmetric oracle O-5..O-7 (pinned in test_oracle_gemm.py) element for element."""
+    M, N, K = 6, 64, 64
+    g = np.random.default_rng(23)
+    q = g.integers(0, 8, (M, K)).astype(np.int8)
+    a = orc.pack_int4(q)
+    sa, za = (g.uniform(0.5, 2, M) / 7).astype(np.float32), np.zeros(M, np.float32)
+    w, sw = orc.quantize_rows(synth.weight(N, K, "ae_sym_w"))
+    b = synth.bias(N, "ae_sym_b")
+    res = synth.hidden(M, N, "ae_sym_r")
+    gm, bt = synth.ln_params(N, "ae_sym_ln")
+    for epi, kw in ((orc.EPI_F16, {}), (orc.EPI_GELU_Q4, {}), (orc.EPI_RESLN_Q4, dict(residual=res, gamma=gm, beta=bt))):
+        ra = orc.w4a4_asym_linear(a, sa, za, w, sw, M, N, K, epi, bias=b, asym_out=False, **kw)
+        rs = orc.w4a4_linear(a, sa, w, sw, M, N, K, epi, bias=b, **kw)
+        assert np.array_equal(ra["f16"], rs["f16"])
+        if epi != orc.EPI_F16:
+            assert np.array_equal(ra["codes"], rs["codes"]) and np.array_equal(ra["scales"], rs["scales"])
