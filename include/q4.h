@@ -139,6 +139,10 @@ typedef struct {
   float* out_scales;         /* [M]      *_Q4                                            */
   const int8_t* w_i8;        /* optional [N, K] prepacked weights (q4_prepack_weights) of the
                                 same codes as w_codes; NULL = unpack w_codes on chip       */
+  float* out_zeros;          /* [M] GELU_Q4 / RESLN_Q4: non-NULL = ASYMMETRIC requant of the
+                                fp16 output (NEXT-3, q4_quantize_rows_asym's
+                                definition: unsigned codes, scales = (max-min)/15, zeros = min);
+                                requant_clip must be 0; NULL = symmetric (a1)               */
 } q4_epilogue;
 
 /* Requirements: M >= 0; N % 32 == 0 (row epilogues N % 64 == 0); K % 32 == 0; K <= 8192
@@ -203,8 +207,13 @@ Q4_API q4_status q4_f16_linear(const uint16_t* a, const uint16_t* w, int64_t M, 
  *   cols <= 4096.
  * q4_weight_code_sums: sums[n] = sum_k qw[n, k] of packed INT4 weights (offline, as float).
  * q4_w4a4_asym_linear: unsigned activation codes x signed weight codes on tcgen05 (u8 x s8),
- *   t = w_scales[n] (a_scales[m] acc + a_zeros[m] w_sums[n]) + bias[n]; epilogues F16 and
- *   I32 (acc = sum qa qw); epi->w_i8 (prepacked weights) honoured.  No workspace. */
+ *   t = w_scales[n] (a_scales[m] acc + a_zeros[m] w_sums[n]) + bias[n]; all four epilogues
+ *   (I32: acc = sum qa qw; F16; GELU_Q4 and RESLN_Q4 as in q4_w4a4_linear, their codes
+ *   asymmetric when epi->out_zeros is set -- the asymmetric encoder layer -- else symmetric);
+ *   epi->w_i8 (prepacked weights) honoured; requant_clip must be 0.  The row epilogues take
+ *   a q4_w4a4_linear_workspace(M, N, K, kind) workspace (same contract); I32 / F16 none.
+ * q4_attention_f16_q4_asym: q4_attention_f16_q4 with the per-token ctx codes of
+ *   q4_quantize_rows_asym (codes, scales, zeros [B*S] fp32, 4-byte aligned). */
 Q4_API q4_status q4_quantize_rows_asym(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x,
                                        uint8_t* codes, float* scales, float* zeros, void* stream);
 Q4_API q4_status q4_weight_code_sums(const uint8_t* w_codes, int64_t N, int64_t K, float* sums,
@@ -212,7 +221,11 @@ Q4_API q4_status q4_weight_code_sums(const uint8_t* w_codes, int64_t N, int64_t 
 Q4_API q4_status q4_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales,
                                      const float* a_zeros, const uint8_t* w_codes,
                                      const float* w_scales, const float* w_sums, int64_t M, int64_t N,
-                                     int64_t K, const q4_epilogue* epi, void* stream);
+                                     int64_t K, const q4_epilogue* epi, void* workspace, size_t ws_bytes,
+                                     void* stream);
+Q4_API q4_status q4_attention_f16_q4_asym(const uint16_t* qkv, int64_t B, int64_t S, int32_t heads,
+                                          int32_t head_dim, uint16_t* ctx_f16, uint8_t* ctx_codes,
+                                          float* ctx_scales, float* ctx_zeros, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * a2' Offline weight prepack (once per weight, not on the forward path): packed INT4 codes
@@ -261,6 +274,13 @@ typedef struct {
    * best small-batch strategy "q3" (only the MLP intermediate quantized) is 0xB.  W4A4
    * entry points only (the *_w8a8 ones require 0). */
   int32_t fp16_parts;
+  /* Asymmetric activations: 1 = every activation
+   * quantize of the layer is q4_quantize_rows_asym's (unsigned codes, scales, zeros) -- the
+   * layer-0 input, the attention ctx codes and the three requantizing epilogues -- and the four
+   * linears run q4_w4a4_asym_linear with the weight code sums (cqkv/co/c1/c2).  Requires
+   * fp16_parts == 0; the single-layer entry is q4_encoder_layer_asym; q4_encoder_stack(_w4a4)
+   * and q4_encoder_pipeline honour it; the *_w8a8 entry points require 0. */
+  int32_t asym_acts;
 } q4_layer_cfg;
 typedef struct {
   const uint8_t *wqkv, *wo, *w1, *w2;   /* packed [3h,h/2], [h,h/2], [ffn,h/2], [h,ffn/2] */
@@ -270,14 +290,24 @@ typedef struct {
   const uint16_t *ln1_g, *ln1_b, *ln2_g, *ln2_b;
   const uint16_t *fqkv, *fo, *f1, *f2;  /* fp16 [N, K] weights of the FP16 parts (cfg->fp16_parts);
                                            NULL when the part is quantized               */
+  const float *cqkv, *co, *c1, *c2;     /* cfg->asym_acts: per-output-channel weight code sums
+                                           (q4_weight_code_sums), 16-byte aligned; else NULL  */
 } q4_layer_weights;
 typedef struct {
   uint16_t *qkv, *ctx, *h1, *ffn1;
   int32_t *acc_qkv, *acc_o, *acc_1, *acc_2;
   uint8_t *ctx_codes, *h1_codes, *f_codes;
   float *ctx_scales, *h1_scales, *f_scales;
+  float *ctx_zeros, *h1_zeros, *f_zeros;  /* asymmetric layer: zero points of the codes above */
 } q4_taps;
 Q4_API size_t q4_encoder_layer_workspace(const q4_layer_cfg* cfg, int64_t B, int64_t S);
+/* The asymmetric layer (cfg->asym_acts = 1): (hq_in, hs_in, hz_in) = q4_quantize_rows_asym(h_in)
+ * or the previous asymmetric layer's output; writes (hq_out, hs_out, hz_out) likewise. */
+Q4_API q4_status q4_encoder_layer_asym(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B,
+                                       int64_t S, const uint16_t* h_in, const uint8_t* hq_in,
+                                       const float* hs_in, const float* hz_in, uint16_t* h_out,
+                                       uint8_t* hq_out, float* hs_out, float* hz_out, void* workspace,
+                                       size_t ws_bytes, const q4_taps* taps, void* stream);
 Q4_API q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B,
                            int64_t S, const uint16_t* h_in, const uint8_t* hq_in,
                            const float* hs_in, uint16_t* h_out, uint8_t* hq_out, float* hs_out,

@@ -25,7 +25,8 @@ EXPORTS = (
     "q4_attention_f16_q8", "q4_encoder_layer_w8a8_workspace", "q4_encoder_layer_w8a8",
     "q4_encoder_stack_w8a8_workspace", "q4_encoder_stack_w8a8", "q4_f16_linear_workspace", "q4_f16_linear",
     "q4_quantize_rows_asym", "q4_weight_code_sums", "q4_w4a4_asym_linear",
-    "q4_encoder_pipeline_workspace", "q4_encoder_pipeline", "q4_launch_floor",
+    "q4_encoder_pipeline_workspace", "q4_encoder_pipeline", "q4_launch_floor", "q4_attention_f16_q4_asym",
+    "q4_encoder_layer_asym",
 )
 
 
@@ -41,19 +42,20 @@ class Epilogue(C.Structure):
         ("bias", C.c_void_p), ("residual", C.c_void_p), ("gamma", C.c_void_p), ("beta", C.c_void_p),
         ("ln_eps", C.c_float), ("requant_clip", C.c_float),
         ("out_i32", C.c_void_p), ("out_f16", C.c_void_p), ("out_codes", C.c_void_p),
-        ("out_scales", C.c_void_p), ("w_i8", C.c_void_p),
+        ("out_scales", C.c_void_p), ("w_i8", C.c_void_p), ("out_zeros", C.c_void_p),
     ]
 
 
 class LayerCfg(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("heads", C.c_int32), ("head_dim", C.c_int32),
-                ("ffn", C.c_int32), ("ln_eps", C.c_float), ("fp16_parts", C.c_int32)]
+                ("ffn", C.c_int32), ("ln_eps", C.c_float), ("fp16_parts", C.c_int32), ("asym_acts", C.c_int32)]
 
 
 WEIGHT_FIELDS = ("wqkv", "wo", "w1", "w2", "wqkv8", "wo8", "w18", "w28", "sqkv", "so", "s1", "s2",
-                 "bqkv", "bo", "b1", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b", "fqkv", "fo", "f1", "f2")
+                 "bqkv", "bo", "b1", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b", "fqkv", "fo", "f1", "f2",
+                 "cqkv", "co", "c1", "c2")
 TAP_FIELDS = ("qkv", "ctx", "h1", "ffn1", "acc_qkv", "acc_o", "acc_1", "acc_2", "ctx_codes",
-              "h1_codes", "f_codes", "ctx_scales", "h1_scales", "f_scales")
+              "h1_codes", "f_codes", "ctx_scales", "h1_scales", "f_scales", "ctx_zeros", "h1_zeros", "f_zeros")
 
 
 class LayerWeights(C.Structure):
@@ -107,7 +109,10 @@ def lib():
         L.q4_encoder_pipeline.argtypes = [C.POINTER(LayerCfg), C.POINTER(LayerWeights), I32, I64, I64, P, P, I32,
                                           P, SZ, P]
         L.q4_weight_code_sums.argtypes = [P, I64, I64, P, P]
-        L.q4_w4a4_asym_linear.argtypes = [P, P, P, P, P, P, I64, I64, I64, C.POINTER(Epilogue), P]
+        L.q4_w4a4_asym_linear.argtypes = [P, P, P, P, P, P, I64, I64, I64, C.POINTER(Epilogue), P, SZ, P]
+        L.q4_attention_f16_q4_asym.argtypes = [P, I64, I64, I32, I32, P, P, P, P, P]
+        L.q4_encoder_layer_asym.argtypes = [C.POINTER(LayerCfg), C.POINTER(LayerWeights), I64, I64, P, P, P, P,
+                                            P, P, P, P, P, SZ, C.POINTER(Taps), P]
         L.q4_encoder_layer_w8a8_workspace.argtypes = [C.POINTER(LayerCfg), I64, I64]
         L.q4_encoder_layer_w8a8_workspace.restype = SZ
         L.q4_encoder_layer_w8a8.argtypes = L.q4_encoder_layer.argtypes

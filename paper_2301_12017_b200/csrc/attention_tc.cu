@@ -32,8 +32,8 @@ constexpr int NST = 2;                        // Q/K/V ring stages (2 CTAs per S
 constexpr int TILE = 128 * 128;               // bytes of one [128 x 64] fp16 tile
 constexpr int STAGE = 3 * TILE;               // Q | K | V
 constexpr int OFF_SLAB = NST * STAGE;         // 8 warps x 16 rows x 64 B
-constexpr int OFF_RED = OFF_SLAB + 8 * 1024;  // [2 halves][128] row partials
-constexpr int OFF_BAR = OFF_RED + 2 * 128 * 4;
+constexpr int OFF_RED = OFF_SLAB + 8 * 1024;  // [2 halves][128] max-abs | asym: [2][128] min | [2][128] max
+constexpr int OFF_BAR = OFF_RED + 6 * 128 * 4;
 constexpr int SMEM_AT = OFF_BAR + 256 + 1024;
 
 // kind::f16 instruction descriptor: f16 x f16 -> f32, A K-major, B K-major (b_mn = 0) or
@@ -67,7 +67,8 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
 __global__ void __launch_bounds__(AT_THREADS, 2)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tq, int S, int heads, __half* __restrict__ ctx_f16,
                         uint8_t* __restrict__ ctx_codes, float* __restrict__ ctx_scales,
-                        unsigned long long* __restrict__ trace, int dbg, int G, int i8) {
+                        unsigned long long* __restrict__ trace, int dbg, int G, int i8,
+                        float* __restrict__ ctx_zeros) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* kv_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
   const int b = blockIdx.x / G, g = blockIdx.x % G;
   const int hpc = heads / G, j0 = g * hpc;
   const int row0 = b * S;  // first token of this sequence
+  const bool asym = ctx_zeros != nullptr;  // asymmetric ctx codes (NEXT-3)
 
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tq);
@@ -163,6 +165,8 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
     float* red = reinterpret_cast<float*>(smem + OFF_RED);  // [2][128]
     float inv = 0.f;
     float amax = 0.f;
+    // asymmetric ctx codes (NEXT-3, ctx_zeros != nullptr): running per-token min and max
+    float vmn = INFINITY, vmx = -INFINITY;
     // profiling only (Q4_TRACE): per-head stamps of thread 0 of CTAs < 512
     unsigned long long* tr = (trace && threadIdx.x == 0 && blockIdx.x < 512) ? trace + (size_t)blockIdx.x * 16 * 16 : nullptr;
     auto stamp = [&](int j, int k) {
@@ -264,6 +268,10 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
           hw[e] = pack_half2(y.x, y.y);
           // fp16 rounding is monotonic and odd, so max |fp16(y)| == fp16(max |y|) (rounded below)
           amax = fmaxf(amax, fmaxf(fabsf(y.x), fabsf(y.y)));
+          if (asym) {  // likewise min / max of fp16(y) == fp16 of the fp32 min / max
+            vmn = fminf(vmn, fminf(y.x, y.y));
+            vmx = fmaxf(vmx, fmaxf(y.x, y.y));
+          }
         }
         hw4[u] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
       }
@@ -302,6 +310,10 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
     // per-token quantize (R1-R3): full-row max-abs from both halves, then
     // warp w re-reads rows 16w..16w+15 (L2), and writes codes + scales
     red[hf * 128 + r] = __half2float(__float2half_rn(amax));
+    if (asym) {
+      red[256 + hf * 128 + r] = __half2float(__float2half_rn(vmn));
+      red[512 + hf * 128 + r] = __half2float(__float2half_rn(vmx));
+    }
     __threadfence_block();  // ctx rows written by the other half's warps are re-read below
     asm volatile("bar.sync 1, 256;" ::: "memory");
     if (G > 1) goto cluster_tail;  // the row max-abs spans the cluster: combined below
@@ -329,6 +341,21 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
         if (tok >= S) continue;
         const float a = fmaxf(red[tok], red[128 + tok]);
         const size_t grow = (size_t)row0 + tok;
+        if (asym) {  // O-15 on the fp16 ctx row: zero = min, scale = (max - min) / 15
+          const float mn = fminf(red[256 + tok], red[384 + tok]), mx = fmaxf(red[512 + tok], red[640 + tok]);
+          uint32_t* cw = reinterpret_cast<uint32_t*>(ctx_codes + grow * (h / 2));
+          if (lane == 0) {
+            const double D = (double)mx - (double)mn;
+            ctx_scales[grow] = D > 0.0 ? (float)(D / 15.0) : 1.0f;
+            ctx_zeros[grow] = mn;
+          }
+          for (int c = lane; c < h / 8; c += 32) {
+            const uint4 x = *reinterpret_cast<const uint4*>(qb + rr * 2048 + c * 16);
+            const uint32_t hh[4] = {x.x, x.y, x.z, x.w};
+            cw[c] = requant8_asym(hh, mn, mx);
+          }
+          continue;
+        }
         if (i8) {  // W8A8 baseline: int8 codes, scale amax/127 (oracle O-11)
           uint2* c8 = reinterpret_cast<uint2*>(ctx_codes + grow * h);
           if (lane == 0) ctx_scales[grow] = a > 0.f ? __fdiv_rn(a, 127.0f) : 1.0f;
@@ -395,22 +422,38 @@ cluster_tail:
     float* amx = reinterpret_cast<float*>(smem + OFF_SLAB);       // [128] combined max-abs
     float* rr7 = amx + 128;                                       // [128] 7 / amax
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    float* zmn = rr7 + 128;                                       // [128] asym: min
+    float* zmx = zmn + 128;                                       // [128] asym: max
     if (threadIdx.x < 128) {
       const int r = threadIdx.x;
-      float a = 0.f;
-      for (int c = 0; c < G; ++c) {
-        uint32_t ra, rb;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(red + r)), "r"(c));
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(red + 128 + r)), "r"(c));
-        float x, y;
+      float a = 0.f, mn = INFINITY, mx = -INFINITY;
+      auto rd = [&](const float* loc, int c) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(loc)), "r"(c));
+        float x;
         asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(ra) : "memory");
-        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(y) : "r"(rb) : "memory");
-        a = fmaxf(a, fmaxf(x, y));
+        return x;
+      };
+      for (int c = 0; c < G; ++c) {
+        a = fmaxf(a, fmaxf(rd(red + r, c), rd(red + 128 + r, c)));
+        if (asym) {
+          mn = fminf(mn, fminf(rd(red + 256 + r, c), rd(red + 384 + r, c)));
+          mx = fmaxf(mx, fmaxf(rd(red + 512 + r, c), rd(red + 640 + r, c)));
+        }
+      }
+      if (asym) {
+        zmn[r] = mn;
+        zmx[r] = mx;
+        if (g == 0 && r < S) {
+          const double D = (double)mx - (double)mn;
+          ctx_scales[row0 + r] = D > 0.0 ? (float)(D / 15.0) : 1.0f;
+          ctx_zeros[row0 + r] = mn;
+        }
       }
       const float qm = i8 ? 127.0f : 7.0f;
       amx[r] = a;
       rr7[r] = a > 0.f ? __fdiv_rn(qm, a) : 0.f;
-      if (g == 0 && r < S) ctx_scales[row0 + r] = a > 0.f ? __fdiv_rn(a, qm) : 1.0f;
+      if (g == 0 && r < S && !asym) ctx_scales[row0 + r] = a > 0.f ? __fdiv_rn(a, qm) : 1.0f;
     }
     __syncthreads();
     // this CTA's columns [64 j0, 64 (j0 + hpc)): cpr 16-byte chunks (8 values) per row; eight
@@ -433,7 +476,9 @@ cluster_tail:
         const int rw = idx / cpr, c = idx - rw * cpr;
         const float a = amx[rw];
         const uint32_t hh[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
-        if (i8)
+        if (asym)
+          reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] = requant8_asym(hh, zmn[rw], zmx[rw]);
+        else if (i8)
           reinterpret_cast<uint2*>(ctx_codes + (size_t)(row0 + rw) * h + j0 * 64)[c] = requant8_i8(hh, a, rr7[rw], 0.f);
         else
           reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] =
@@ -448,7 +493,7 @@ cluster_tail:
 }
 
 cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __half* ctx_f16, uint8_t* ctx_codes,
-                                float* ctx_scales, cudaStream_t s, bool i8) {
+                                float* ctx_scales, cudaStream_t s, bool i8, float* ctx_zeros) {
   if (B == 0) return cudaSuccess;
   static EncodeFn enc = nullptr;
   if (!enc) {
@@ -504,7 +549,7 @@ cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __ha
   static const bool no_pdl = prof_env("Q4_NO_PDL") != nullptr;  // profiling only
   cfg.numAttrs = (no_pdl || (int64_t)B * S > kPdlMaxRows) ? 1 : 2;
   cudaError_t le = cudaLaunchKernelEx(&cfg, attention_tc_kernel, tq, S, heads, ctx_f16, ctx_codes, ctx_scales,
-                                      trace_path ? trace_buf : nullptr, dbg, G, i8 ? 1 : 0);
+                                      trace_path ? trace_buf : nullptr, dbg, G, i8 ? 1 : 0, ctx_zeros);
   if (le != cudaSuccess) return le;
   if (trace_path) {  // profiling only: dump this launch's stamps
     static unsigned long long host[512 * 16 * 16];

@@ -488,8 +488,11 @@ Q4_DEV void tmem_wait_ld_dep(uint32_t (&v)[16]) {
 // the fp64 erf form in this float32 evaluation order, 1/24 of the 1e-3 absolute parity budget).
 // The 8 pairs advance in lockstep, one Horner step for all of them at a time: 8 independent
 // chains per step instead of the compiler's register-bound interleave.
-template <bool FACC>
-Q4_DEV void gelu16(const uint32_t (&v)[16], float2 sa2, const float* sw, const float* bs, uint32_t (&h)[8]) {
+// ASYM (asymmetric activations, O-16): t = sw (sa acc + za colsum) + b with the per-column
+// weight-code sums at `cs`.
+template <bool FACC, bool ASYM = false>
+Q4_DEV void gelu16(const uint32_t (&v)[16], float2 sa2, const float* sw, const float* bs, uint32_t (&h)[8],
+                   float2 za2 = make_float2(0.f, 0.f), const float* cs = nullptr) {
   constexpr float HI = 4.5f, H2 = 2.25f;
   const float4* pw = reinterpret_cast<const float4*>(sw);
   const float4* pb = reinterpret_cast<const float4*>(bs);
@@ -501,8 +504,15 @@ Q4_DEV void gelu16(const uint32_t (&v)[16], float2 sa2, const float* sw, const f
                            : make_float2((float)(int)v[4 * j], (float)(int)v[4 * j + 1]);
     const float2 a1 = FACC ? make_float2(__uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]))
                            : make_float2((float)(int)v[4 * j + 2], (float)(int)v[4 * j + 3]);
-    t[2 * j] = ffma2(fmul2(a0, sa2), make_float2(w.x, w.y), make_float2(bb.x, bb.y));
-    t[2 * j + 1] = ffma2(fmul2(a1, sa2), make_float2(w.z, w.w), make_float2(bb.z, bb.w));
+    if constexpr (ASYM) {
+      const float4 c = reinterpret_cast<const float4*>(cs)[j];
+      t[2 * j] = ffma2(ffma2(a0, sa2, fmul2(za2, make_float2(c.x, c.y))), make_float2(w.x, w.y), make_float2(bb.x, bb.y));
+      t[2 * j + 1] = ffma2(ffma2(a1, sa2, fmul2(za2, make_float2(c.z, c.w))), make_float2(w.z, w.w),
+                           make_float2(bb.z, bb.w));
+    } else {
+      t[2 * j] = ffma2(fmul2(a0, sa2), make_float2(w.x, w.y), make_float2(bb.x, bb.y));
+      t[2 * j + 1] = ffma2(fmul2(a1, sa2), make_float2(w.z, w.w), make_float2(bb.z, bb.w));
+    }
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j)
@@ -527,6 +537,37 @@ Q4_DEV void gelu16(const uint32_t (&v)[16], float2 sa2, const float* sw, const f
     const float2 y = ffma2(tn, qv, make_float2(fmaxf(t[j].x, 0.f), fmaxf(t[j].y, 0.f)));
     h[j] = pack_half2(y.x, y.y);
   }
+}
+
+// Asymmetric INT4 code of fp16 value x (as float) given the row min mn and D = max - min > 0
+// (NEXT-3, oracle O-15; readings R17/R18): q = rhe(15 (x - mn) / D) in [0, 15].  x - mn and D
+// are differences of fp16 values, exact in fp64 (<= 41 significant bits), so p = d * (15/D) is
+// within 1e-14 of the rational; near a half-integer the exact residual 15 d - D h decides.
+Q4_DEV uint32_t asym_code(float x, double mn, double D, double r15) {
+  const double d = (double)x - mn;
+  const double p = d * r15;
+  double n = rint(p);
+  if (fabs(p - n) > 0.4999999) {
+    const double h = floor(p) + 0.5;
+    const double e = fma(-D, h, 15.0 * d);
+    n = e > 0.0 ? h + 0.5 : (e < 0.0 ? h - 0.5 : (fmod(h - 0.5, 2.0) == 0.0 ? h - 0.5 : h + 0.5));
+  }
+  return (uint32_t)(int)fmin(n, 15.0);
+}
+// 8 fp16 values (4 packed words) -> 8 asymmetric codes in one word (element i at bits 4i);
+// D <= 0 (constant row) gives all-zero codes.
+Q4_DEV uint32_t requant8_asym(const uint32_t (&h)[4], float mn, float mx) {
+  const double D = (double)mx - (double)mn;
+  if (!(D > 0.0)) return 0u;
+  const double r15 = 15.0 / D, m = (double)mn;
+  uint32_t w = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = unpack_half2(h[j]);
+    w |= asym_code(f.x, m, D, r15) << (8 * j);
+    w |= asym_code(f.y, m, D, r15) << (8 * j + 4);
+  }
+  return w;
 }
 
 }  // namespace q4

@@ -32,6 +32,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "../../include/q4.h"
 #include "kernels.h"
@@ -63,6 +64,8 @@ struct TcParams {
   __half* out_f16;
   uint8_t* out_codes;
   float* out_scales;
+  float* out_zeros;   // asymmetric requant output (NEXT-3): per-row zero point; nullptr = symmetric
+  float2* xmm;        // asymmetric requant: [mblocks][ntn][128] (min, max) partials
   float2* xstat;      // [mblocks][ntn][128] (mean, M2) partials
   float* xamax;       // [mblocks][ntn][128] max-abs partials
   unsigned* xcnt;     // [4][mblocks] arrival / departure counters (self-resetting; zero on entry)
@@ -117,8 +120,8 @@ struct TcCfg {
   static constexpr int OFF_PK = SU * UN_STAGE;
   static constexpr int NSLAB = R4 ? 16 : 8;              // 4 KB staging slabs: per warp (R4) or warp pair
   static constexpr int OFF_STG = OFF_PK + SP * PK_STAGE;
-  static constexpr int OFF_PRM = OFF_STG + NSLAB * 4096;  // [R4 ? 4 groups : 1][4][TN] fp32 column params
-  static constexpr int OFF_ROW = OFF_PRM + (R4 ? 4 : 1) * 4 * TN * 4;  // [2 groups][2 sides][128] float4 row partials
+  static constexpr int OFF_PRM = OFF_STG + NSLAB * 4096;  // [R4 ? 4 groups : 1][5][TN] fp32 column params
+  static constexpr int OFF_ROW = OFF_PRM + (R4 ? 4 : 1) * 5 * TN * 4;  // [2 groups][2 sides][128] float4 row partials
   static constexpr int OFF_BAR = OFF_ROW + (R4 ? 0 : 2 * 2 * 128 * 16);
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int NBUF = R4 ? 4 : 2;
@@ -903,11 +906,12 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
     const int N = p.N;
     const float clip = p.clip;
     // sw | bias | gamma | beta of this CTA's n-block (staged once) or, R4, of the group's tile
-    float* const prm0 = reinterpret_cast<float*>(smem + C::OFF_PRM) + (R4 ? grp * 4 * TN : 0);
+    float* const prm0 = reinterpret_cast<float*>(smem + C::OFF_PRM) + (R4 ? grp * 5 * TN : 0);
     auto load_prm = [&](int c0, int i) {
       prm0[i] = p.w_scales ? p.w_scales[c0 + i] : 1.0f;
       prm0[TN + i] = p.bias ? __half2float(p.bias[c0 + i]) : 0.f;
       if (KIND == EPI_F16 && p.a_zeros) prm0[2 * TN + i] = p.w_sums[c0 + i];
+      if (E::ROW && p.a_zeros) prm0[4 * TN + i] = p.w_sums[c0 + i];  // asymmetric input: colsum
       if constexpr (KIND == EPI_RESLN_Q4) {
         prm0[2 * TN + i] = __half2float(p.gamma[c0 + i]);
         prm0[3 * TN + i] = __half2float(p.beta[c0 + i]);
@@ -1015,6 +1019,10 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
           // pass 1: z = acc*sa*sw + b + residual -> TMEM (in place); moments shifted by a pivot.
           // The residual goes straight to registers, one chunk ahead of its use.
           float2 s1 = f2(0.f), s2 = f2(0.f), npiv = f2(0.f);
+          // asymmetric input (O-16: sa acc + za colsum) as a separate instantiation of the
+          // loop, so the symmetric path keeps its instruction count
+          auto pass1 = [&](auto asym_tag) {
+          constexpr bool AS = decltype(asym_tag)::value;
           for (int j = sub; j < NCH; j += NS) {
             uint32_t v[32];
             tmem_ld32(tbase + 32 * j, v);
@@ -1034,9 +1042,14 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
 #pragma unroll
               for (int hh = 0; hh < 2; ++hh) {
                 const int e = 4 * jj + 2 * hh;
-                const float2 t = ffma2(fmul2(H16 ? make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1]))
-                                                 : make_float2((float)(int)v[e], (float)(int)v[e + 1]), sa2),
-                                       hh ? make_float2(w.z, w.w) : make_float2(w.x, w.y),
+                const float2 av = H16 ? make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1]))
+                                      : make_float2((float)(int)v[e], (float)(int)v[e + 1]);
+                float2 sacc;
+                if constexpr (AS)
+                  sacc = ffma2(av, sa2, fmul2(za2, make_float2(prm[4 * TN + 32 * j + e], prm[4 * TN + 32 * j + e + 1])));
+                else
+                  sacc = fmul2(av, sa2);
+                const float2 t = ffma2(sacc, hh ? make_float2(w.z, w.w) : make_float2(w.x, w.y),
                                        hh ? make_float2(bb.z, bb.w) : make_float2(bb.x, bb.y));
                 const float2 z = add_half2_f32(ru[e / 2], t);
                 if (j == sub && e == 0) npiv = f2(-z.x);
@@ -1051,6 +1064,8 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
 #pragma unroll
             for (int u = 0; u < 4; ++u) rr[u] = rn[u];
           }
+          };
+          if (p.a_zeros) pass1(std::true_type{}); else pass1(std::false_type{});
           tmem_wait_st();
           stamp(2);
           {
@@ -1091,6 +1106,9 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
         }
         // pass A: y = fp16(GELU(t)) or fp16(LN(z)); row max-abs; y -> TMEM as packed halves
         __half2 hmax = __float2half2_rn(0.f);
+        // asymmetric output (NEXT-3): the row min and max of y instead of max |y|
+        const bool aout = !A8 && p.out_zeros != nullptr;
+        __half2 hmn = __float2half2_rn(65504.f), hmx = __float2half2_rn(-65504.f);
         const bool want_f16 = p.out_f16 != nullptr;
         const float2 nmean2 = f2(-mean), rstd2 = f2(rstd);
         for (int k = 0; k < NSL; ++k) {
@@ -1118,12 +1136,23 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
               uint32_t v0[16], v1[16], h0[8], h1[8];
 #pragma unroll
               for (int u = 0; u < 16; ++u) { v0[u] = v[u]; v1[u] = v[16 + u]; }
-              gelu16<H16>(v0, sa2, prm + 32 * j, prm + TN + 32 * j, h0);
-              gelu16<H16>(v1, sa2, prm + 32 * j + 16, prm + TN + 32 * j + 16, h1);
+              if (p.a_zeros) {  // asymmetric input (O-16)
+                gelu16<H16, true>(v0, sa2, prm + 32 * j, prm + TN + 32 * j, h0, za2, prm + 4 * TN + 32 * j);
+                gelu16<H16, true>(v1, sa2, prm + 32 * j + 16, prm + TN + 32 * j + 16, h1, za2, prm + 4 * TN + 32 * j + 16);
+              } else {
+                gelu16<H16>(v0, sa2, prm + 32 * j, prm + TN + 32 * j, h0);
+                gelu16<H16>(v1, sa2, prm + 32 * j + 16, prm + TN + 32 * j + 16, h1);
+              }
 #pragma unroll
               for (int u = 0; u < 8; ++u) { h[u] = h0[u]; h[8 + u] = h1[u]; }
             }
-            if (clip > 0.f) {
+            if (aout) {
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                hmn = __hmin2(hmn, *reinterpret_cast<const __half2*>(&h[u]));
+                hmx = __hmax2(hmx, *reinterpret_cast<const __half2*>(&h[u]));
+              }
+            } else if (clip > 0.f) {
               const __half2 cl = __float2half2_rn(clip);
 #pragma unroll
               for (int u = 0; u < 16; ++u)
@@ -1149,6 +1178,45 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
         }
         tmem_wait_st();
         stamp(4);
+        if (aout) {
+          // asymmetric requant (O-15 on the fp16 row): row (min, max) over the sides, then the ntn
+          // CTAs; codes = rhe(15 (y - min) / (max - min)) with the exact fp64 tie-break
+          float mn = fminf(__low2float(hmn), __high2float(hmn)), mx = fmaxf(__low2float(hmx), __high2float(hmx));
+          if constexpr (NS > 1) {
+            rowp[sub * 128 + r].z = mn;
+            rowp[sub * 128 + r].w = mx;
+            named_bar(gbar, GT);
+            mn = fminf(rowp[r].z, rowp[128 + r].z);
+            mx = fmaxf(rowp[r].w, rowp[128 + r].w);
+          }
+          if (sub == 0) p.xmm[((size_t)mb * ntn + nb) * 128 + r] = make_float2(mn, mx);
+          exchange_sync(p.xcnt + p.mblocks + mb, 2 * (size_t)p.mblocks, ntn, gbar, GT, leader, p.dbg);
+          for (int kk = 0; kk < ntn; ++kk) {
+            const float2 o = __ldcg(&p.xmm[((size_t)mb * ntn + kk) * 128 + r]);
+            mn = fminf(mn, o.x);
+            mx = fmaxf(mx, o.y);
+          }
+          for (int j = sub; j < NCH; j += NS) {
+            uint32_t h[16];
+            tmem_ld16(tbase + 32 * j, h);
+            tmem_wait_ld();
+            uint32_t w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t hk[4] = {h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]};
+              w[u] = requant8_asym(hk, mn, mx);
+            }
+            *reinterpret_cast<uint4*>(stg + slab_off(lane, j)) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+          slab_sync();
+          slab_store16(stg, p.out_codes, m0 + q * 32, RS * sub, RS, p.M, (size_t)N / 2, (size_t)c0 / 2, TN / 2, lane);
+          slab_sync();
+          if (row_ok && nb == 0 && sub == 0) {
+            const double D = (double)mx - (double)mn;
+            p.out_scales[gm] = D > 0.0 ? (float)(D / 15.0) : 1.0f;
+            p.out_zeros[gm] = mn;
+          }
+        } else {
         float amax = fmaxf(__low2float(hmax), __high2float(hmax));
         // row max-abs over the sides, then the ntn CTAs
         if constexpr (NS > 1) {
@@ -1199,6 +1267,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
         slab_store16(stg, p.out_codes, m0 + q * 32, RS * sub, RS, p.M, (size_t)N / 2, (size_t)c0 / 2, TN / 2, lane);
         slab_sync();
         if (row_ok && nb == 0 && sub == 0) p.out_scales[gm] = amax > 0.f ? __fdiv_rn(amax, 7.0f) : 1.0f;
+        }
         }
       }
       stamp(6);
@@ -1308,7 +1377,8 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.bias = g.bias; p.residual = g.residual; p.gamma = g.gamma; p.beta = g.beta;
   p.ln_eps = g.ln_eps; p.clip = g.clip;
   p.out_i32 = g.out_i32; p.out_f16 = g.out_f16; p.out_codes = g.out_codes; p.out_scales = g.out_scales;
-  p.xstat = nullptr; p.xamax = nullptr; p.xcnt = nullptr; p.yscr = nullptr;
+  p.out_zeros = g.out_zeros;
+  p.xstat = nullptr; p.xamax = nullptr; p.xcnt = nullptr; p.yscr = nullptr; p.xmm = nullptr;
   static const int dbg = [] { const char* e = prof_env("Q4_DEBUG_SKIP"); return e ? atoi(e) : 0; }();
   p.dbg = dbg;
   p.trace = nullptr;
@@ -1364,7 +1434,8 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     p.xcnt = reinterpret_cast<unsigned*>(w);
     p.xstat = reinterpret_cast<float2*>(w + cnt_bytes);
     p.xamax = reinterpret_cast<float*>(w + cnt_bytes + nslot * 8);
-    p.yscr = KIND == EPI_GELU_Q4 ? reinterpret_cast<__half*>(w + cnt_bytes + nslot * 12) : nullptr;
+    p.xmm = reinterpret_cast<float2*>(w + cnt_bytes + nslot * 12);
+    p.yscr = KIND == EPI_GELU_Q4 ? reinterpret_cast<__half*>(w + cnt_bytes + nslot * 20) : nullptr;
     if (KIND == EPI_GELU_Q4 && Q4_GELU_DECOUPLED && (size_t)grid > tc_row_grid(g.M, g.N, TN)) {
       *why = "row-epilogue grid larger than the workspace sizing assumed";
       return cudaErrorInvalidValue;
@@ -1502,7 +1573,7 @@ size_t tc_workspace_bytes(int M, int N, int TN, int kind) {
   if (TN <= 0) return 0;
   // partial slots for ntn = N / min(TN, 128): the R4 row kernel (TN = 128) may run instead
   const size_t mblocks = (size_t)(M + 127) / 128, ntn = (size_t)N / (TN < 128 ? TN : 128);
-  size_t b = tc_counter_bytes(M) + mblocks * ntn * 128 * 12;
+  size_t b = tc_counter_bytes(M) + mblocks * ntn * 128 * 20;  // stats (8) | amax (4) | asym min/max (8)
   // GELU_Q4: two y parking slots per epilogue group (pass B of tile t runs after pass A of t + 2)
   if (kind == EPI_GELU_Q4 && Q4_GELU_DECOUPLED) b += tc_row_grid(M, N, TN) * 4 * 128 * (size_t)TN * 2;
   return b;

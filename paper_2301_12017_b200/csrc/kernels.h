@@ -51,6 +51,7 @@ struct GemmArgs {
                            // in natural K order and requant kinds write int8 codes [M, N]); else nullptr
   const float* a_zeros = nullptr;  // asymmetric activations: per-row zero point; a_codes unsigned nibbles
   const float* w_sums = nullptr;   // with a_zeros: per-output-channel weight-code sums (as float)
+  float* out_zeros = nullptr;      // GELU_Q4 / RESLN_Q4: asymmetric requant output (zero points)
   bool f16_ops = false;    // with a_i8 / w_i8 pointing at fp16 [M, K] / [N, K] and K counted in
                            // bytes (2 x elements): kind::f16 MMA, unit scales, INT4 requant
   const float* a_scales;   // [M]
@@ -90,6 +91,7 @@ cudaError_t launch_floor_kernel(int ctas, cudaStream_t s);  // empty PDL kernel 
 cudaError_t launch_w4a4_legacy(const GemmArgs& g, bool s4, cudaStream_t s, const char** why);
 // i8: W8A8 baseline -- int8 ctx codes [B*S, h] with scale amax/127 instead of packed INT4
 cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __half* ctx_f16,
-                                uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s, bool i8 = false);
+                                uint8_t* ctx_codes, float* ctx_scales, cudaStream_t s, bool i8 = false,
+                                float* ctx_zeros = nullptr);
 
 }  // namespace q4

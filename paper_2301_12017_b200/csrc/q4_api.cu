@@ -199,16 +199,16 @@ q4_status q4_weight_code_sums(const uint8_t* w_codes, int64_t N, int64_t K, floa
 
 q4_status q4_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales, const float* a_zeros,
                               const uint8_t* w_codes, const float* w_scales, const float* w_sums, int64_t M, int64_t N,
-                              int64_t K, const q4_epilogue* epi, void* stream) {
+                              int64_t K, const q4_epilogue* epi, void* workspace, size_t ws_bytes, void* stream) {
   g_err[0] = 0;
   if (!epi) return fail(Q4_EINVAL, "q4_w4a4_asym_linear: epi is NULL");
-  if (epi->kind != Q4_EPI_F16 && epi->kind != Q4_EPI_I32)
-    return fail(Q4_EUNSUPPORTED, "q4_w4a4_asym_linear: epilogue kind %d (F16 or I32)", epi->kind);
+  const int kind = epi->kind;
+  if (kind < Q4_EPI_I32 || kind > Q4_EPI_RESLN_Q4) return fail(Q4_EINVAL, "q4_w4a4_asym_linear: unknown epilogue kind %d", kind);
   if (epi->mainloop != Q4_MAINLOOP_AUTO && epi->mainloop != Q4_MAINLOOP_TCGEN05 && epi->mainloop != Q4_MAINLOOP_TCGEN05_W8)
     return fail(Q4_EUNSUPPORTED, "q4_w4a4_asym_linear: mainloop %d (tcgen05 only)", epi->mainloop);
-  if (!a_zeros || (epi->kind == Q4_EPI_F16 && !w_sums))
+  if (!a_zeros || (kind != Q4_EPI_I32 && !w_sums))
     return fail(Q4_EINVAL, "q4_w4a4_asym_linear: NULL a_zeros / w_sums");
-  if (epi->kind == Q4_EPI_F16 && !al16(w_sums)) return fail(Q4_EALIGN, "q4_w4a4_asym_linear: w_sums 16-byte aligned");
+  if (kind != Q4_EPI_I32 && !al16(w_sums)) return fail(Q4_EALIGN, "q4_w4a4_asym_linear: w_sums 16-byte aligned");
   // the validation of q4_w4a4_linear with the asymmetric fields set
   if (M < 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1 << 24) || N % 32 || K % 32 || K > 8192)
     return fail(Q4_ESHAPE, "q4_w4a4_asym_linear: M=%lld N=%lld K=%lld (N %% 32 == 0, K %% 32 == 0, K <= 8192)",
@@ -218,25 +218,56 @@ q4_status q4_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales, con
     return fail(Q4_EINVAL, "q4_w4a4_asym_linear: NULL operand (a_codes/a_scales/w_codes/w_scales)");
   if (!al16(a_codes) || !al16(w_codes) || !al16(w_scales) || !al4(a_scales) || !al4(a_zeros))
     return fail(Q4_EALIGN, "q4_w4a4_asym_linear: codes / w_scales 16-byte aligned, a_scales / a_zeros 4-byte aligned");
-  if (epi->bias && !al4(epi->bias)) return fail(Q4_EALIGN, "q4_w4a4_asym_linear: bias must be 4-byte aligned");
+  if ((epi->bias && !al4(epi->bias)) || (epi->gamma && !al4(epi->gamma)) || (epi->beta && !al4(epi->beta)))
+    return fail(Q4_EALIGN, "q4_w4a4_asym_linear: bias/gamma/beta must be 4-byte aligned");
   if (epi->mainloop == Q4_MAINLOOP_TCGEN05_W8 && (!epi->w_i8 || !al16(epi->w_i8)))
     return fail(Q4_EINVAL, "q4_w4a4_asym_linear: TCGEN05_W8 needs 16-byte aligned epi->w_i8 (q4_prepack_weights)");
   if (epi->mainloop == Q4_MAINLOOP_AUTO && epi->w_i8 && !al16(epi->w_i8))
     return fail(Q4_EALIGN, "q4_w4a4_asym_linear: epi->w_i8 must be 16-byte aligned");
-  if ((epi->kind == Q4_EPI_F16 && (!epi->out_f16 || !al16(epi->out_f16))) ||
-      (epi->kind == Q4_EPI_I32 && (!epi->out_i32 || !al16(epi->out_i32))))
-    return fail(Q4_EINVAL, "q4_w4a4_asym_linear: output NULL or not 16-byte aligned");
+  switch (kind) {
+    case Q4_EPI_I32:
+      if (!epi->out_i32 || !al16(epi->out_i32)) return fail(Q4_EINVAL, "q4_w4a4_asym_linear(I32): out_i32 NULL or not 16-byte aligned");
+      break;
+    case Q4_EPI_F16:
+      if (!epi->out_f16 || !al16(epi->out_f16)) return fail(Q4_EINVAL, "q4_w4a4_asym_linear(F16): out_f16 NULL or not 16-byte aligned");
+      break;
+    case Q4_EPI_GELU_Q4:
+      if (!epi->out_codes || !epi->out_scales) return fail(Q4_EINVAL, "q4_w4a4_asym_linear(GELU_Q4): out_codes/out_scales NULL");
+      if (!al16(epi->out_codes) || (epi->out_f16 && !al16(epi->out_f16)))
+        return fail(Q4_EALIGN, "q4_w4a4_asym_linear(GELU_Q4): outputs must be 16-byte aligned");
+      break;
+    case Q4_EPI_RESLN_Q4:
+      if (!epi->out_codes || !epi->out_scales || !epi->out_f16 || !epi->residual || !epi->gamma || !epi->beta)
+        return fail(Q4_EINVAL, "q4_w4a4_asym_linear(RESLN_Q4): out_f16/out_codes/out_scales/residual/gamma/beta must be non-NULL");
+      if (!al16(epi->out_codes) || !al16(epi->out_f16) || !al16(epi->residual))
+        return fail(Q4_EALIGN, "q4_w4a4_asym_linear(RESLN_Q4): out_f16/out_codes/residual must be 16-byte aligned");
+      if (!(epi->ln_eps >= 0.f)) return fail(Q4_EINVAL, "q4_w4a4_asym_linear(RESLN_Q4): ln_eps=%g", epi->ln_eps);
+      break;
+  }
+  if (epi->requant_clip != 0.f) return fail(Q4_EUNSUPPORTED, "q4_w4a4_asym_linear: requant_clip must be 0");
+  if (kind == Q4_EPI_GELU_Q4 || kind == Q4_EPI_RESLN_Q4) {
+    if (N % 64) return fail(Q4_ESHAPE, "q4_w4a4_asym_linear: N=%lld must be a multiple of 64 for row epilogues", (long long)N);
+    if (epi->out_zeros && !al4(epi->out_zeros)) return fail(Q4_EALIGN, "q4_w4a4_asym_linear: out_zeros 4-byte aligned");
+    const size_t need = q4_w4a4_linear_workspace(M, N, K, kind);
+    if (!workspace || ws_bytes < need)
+      return fail(Q4_EINVAL, "q4_w4a4_asym_linear: workspace %zu bytes < required %zu (q4_w4a4_linear_workspace)", ws_bytes, need);
+    if (!al16(workspace)) return fail(Q4_EALIGN, "q4_w4a4_asym_linear: workspace must be 16-byte aligned");
+  }
   q4::GemmArgs g;
   g.a_codes = a_codes; g.a_i8 = nullptr; g.a_scales = a_scales; g.w_codes = w_codes; g.w_scales = w_scales;
   g.a_zeros = a_zeros; g.w_sums = w_sums;
-  g.M = (int)M; g.N = (int)N; g.K = (int)K; g.kind = epi->kind; g.mainloop = epi->mainloop;
+  g.M = (int)M; g.N = (int)N; g.K = (int)K; g.kind = kind; g.mainloop = epi->mainloop;
   g.bias = reinterpret_cast<const __half*>(epi->bias);
-  g.residual = nullptr; g.gamma = nullptr; g.beta = nullptr; g.ln_eps = 0.f; g.clip = 0.f;
-  g.out_i32 = epi->out_i32; g.out_f16 = reinterpret_cast<__half*>(epi->out_f16); g.out_codes = nullptr;
-  g.out_scales = nullptr;
+  g.residual = reinterpret_cast<const __half*>(epi->residual);
+  g.gamma = reinterpret_cast<const __half*>(epi->gamma);
+  g.beta = reinterpret_cast<const __half*>(epi->beta);
+  g.ln_eps = epi->ln_eps; g.clip = 0.f;
+  g.out_i32 = epi->out_i32; g.out_f16 = reinterpret_cast<__half*>(epi->out_f16); g.out_codes = epi->out_codes;
+  g.out_scales = epi->out_scales;
+  g.out_zeros = (kind == Q4_EPI_GELU_Q4 || kind == Q4_EPI_RESLN_Q4) ? epi->out_zeros : nullptr;
   g.w_i8 = (epi->mainloop != Q4_MAINLOOP_TCGEN05 && epi->w_i8) ? epi->w_i8 : nullptr;
   const char* why = "";
-  cudaError_t e = q4::launch_w4a4_tc(g, nullptr, 0, (cudaStream_t)stream, &why);
+  cudaError_t e = q4::launch_w4a4_tc(g, workspace, ws_bytes, (cudaStream_t)stream, &why);
   if (e == cudaErrorNotSupported) return fail(Q4_EUNSUPPORTED, "q4_w4a4_asym_linear: %s", why);
   if (e != cudaSuccess) return fail(Q4_ECUDA, "q4_w4a4_asym_linear: %s %s", cudaGetErrorString(e), why);
   return Q4_OK;
@@ -369,6 +400,11 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
   g.ln_eps = epi->ln_eps; g.clip = epi->requant_clip;
   g.out_i32 = epi->out_i32; g.out_f16 = reinterpret_cast<__half*>(epi->out_f16);
   g.out_codes = epi->out_codes; g.out_scales = epi->out_scales;
+  g.out_zeros = (kind == Q4_EPI_GELU_Q4 || kind == Q4_EPI_RESLN_Q4) ? epi->out_zeros : nullptr;
+  if (g.out_zeros && (epi->requant_clip != 0.f || !al4(g.out_zeros)))
+    return fail(Q4_EUNSUPPORTED, "q4_w4a4_linear: asymmetric requant (out_zeros) needs requant_clip 0 and 4-byte aligned zeros");
+  if (g.out_zeros && (epi->mainloop == Q4_MAINLOOP_MMA_SYNC_S8 || epi->mainloop == Q4_MAINLOOP_MMA_SYNC_S4))
+    return fail(Q4_EUNSUPPORTED, "q4_w4a4_linear: asymmetric requant on the tcgen05 mainloops only");
   g.w_i8 = nullptr;
   if (epi->mainloop == Q4_MAINLOOP_TCGEN05_W8 || epi->mainloop == Q4_MAINLOOP_TCGEN05_W8_1CTA ||
       (epi->mainloop == Q4_MAINLOOP_AUTO && epi->w_i8)) {
@@ -420,6 +456,25 @@ q4_status q4_attention_f16_q4(const uint16_t* qkv, int64_t B, int64_t S, int32_t
   return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_attention_f16_q4");
 }
 
+q4_status q4_attention_f16_q4_asym(const uint16_t* qkv, int64_t B, int64_t S, int32_t heads, int32_t head_dim,
+                                   uint16_t* ctx_f16, uint8_t* ctx_codes, float* ctx_scales, float* ctx_zeros,
+                                   void* stream) {
+  g_err[0] = 0;
+  if (head_dim != 64) return fail(Q4_EUNSUPPORTED, "q4_attention_f16_q4_asym: head_dim=%d (only 64)", head_dim);
+  if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "q4_attention_f16_q4_asym: B=%lld S=%lld (need B>=0, 1<=S<=128)", (long long)B, (long long)S);
+  if (heads < 1 || heads * 64 > 1024) return fail(Q4_ESHAPE, "q4_attention_f16_q4_asym: heads=%d (need 1..16)", heads);
+  if (B > 65535) return fail(Q4_ESHAPE, "q4_attention_f16_q4_asym: B=%lld > 65535", (long long)B);
+  if (B == 0) return Q4_OK;
+  if (!qkv || !ctx_f16 || !ctx_codes || !ctx_scales || !ctx_zeros)
+    return fail(Q4_EINVAL, "q4_attention_f16_q4_asym: NULL qkv/ctx_f16/ctx_codes/ctx_scales/ctx_zeros");
+  if (!al16(qkv) || !al4(ctx_codes) || !al16(ctx_f16) || !al4(ctx_zeros))
+    return fail(Q4_EALIGN, "q4_attention_f16_q4_asym: qkv/ctx_f16 16-byte aligned, codes / zeros 4-byte");
+  cudaError_t e = q4::launch_attention_tc(reinterpret_cast<const __half*>(qkv), (int)B, (int)S, heads,
+                                          reinterpret_cast<__half*>(ctx_f16), ctx_codes, ctx_scales,
+                                          (cudaStream_t)stream, false, ctx_zeros);
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_attention_f16_q4_asym");
+}
+
 q4_status q4_attention_f16_q8(const uint16_t* qkv, int64_t B, int64_t S, int32_t heads, int32_t head_dim,
                               uint16_t* ctx_f16, int8_t* ctx_codes, float* ctx_scales, void* stream) {
   g_err[0] = 0;
@@ -453,6 +508,7 @@ struct LayerWs {
   float* h1_scales;
   uint8_t* f_codes;
   float* f_scales;
+  float *ctx_zeros, *h1_zeros, *f_zeros;  // asymmetric activations (cfg->asym_acts)
   uint16_t* ffn1;  // fp16 MLP intermediate, only when the MLP output part runs in FP16
   size_t bytes;
 };
@@ -479,6 +535,10 @@ LayerWs layer_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base, bool i8 = fals
   w.h1_scales = (float*)take((size_t)M * 4);
   w.f_codes = take((size_t)(M * f / cd));
   w.f_scales = (float*)take((size_t)M * 4);
+  const bool az = !i8 && c->asym_acts;
+  w.ctx_zeros = az ? (float*)take((size_t)M * 4) : nullptr;
+  w.h1_zeros = az ? (float*)take((size_t)M * 4) : nullptr;
+  w.f_zeros = az ? (float*)take((size_t)M * 4) : nullptr;
   w.ffn1 = (!i8 && (c->fp16_parts & 8)) ? (uint16_t*)take((size_t)M * f * 2) : nullptr;
   w.bytes = o;
   return w;
@@ -490,6 +550,10 @@ q4_status check_cfg(const q4_layer_cfg* c, const char* who) {
                 who, c->hidden, c->heads, c->head_dim);
   if (c->ffn % 32 || c->ffn <= 0 || c->ffn > 4096) return fail(Q4_ESHAPE, "%s: ffn=%d (need multiple of 32, <= 4096)", who, c->ffn);
   if (c->fp16_parts < 0 || c->fp16_parts > 15) return fail(Q4_EINVAL, "%s: fp16_parts=%d (bits 0..3)", who, c->fp16_parts);
+  if (c->asym_acts != 0 && c->asym_acts != 1) return fail(Q4_EINVAL, "%s: asym_acts=%d (0 or 1)", who, c->asym_acts);
+  if (c->asym_acts && c->fp16_parts)
+    return fail(Q4_EUNSUPPORTED, "%s: asym_acts with fp16_parts=%d (the asymmetric layer quantizes all four parts)", who,
+                c->fp16_parts);
   return Q4_OK;
 }
 }  // namespace
@@ -512,11 +576,15 @@ namespace {
 q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B, int64_t S,
                              const uint16_t* h_in, const uint8_t* hq_in, const float* hs_in, uint16_t* h_out,
                              uint8_t* hq_out, float* hs_out, void* workspace, size_t ws_bytes, const q4_taps* taps,
-                             void* stream, bool i8) {
-  const char* who = i8 ? "q4_encoder_layer_w8a8" : "q4_encoder_layer";
+                             void* stream, bool i8, const float* hz_in = nullptr, float* hz_out = nullptr) {
+  const char* who = i8 ? "q4_encoder_layer_w8a8" : (cfg && cfg->asym_acts) ? "q4_encoder_layer_asym" : "q4_encoder_layer";
   q4_status st = check_cfg(cfg, who);
   if (st) return st;
   if (!w) return fail(Q4_EINVAL, "%s: weights NULL", who);
+  const bool asym = cfg->asym_acts != 0;
+  if (i8 && asym) return fail(Q4_EUNSUPPORTED, "%s: asym_acts on the W8A8 baseline", who);
+  if (asym && (!hz_in || !hz_out || !w->cqkv || !w->co || !w->c1 || !w->c2))
+    return fail(Q4_EINVAL, "%s: asym_acts needs hz_in / hz_out and the weight code sums cqkv/co/c1/c2", who);
   if (B < 0 || S < 1 || S > 128) return fail(Q4_ESHAPE, "%s: B=%lld S=%lld", who, (long long)B, (long long)S);
   const int64_t M = B * S, h = cfg->hidden, f = cfg->ffn;
   if (M == 0) return Q4_OK;
@@ -539,7 +607,26 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
   float* h1_scales = tp.h1_scales ? tp.h1_scales : ws.h1_scales;
   uint8_t* f_codes = tp.f_codes ? tp.f_codes : ws.f_codes;
   float* f_scales = tp.f_scales ? tp.f_scales : ws.f_scales;
+  float* ctx_zeros = tp.ctx_zeros ? tp.ctx_zeros : ws.ctx_zeros;
+  float* h1_zeros = tp.h1_zeros ? tp.h1_zeros : ws.h1_zeros;
+  float* f_zeros = tp.f_zeros ? tp.f_zeros : ws.f_zeros;
 
+  // asymmetric layer: (codes, scales, zeros) -> linear with the weight code sums; the
+  // requantizing epilogues write asymmetric codes (e.out_zeros set by the caller)
+  auto alin = [&](const uint8_t* ac, const float* as, const float* az, const uint8_t* wc, const float* wsc,
+                  const float* wsum, int64_t N, int64_t K, q4_epilogue e) -> q4_status {
+    return q4_w4a4_asym_linear(ac, as, az, wc, wsc, wsum, M, N, K, &e, ws.gemm_ws, ws.gemm_ws_bytes, stream);
+  };
+  auto aacc_tap = [&](const uint8_t* ac, const float* as, const float* az, const uint8_t* wc, const float* wsc,
+                      int64_t N, int64_t K, int32_t* out, const int8_t* w8) -> q4_status {
+    if (!out) return Q4_OK;
+    q4_epilogue e;
+    memset(&e, 0, sizeof e);
+    e.kind = Q4_EPI_I32;
+    e.out_i32 = out;
+    e.w_i8 = w8;
+    return q4_w4a4_asym_linear(ac, as, az, wc, wsc, nullptr, M, N, K, &e, nullptr, 0, stream);
+  };
   auto lin = [&](const uint8_t* ac, const float* as, const uint8_t* wc, const float* wsc, int64_t N, int64_t K,
                  q4_epilogue e) -> q4_status {
     if (i8) {
@@ -579,22 +666,31 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
   // QKV projection: dequant + bias -> fp16
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_F16; e.bias = w->bqkv; e.out_f16 = qkv; e.w_i8 = w->wqkv8;
-  if (fp & 1) {
+  if (asym) {
+    if ((st = alin(hq_in, hs_in, hz_in, w->wqkv, w->sqkv, w->cqkv, 3 * h, h, e))) return st;
+    if ((st = aacc_tap(hq_in, hs_in, hz_in, w->wqkv, w->sqkv, 3 * h, h, tp.acc_qkv, w->wqkv8))) return st;
+  } else if (fp & 1) {
     if ((st = f16lin(h_in, w->fqkv, 3 * h, h, e))) return st;
   } else {
     if ((st = lin(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, e))) return st;
     if ((st = acc_tap(hq_in, hs_in, w->wqkv, w->sqkv, 3 * h, h, tp.acc_qkv, w->wqkv8, false))) return st;
   }
   // FP16 attention + fused per-token ctx quantize
-  if ((st = i8 ? q4_attention_f16_q8(qkv, B, S, cfg->heads, cfg->head_dim, ctx_f16,
-                                     reinterpret_cast<int8_t*>(ctx_codes), ctx_scales, stream)
-              : q4_attention_f16_q4(qkv, B, S, cfg->heads, cfg->head_dim, ctx_f16, ctx_codes, ctx_scales, stream)))
+  if ((st = i8     ? q4_attention_f16_q8(qkv, B, S, cfg->heads, cfg->head_dim, ctx_f16,
+                                         reinterpret_cast<int8_t*>(ctx_codes), ctx_scales, stream)
+            : asym ? q4_attention_f16_q4_asym(qkv, B, S, cfg->heads, cfg->head_dim, ctx_f16, ctx_codes, ctx_scales,
+                                              ctx_zeros, stream)
+                   : q4_attention_f16_q4(qkv, B, S, cfg->heads, cfg->head_dim, ctx_f16, ctx_codes, ctx_scales, stream)))
     return st;
   // attention output: dequant + bias + residual(h_in) + LN1 + requant
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_RESLN_Q4; e.bias = w->bo; e.residual = h_in; e.gamma = w->ln1_g; e.beta = w->ln1_b;
   e.ln_eps = cfg->ln_eps; e.out_f16 = h1; e.out_codes = h1_codes; e.out_scales = h1_scales; e.w_i8 = w->wo8;
-  if (fp & 2) {
+  if (asym) {
+    e.out_zeros = h1_zeros;
+    if ((st = alin(ctx_codes, ctx_scales, ctx_zeros, w->wo, w->so, w->co, h, h, e))) return st;
+    if ((st = aacc_tap(ctx_codes, ctx_scales, ctx_zeros, w->wo, w->so, h, h, tp.acc_o, w->wo8))) return st;
+  } else if (fp & 2) {
     if ((st = f16lin(ctx_f16, w->fo, h, h, e))) return st;
   } else {
     if ((st = lin(ctx_codes, ctx_scales, w->wo, w->so, h, h, e))) return st;
@@ -604,7 +700,11 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_GELU_Q4; e.bias = w->b1; e.out_f16 = ffn1; e.out_codes = f_codes; e.out_scales = f_scales;
   e.w_i8 = w->w18;
-  if (fp & 4) {
+  if (asym) {
+    e.out_zeros = f_zeros;
+    if ((st = alin(h1_codes, h1_scales, h1_zeros, w->w1, w->s1, w->c1, f, h, e))) return st;
+    if ((st = aacc_tap(h1_codes, h1_scales, h1_zeros, w->w1, w->s1, f, h, tp.acc_1, w->w18))) return st;
+  } else if (fp & 4) {
     if ((st = f16lin(h1, w->f1, f, h, e))) return st;
   } else {
     if ((st = lin(h1_codes, h1_scales, w->w1, w->s1, f, h, e))) return st;
@@ -614,7 +714,11 @@ q4_status encoder_layer_impl(const q4_layer_cfg* cfg, const q4_layer_weights* w,
   memset(&e, 0, sizeof e);
   e.kind = Q4_EPI_RESLN_Q4; e.bias = w->b2; e.residual = h1; e.gamma = w->ln2_g; e.beta = w->ln2_b;
   e.ln_eps = cfg->ln_eps; e.out_f16 = h_out; e.out_codes = hq_out; e.out_scales = hs_out; e.w_i8 = w->w28;
-  if (fp & 8) {
+  if (asym) {
+    e.out_zeros = hz_out;
+    if ((st = alin(f_codes, f_scales, f_zeros, w->w2, w->s2, w->c2, h, f, e))) return st;
+    if ((st = aacc_tap(f_codes, f_scales, f_zeros, w->w2, w->s2, h, f, tp.acc_2, w->w28))) return st;
+  } else if (fp & 8) {
     if ((st = f16lin(ffn1, w->f2, h, f, e))) return st;
   } else {
     if ((st = lin(f_codes, f_scales, w->w2, w->s2, h, f, e))) return st;
@@ -631,8 +735,19 @@ q4_status q4_encoder_layer(const q4_layer_cfg* cfg, const q4_layer_weights* w, i
                            uint8_t* hq_out, float* hs_out, void* workspace, size_t ws_bytes, const q4_taps* taps,
                            void* stream) {
   g_err[0] = 0;
+  if (cfg && cfg->asym_acts) return fail(Q4_EINVAL, "q4_encoder_layer: asym_acts set (use q4_encoder_layer_asym)");
   return encoder_layer_impl(cfg, w, B, S, h_in, hq_in, hs_in, h_out, hq_out, hs_out, workspace, ws_bytes, taps,
                             stream, false);
+}
+
+q4_status q4_encoder_layer_asym(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B, int64_t S,
+                                const uint16_t* h_in, const uint8_t* hq_in, const float* hs_in, const float* hz_in,
+                                uint16_t* h_out, uint8_t* hq_out, float* hs_out, float* hz_out, void* workspace,
+                                size_t ws_bytes, const q4_taps* taps, void* stream) {
+  g_err[0] = 0;
+  if (!cfg || !cfg->asym_acts) return fail(Q4_EINVAL, "q4_encoder_layer_asym: cfg->asym_acts must be 1");
+  return encoder_layer_impl(cfg, w, B, S, h_in, hq_in, hs_in, h_out, hq_out, hs_out, workspace, ws_bytes, taps, stream,
+                            false, hz_in, hz_out);
 }
 
 q4_status q4_encoder_layer_w8a8(const q4_layer_cfg* cfg, const q4_layer_weights* w, int64_t B, int64_t S,
@@ -651,6 +766,7 @@ struct StackWs {
   uint16_t* hid[2];
   uint8_t* hq[2];
   float* hs[2];
+  float* hz[2];  // asymmetric activations: zero points
   uint8_t* layer;
   size_t layer_bytes, bytes;
 };
@@ -662,6 +778,7 @@ StackWs stack_ws(const q4_layer_cfg* c, int64_t M, uint8_t* base, bool i8 = fals
     w.hid[i] = (uint16_t*)take((size_t)M * c->hidden * 2);
     w.hq[i] = take((size_t)M * c->hidden / (i8 ? 1 : 2));
     w.hs[i] = (float*)take((size_t)M * 4);
+    w.hz[i] = (!i8 && c->asym_acts) ? (float*)take((size_t)M * 4) : nullptr;
   }
   w.layer_bytes = layer_ws(c, M, nullptr, i8).bytes;
   w.layer = take(w.layer_bytes);
@@ -702,8 +819,10 @@ q4_status encoder_stack_impl(const q4_layer_cfg* cfg, const q4_layer_weights* la
     return fail(Q4_EALIGN, "q4_encoder_stack: h_in must be 16-byte aligned");
   }
   // layer-0 activation quantize (the only standalone quantize in the forward)
-  if ((st = i8 ? q4_quantize_rows_i8(x, M, h, h, 0.f, reinterpret_cast<int8_t*>(ws.hq[1]), ws.hs[1], stream)
-               : q4_quantize_rows(x, M, h, h, 0.f, ws.hq[1], ws.hs[1], stream)))
+  if (i8 && cfg->asym_acts) return fail(Q4_EUNSUPPORTED, "%s: asym_acts on the W8A8 baseline", who);
+  if ((st = i8               ? q4_quantize_rows_i8(x, M, h, h, 0.f, reinterpret_cast<int8_t*>(ws.hq[1]), ws.hs[1], stream)
+            : cfg->asym_acts ? q4_quantize_rows_asym(x, M, h, h, ws.hq[1], ws.hs[1], ws.hz[1], stream)
+                             : q4_quantize_rows(x, M, h, h, 0.f, ws.hq[1], ws.hs[1], stream)))
     return st;
   const bool out_dev = is_device_ptr(h_out);
   for (int l = 0; l < L; ++l) {
@@ -711,7 +830,7 @@ q4_status encoder_stack_impl(const q4_layer_cfg* cfg, const q4_layer_weights* la
     const uint16_t* hin = (l == 0) ? x : ws.hid[1 - o];
     uint16_t* hout = (l == L - 1 && out_dev) ? h_out : ws.hid[o];
     if ((st = encoder_layer_impl(cfg, &layers[l], B, S, hin, ws.hq[1 - o], ws.hs[1 - o], hout, ws.hq[o], ws.hs[o],
-                                 ws.layer, ws.layer_bytes, nullptr, stream, i8)))
+                                 ws.layer, ws.layer_bytes, nullptr, stream, i8, ws.hz[1 - o], ws.hz[o])))
       return st;
   }
   if (!out_dev) {

@@ -126,18 +126,6 @@ cudaError_t launch_prepack_weights(const uint8_t* w_codes, int64_t N, int64_t K,
 // x - min and max - min of two fp16 values are exact in fp64 (<= 41 significant bits), so
 // p = d * (15/D) in fp64 is within 1e-14 of the rational; near a half-integer the exact
 // fp64 residual 15 d - D h (both products exact) decides.  Warp per row, one HBM read.
-__device__ __forceinline__ uint32_t asym_code(float x, double mn, double D, double r15) {
-  const double d = (double)x - mn;
-  const double p = d * r15;
-  double n = rint(p);
-  if (fabs(p - n) > 0.4999999) {
-    const double h = floor(p) + 0.5;
-    const double e = fma(-D, h, 15.0 * d);
-    n = e > 0.0 ? h + 0.5 : (e < 0.0 ? h - 0.5 : (fmod(h - 0.5, 2.0) == 0.0 ? h - 0.5 : h + 0.5));
-  }
-  return (uint32_t)(int)fmin(n, 15.0);
-}
-
 template <int MAXV>
 __global__ void __launch_bounds__(256) quantize_rows_asym_kernel(const __half* __restrict__ x, int64_t rows, int cols,
                                                                  int64_t ld_x, uint8_t* __restrict__ codes,

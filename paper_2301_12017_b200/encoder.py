@@ -15,14 +15,17 @@ from ._lib import LayerWeights, check, lib
 class W4A4Encoder:
     bits = 4
 
-    def __init__(self, cfg: dict, layers: list, device="cuda", fp16_parts: int = 0):
+    def __init__(self, cfg: dict, layers: list, device="cuda", fp16_parts: int = 0, asym: bool = False):
         """cfg: BERT dims (hidden, heads, head_dim, ffn, ln_eps); layers: per-layer fp16
         parameter dicts (synth.layer_params) -- quantized on the device here (offline).
-        fp16_parts: the per-part quantization strategy (q4_layer_cfg; 0 = qall)."""
+        fp16_parts: the per-part quantization strategy (q4_layer_cfg; 0 = qall).
+        asym: asymmetric activation quantization throughout (NEXT-3, q4_layer_cfg.asym_acts)."""
         self.cfg = dict(cfg)
         self.cfg["fp16_parts"] = fp16_parts
+        self.cfg["asym_acts"] = int(asym)
         self.device = torch.device(device)
-        self.weights = [ops.quantize_layer(p, self.device, bits=self.bits, fp16_parts=fp16_parts) for p in layers]
+        self.weights = [ops.quantize_layer(p, self.device, bits=self.bits, fp16_parts=fp16_parts, asym=asym)
+                        for p in layers]
         i8 = self.bits == 8
         self._ws_fn = lib().q4_encoder_stack_w8a8_workspace if i8 else lib().q4_encoder_stack_workspace
         self._stack_fn = lib().q4_encoder_stack_w8a8 if i8 else lib().q4_encoder_stack

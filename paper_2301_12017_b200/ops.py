@@ -48,9 +48,10 @@ def quantize_rows(x: torch.Tensor, clip: float = 0.0, codes=None, scales=None):
 
 def w4a4_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None, residual=None,
                 gamma=None, beta=None, ln_eps=1e-12, clip=0.0, mainloop=0, f16_tap=False,
-                out=None, workspace=None, w_i8=None):
+                out=None, workspace=None, w_i8=None, asym_out=False):
     """a3-a6: INT4 x INT4 -> exact INT32 -> fused epilogue.  Returns a dict with the
-    outputs of the epilogue kind: i32 | f16 | (codes, scales[, f16])."""
+    outputs of the epilogue kind: i32 | f16 | (codes, scales[, zeros][, f16]).
+    asym_out: the requantizing kinds write asymmetric codes + zeros (NEXT-3)."""
     _need(a_codes, torch.uint8, "a_codes", 2)
     _need(w_codes, torch.uint8, "w_codes", 2)
     _need(a_scales, torch.float32, "a_scales", 1)
@@ -70,10 +71,13 @@ def w4a4_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None
     if kind in (EPI_GELU_Q4, EPI_RESLN_Q4):
         o.setdefault("codes", torch.empty(M, N // 2, dtype=torch.uint8, device=dev))
         o.setdefault("scales", torch.empty(M, dtype=torch.float32, device=dev))
+        if asym_out:
+            o.setdefault("zeros", torch.empty(M, dtype=torch.float32, device=dev))
     e = Epilogue(kind=kind, mainloop=mainloop, bias=_ptr(bias), residual=_ptr(residual),
                  gamma=_ptr(gamma), beta=_ptr(beta), ln_eps=ln_eps, requant_clip=clip,
                  out_i32=_ptr(o.get("i32")), out_f16=_ptr(o.get("f16")),
-                 out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")), w_i8=_ptr(w_i8))
+                 out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")), w_i8=_ptr(w_i8),
+                 out_zeros=_ptr(o.get("zeros")))
     ws_bytes = lib().q4_w4a4_linear_workspace(M, N, K, kind)
     if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
         workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
@@ -182,8 +186,10 @@ def weight_code_sums(w_codes: torch.Tensor) -> torch.Tensor:
 
 
 def w4a4_asym_linear(a_codes, a_scales, a_zeros, w_codes, w_scales, w_sums, kind=EPI_F16, *, bias=None,
-                     mainloop=0, w_i8=None, out=None):
-    """NEXT-3: asymmetric activations x symmetric INT4 weights, F16 or I32 epilogue."""
+                     residual=None, gamma=None, beta=None, ln_eps=1e-12, mainloop=0, w_i8=None, out=None,
+                     f16_tap=False, asym_out=True, workspace=None):
+    """NEXT-3: asymmetric activations x symmetric INT4 weights with the four epilogues; the
+    requantizing kinds write asymmetric codes + zeros (asym_out) or symmetric codes."""
     _need(a_codes, torch.uint8, "a_codes", 2)
     _need(w_codes, torch.uint8, "w_codes", 2)
     M, K = a_codes.shape[0], a_codes.shape[1] * 2
@@ -192,14 +198,38 @@ def w4a4_asym_linear(a_codes, a_scales, a_zeros, w_codes, w_scales, w_sums, kind
     o = dict(out or {})
     if kind == EPI_I32:
         o.setdefault("i32", torch.empty(M, N, dtype=torch.int32, device=dev))
-    else:
+    if kind in (EPI_F16, EPI_RESLN_Q4) or (kind == EPI_GELU_Q4 and f16_tap):
         o.setdefault("f16", torch.empty(M, N, dtype=torch.float16, device=dev))
-    e = Epilogue(kind=kind, mainloop=mainloop, bias=_ptr(bias), residual=None, gamma=None, beta=None, ln_eps=0.0,
-                 requant_clip=0.0, out_i32=_ptr(o.get("i32")), out_f16=_ptr(o.get("f16")), out_codes=None,
-                 out_scales=None, w_i8=_ptr(w_i8))
+    if kind in (EPI_GELU_Q4, EPI_RESLN_Q4):
+        o.setdefault("codes", torch.empty(M, N // 2, dtype=torch.uint8, device=dev))
+        o.setdefault("scales", torch.empty(M, dtype=torch.float32, device=dev))
+        if asym_out:
+            o.setdefault("zeros", torch.empty(M, dtype=torch.float32, device=dev))
+    e = Epilogue(kind=kind, mainloop=mainloop, bias=_ptr(bias), residual=_ptr(residual), gamma=_ptr(gamma),
+                 beta=_ptr(beta), ln_eps=ln_eps, requant_clip=0.0, out_i32=_ptr(o.get("i32")),
+                 out_f16=_ptr(o.get("f16")), out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")),
+                 w_i8=_ptr(w_i8), out_zeros=_ptr(o.get("zeros")))
+    ws_bytes = lib().q4_w4a4_linear_workspace(M, N, K, kind)
+    if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
+        workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
     check(lib().q4_w4a4_asym_linear(_ptr(a_codes), _ptr(a_scales), _ptr(a_zeros), _ptr(w_codes), _ptr(w_scales),
-                                    _ptr(w_sums), M, N, K, C.byref(e), _stream()))
+                                    _ptr(w_sums), M, N, K, C.byref(e), _ptr(workspace),
+                                    0 if workspace is None else workspace.numel(), _stream()))
     return o
+
+
+def attention_f16_q4_asym(qkv, B, S, heads, head_dim=64):
+    """NEXT-3 a7: fp16 QKV -> (ctx codes, scales, zeros, ctx fp16) with asymmetric ctx codes."""
+    _need(qkv, torch.float16, "qkv", 2)
+    h = heads * head_dim
+    dev = qkv.device
+    codes = torch.empty(B * S, h // 2, dtype=torch.uint8, device=dev)
+    scales = torch.empty(B * S, dtype=torch.float32, device=dev)
+    zeros = torch.empty(B * S, dtype=torch.float32, device=dev)
+    ctx = torch.empty(B * S, h, dtype=torch.float16, device=dev)
+    check(lib().q4_attention_f16_q4_asym(_ptr(qkv), B, S, heads, head_dim, _ptr(ctx), _ptr(codes), _ptr(scales),
+                                         _ptr(zeros), _stream()))
+    return codes, scales, zeros, ctx
 
 
 def attention_f16_q4(qkv, B, S, heads, head_dim=64, f16_tap=False):
@@ -230,7 +260,7 @@ def attention_f16_q8(qkv, B, S, heads, head_dim=64, f16_tap=False):
 
 def layer_cfg(cfg: dict) -> LayerCfg:
     return LayerCfg(cfg["hidden"], cfg["heads"], cfg["head_dim"], cfg["ffn"], cfg.get("ln_eps", 1e-12),
-                    int(cfg.get("fp16_parts", 0)))
+                    int(cfg.get("fp16_parts", 0)), int(cfg.get("asym_acts", 0)))
 
 
 def launch_floor(n: int, ctas: int = 32):
@@ -255,7 +285,7 @@ def layer_weights(w: dict) -> LayerWeights:
 
 
 def quantize_layer(params: dict, device="cuda", prepack: bool = True, bits: int = 4,
-                   fp16_parts: int = 0) -> dict:
+                   fp16_parts: int = 0, asym: bool = False) -> dict:
     """Offline weight prep (a2, not timed): fp16 [out, in] weights -> per-output-channel
     INT4 codes + scales on the device (and, with prepack, the MMA-ready int8 copy);
     biases and LN parameters copied as fp16.  bits=8: the W8A8 baseline's int8 codes.
@@ -274,6 +304,8 @@ def quantize_layer(params: dict, device="cuda", prepack: bool = True, bits: int 
         w[k], w["s" + k[1:]] = quantize_rows(t)
         if prepack:
             w[k + "8"] = prepack_weights(w[k])
+        if asym:  # asymmetric activations: the zero-point term's weight code sums (NEXT-3)
+            w["c" + k[1:]] = weight_code_sums(w[k])
     for k in ("bqkv", "bo", "b1", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b"):
         w[k] = torch.as_tensor(params[k]).to(device=device, dtype=torch.float16).contiguous()
     return w
@@ -287,7 +319,7 @@ def encoder_layer_workspace_bytes(cfg: dict, B: int, S: int, bits: int = 4) -> i
 
 
 def encoder_layer(cfg: dict, w: dict, B: int, S: int, h_in, hq_in, hs_in, taps: bool = False,
-                  workspace=None, bits: int = 4):
+                  workspace=None, bits: int = 4, hz_in=None):
     """a8: one post-LN BERT layer (qall).  Returns dict(h_out, hq_out, hs_out[, taps...]).
     bits=8: the W8A8 baseline (q4_encoder_layer_w8a8; int8 codes, weights from
     quantize_layer(bits=8))."""
@@ -299,9 +331,12 @@ def encoder_layer(cfg: dict, w: dict, B: int, S: int, h_in, hq_in, hs_in, taps: 
     if workspace is None:
         workspace = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     cdt, cdiv = (torch.int8, 1) if i8 else (torch.uint8, 2)
+    asym = bool(cfg.get("asym_acts", 0))
     out = {"h_out": torch.empty(M, h, dtype=torch.float16, device=dev),
            "hq_out": torch.empty(M, h // cdiv, dtype=cdt, device=dev),
            "hs_out": torch.empty(M, dtype=torch.float32, device=dev)}
+    if asym:
+        out["hz_out"] = torch.empty(M, dtype=torch.float32, device=dev)
     tp = None
     if taps:
         shapes = {"qkv": ((M, 3 * h), torch.float16), "ctx": ((M, h), torch.float16),
@@ -311,13 +346,21 @@ def encoder_layer(cfg: dict, w: dict, B: int, S: int, h_in, hq_in, hs_in, taps: 
                   "ctx_codes": ((M, h // cdiv), cdt), "h1_codes": ((M, h // cdiv), cdt),
                   "f_codes": ((M, f // cdiv), cdt), "ctx_scales": ((M,), torch.float32),
                   "h1_scales": ((M,), torch.float32), "f_scales": ((M,), torch.float32)}
+        if asym:
+            shapes.update({k: ((M,), torch.float32) for k in ("ctx_zeros", "h1_zeros", "f_zeros")})
         for k, (shp, dt) in shapes.items():
             out[k] = torch.empty(shp, dtype=dt, device=dev)
-        tp = Taps(**{k: out[k].data_ptr() for k in _lib.TAP_FIELDS})
+        tp = Taps(**{k: (out[k].data_ptr() if k in out else None) for k in _lib.TAP_FIELDS})
     lw = layer_weights(w)
+    tpp = C.byref(tp) if tp is not None else None
+    if asym:
+        check(lib().q4_encoder_layer_asym(C.byref(lc), C.byref(lw), B, S, _ptr(h_in), _ptr(hq_in), _ptr(hs_in),
+                                          _ptr(hz_in), _ptr(out["h_out"]), _ptr(out["hq_out"]), _ptr(out["hs_out"]),
+                                          _ptr(out["hz_out"]), _ptr(workspace), workspace.numel(), tpp, _stream()))
+        return out
     fn = lib().q4_encoder_layer_w8a8 if i8 else lib().q4_encoder_layer
     check(fn(C.byref(lc), C.byref(lw), B, S, _ptr(h_in), _ptr(hq_in),
                                  _ptr(hs_in), _ptr(out["h_out"]), _ptr(out["hq_out"]),
                                  _ptr(out["hs_out"]), _ptr(workspace), workspace.numel(),
-                                 C.byref(tp) if tp is not None else None, _stream()))
+                                 tpp, _stream()))
     return out

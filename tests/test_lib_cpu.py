@@ -102,11 +102,24 @@ def test_layer_structs_match_the_header():
     import re
     from paper_2301_12017_b200 import _lib
     src = open(os.path.join(ROOT, "include", "q4.h")).read()
-    body = re.search(r"typedef struct \{(.*?)\} q4_layer_weights;", src, re.S).group(1)
+    body = re.search(r"typedef struct \{([^{}]*?)\} q4_layer_weights;", src, re.S).group(1)
     names = re.findall(r"\*(\w+)", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
     assert tuple(names) == _lib.WEIGHT_FIELDS
-    cfg = re.search(r"typedef struct \{(.*?)\} q4_layer_cfg;", src, re.S).group(1)
-    assert "fp16_parts" in cfg and [n for n, _ in _lib.LayerCfg._fields_][-1] == "fp16_parts"
+    body = re.search(r"typedef struct \{([^{}]*?)\} q4_taps;", src, re.S).group(1)
+    assert tuple(re.findall(r"\*(\w+)", re.sub(r"/\*.*?\*/", "", body, flags=re.S))) == _lib.TAP_FIELDS
+
+    def scalar_fields(struct):  # "type a, b;" / "type* a;" declarations, comments removed, in order
+        body = re.search(r"typedef struct \{([^{}]*?)\} " + struct + ";", src, re.S).group(1)
+        body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+        names = []
+        for decl in body.split(";"):
+            decl = decl.strip()
+            if decl:
+                names += [re.sub(r"[*\s]", "", v).split()[-1] if " " in v.strip() else re.sub(r"[*]", "", v).strip()
+                          for v in re.sub(r"^(const\s+)?\w+\s*\**", "", decl, count=1).split(",")]
+        return [n.strip("* ") for n in names]
+    assert scalar_fields("q4_layer_cfg") == [n for n, _ in _lib.LayerCfg._fields_]
+    assert scalar_fields("q4_epilogue") == [n for n, _ in _lib.Epilogue._fields_]
 
 
 def test_workspace_sizes(L):
@@ -117,10 +130,11 @@ def test_workspace_sizes(L):
     assert ws(32768, 3072, 1024, _lib.EPI_F16) == 0 and ws(32768, 3072, 1024, _lib.EPI_I32) == 0
     g = ws(32768, 4096, 1024, _lib.EPI_GELU_Q4)
     r = ws(32768, 1024, 4096, _lib.EPI_RESLN_Q4)
-    # [mblocks][ntn][128] x (8 B stats + 4 B max) + counters: 256 m-blocks, 16 resp. 4 n-blocks
-    assert g >= 256 * 16 * 128 * 12 and r >= 256 * 4 * 128 * 12
+    # [mblocks][ntn][128] x (8 B stats + 4 B max + 8 B asym min/max) + counters: 256 m-blocks,
+    # 16 resp. 4 n-blocks
+    assert g >= 256 * 16 * 128 * 20 and r >= 256 * 4 * 128 * 20
     assert ws(1024, 4096, 1024, _lib.EPI_GELU_Q4) < g
-    cfg = _lib.LayerCfg(1024, 16, 64, 4096, 1e-12, 0)
+    cfg = _lib.LayerCfg(1024, 16, 64, 4096, 1e-12, 0, 0)
     lw = L.q4_encoder_layer_workspace(C.byref(cfg), 256, 128)
     sw = L.q4_encoder_stack_workspace(C.byref(cfg), 256, 128)
     assert lw > g and sw > lw
