@@ -647,6 +647,28 @@ def side_measurements(q4, synth, torch, np, dev, args):
         out[name + "_p50_ms"] = t[n // 2]
         out[name + "_seq_per_s"] = B / (t[n // 2] * 1e-3)
         del enc
+    # Asymmetric activations (NEXT-3; the paper finds asym slower "because of less required
+    # computation for bias term"): the same encoder with asym_acts = 1
+    for size, L, B, name in (("large", 24, 256, "asym_bert_large_24l_bs256"), ("base", 12, 1, "asym_bert_base_12l_bs1")):
+        c = dict(synth.BERT[size])
+        enc = q4.W4A4Encoder(c, [synth.layer_params(c, l, "bert") for l in range(L)], device=dev, asym=True)
+        x = torch.from_numpy(np.concatenate([synth.hidden(128, c["hidden"], "input", b) for b in range(B)])).to(dev)
+        o = torch.empty_like(x)
+        enc.capture(x, o, B, 128)
+        for _ in range(5):
+            enc.replay()
+        n = 20 if B > 1 else 200
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
+        torch.cuda.synchronize()
+        evs[0].record(stream)
+        for i in range(n):
+            enc.replay()
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        t = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(n))
+        out[name + "_p50_ms"] = t[n // 2]
+        out[name + "_seq_per_s"] = B / (t[n // 2] * 1e-3)
+        del enc
     # Per-part quantization strategy tuner (Fig. e2e_i4_fti8 annotations):
     # all 16 strategies of BERT-base 12 L at the paper's small (bs-seq) points and the
     # latency config; argmin reported with the qall and all-FP16 times

@@ -228,6 +228,32 @@ Q4_API q4_status q4_attention_f16_q4_asym(const uint16_t* qkv, int64_t B, int64_
                                           float* ctx_scales, float* ctx_zeros, void* stream);
 
 /* ---------------------------------------------------------------------------------
+ * NEXT-4: W4A4 with 2:4-sparse weights -- the paper's "Pair-(2:4)" (50%)
+ * semi-structured sparsity composed with INT4, pruning before quantization (P => Q) with the
+ * l1 criterion.  Offline: q4_prune_24 -> q4_quantize_rows (a2) ->
+ * q4_sparse24_compress; forward: q4_w4a4_sparse24_linear on the sparse tensor cores
+ * (tcgen05.mma.sp kind::i8, half the weight MMA operand bytes).
+ * q4_prune_24: w [N, K] fp16 rows; in every group of four consecutive k the two largest |w|
+ *   are kept (ties: the lower index) and the other two set to +0.  K % 4 == 0, 8-byte aligned.
+ * q4_sparse24_compress: packed INT4 codes [N, K/2] with at most two nonzero codes per group of
+ *   four -> w_vals [N, K/2] int8 (16*q of the two kept codes per group, in k order; a group
+ *   with fewer nonzeros keeps zero codes at its lowest free positions) + w_meta [N, K/32]
+ *   uint32 (per group the nibble i0 | i1 << 2 of the kept positions, i0 < i1, eight groups per
+ *   word in k order -- the tcgen05.mma.sp metadata layout).  `violations` (nullable, device
+ *   int, accumulated) counts groups with more than two nonzero codes: their extra codes are
+ *   dropped.  K % 256 == 0, pointers 16-byte aligned.
+ * q4_w4a4_sparse24_linear: as q4_w4a4_linear (a3/a4: exact INT32 sum, then
+ *   t = acc * a_scales[m] * w_scales[n] + bias[n]) with the compressed weights; epilogues F16 and
+ *   I32 only.  N % 128 == 0, K % 256 == 0, K <= 8192, N / 128 <= #SMs; no workspace. */
+Q4_API q4_status q4_prune_24(const uint16_t* w, int64_t N, int64_t K, uint16_t* out, void* stream);
+Q4_API q4_status q4_sparse24_compress(const uint8_t* w_codes, int64_t N, int64_t K, int8_t* w_vals,
+                                      uint32_t* w_meta, int32_t* violations, void* stream);
+Q4_API q4_status q4_w4a4_sparse24_linear(const uint8_t* a_codes, const float* a_scales,
+                                         const int8_t* w_vals, const uint32_t* w_meta,
+                                         const float* w_scales, int64_t M, int64_t N, int64_t K,
+                                         const q4_epilogue* epi, void* stream);
+
+/* ---------------------------------------------------------------------------------
  * a2' Offline weight prepack (once per weight, not on the forward path): packed INT4 codes
  * w_codes [N, K/2] -> w_i8 [N, K] int8 holding 16*q in the K order of the on-chip
  * activation unpack (per 32-element group: the 16 even-k values, then the 16 odd-k).

@@ -67,6 +67,7 @@ def lib():
                                          P, P, P, P, I]
         L.oracle_f16_linear.argtypes = [P, P, I64, I64, I64, I, P, P, P, P, D, F, P, P, P, I]
         L.oracle_quantize_rows_asym.argtypes = [P, I64, I64, I64, P, P, P, I]
+        L.oracle_prune_24.argtypes = [P, I64, I64, P]
         L.oracle_w4a4_asym_linear.argtypes = [P, P, P, P, P, I64, I64, I64, I, P, P, P, P, D, P, P, P, P, P, I]
         _lib = L
     return _lib
@@ -268,6 +269,16 @@ def w4a4_asym_linear(a_codes, a_scales, a_zeros, w_codes, w_scales, M, N, K, epi
                                        epi, _p(bias), _p(residual), _p(gamma), _p(beta), float(ln_eps), _p(i32),
                                        _p(f16), _p(codes), _p(scales), _p(zeros), threads)
     _check(rc, "w4a4_asym_linear")
+    return out
+
+
+# ---------------------------------------------------------------- O-17 (2:4 pruning)
+def prune_24(w: np.ndarray) -> np.ndarray:
+    """O-17: l1 Pair-(2:4) pruning of fp16 rows along K."""
+    w = _c(w, np.float16)
+    N, K = w.shape
+    out = np.zeros_like(w)
+    _check(lib().oracle_prune_24(_p(w.view(np.uint16)), N, K, _p(out.view(np.uint16))), "prune_24")
     return out
 
 

@@ -427,6 +427,28 @@ int oracle_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales, const
   return rc;
 }
 
+/* O-17: l1 Pair-(2:4) pruning ("N zero-entries for every M elements",
+ * 268-270: "prunes those small absolute value to be zero while keeping those large weight
+ * value untouched"), applied before quantization (P => Q): in every group of
+ * four consecutive elements of a row the two largest |w| are kept (ties: the lower index) and
+ * the other two set to +0.  The sparse linear is then O-4/O-5 on the pruned, quantized
+ * weights (zeros included) -- no new arithmetic. */
+int oracle_prune_24(const uint16_t* w, int64_t N, int64_t K, uint16_t* out) {
+  if (N < 0 || K <= 0 || K % 4) return -1;
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t g = 0; g < K / 4; ++g) {
+      const uint16_t* v = w + n * K + 4 * g;
+      double a[4];
+      for (int j = 0; j < 4; ++j) a[j] = fabs(oracle_f16_to_f64(v[j]));
+      for (int j = 0; j < 4; ++j) {
+        int beaten = 0; /* elements ranked above j: larger |w|, or equal with a lower index */
+        for (int k = 0; k < 4; ++k) beaten += (a[k] > a[j]) || (a[k] == a[j] && k < j);
+        out[n * K + 4 * g + j] = beaten >= 2 ? (uint16_t)0 : v[j];
+      }
+    }
+  return 0;
+}
+
 /* ------------------------------------------------------------------ O-8 attention */
 
 int oracle_attention(const uint16_t* qkv, int64_t B, int64_t S, int heads, int head_dim,

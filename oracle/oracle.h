@@ -156,6 +156,8 @@ int oracle_w4a4_asym_linear(const uint8_t* a_codes, const float* a_scales, const
                             int epi_kind, const uint16_t* bias, const uint16_t* residual, const uint16_t* gamma,
                             const uint16_t* beta, double ln_eps, int32_t* out_i32, uint16_t* out_f16,
                             uint8_t* out_codes, float* out_scales, float* out_zeros, int threads);
+/* O-17: l1 Pair-(2:4) pruning of fp16 rows along K (two largest |w| of every four kept). */
+int oracle_prune_24(const uint16_t* w, int64_t N, int64_t K, uint16_t* out);
 
 #ifdef __cplusplus
 }

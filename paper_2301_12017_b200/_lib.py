@@ -26,7 +26,7 @@ EXPORTS = (
     "q4_encoder_stack_w8a8_workspace", "q4_encoder_stack_w8a8", "q4_f16_linear_workspace", "q4_f16_linear",
     "q4_quantize_rows_asym", "q4_weight_code_sums", "q4_w4a4_asym_linear",
     "q4_encoder_pipeline_workspace", "q4_encoder_pipeline", "q4_launch_floor", "q4_attention_f16_q4_asym",
-    "q4_encoder_layer_asym",
+    "q4_encoder_layer_asym", "q4_prune_24", "q4_sparse24_compress", "q4_w4a4_sparse24_linear",
 )
 
 
@@ -110,6 +110,9 @@ def lib():
                                           P, SZ, P]
         L.q4_weight_code_sums.argtypes = [P, I64, I64, P, P]
         L.q4_w4a4_asym_linear.argtypes = [P, P, P, P, P, P, I64, I64, I64, C.POINTER(Epilogue), P, SZ, P]
+        L.q4_prune_24.argtypes = [P, I64, I64, P, P]
+        L.q4_sparse24_compress.argtypes = [P, I64, I64, P, P, P, P]
+        L.q4_w4a4_sparse24_linear.argtypes = [P, P, P, P, P, I64, I64, I64, C.POINTER(Epilogue), P]
         L.q4_attention_f16_q4_asym.argtypes = [P, I64, I64, I32, I32, P, P, P, P, P]
         L.q4_encoder_layer_asym.argtypes = [C.POINTER(LayerCfg), C.POINTER(LayerWeights), I64, I64, P, P, P, P,
                                             P, P, P, P, P, SZ, C.POINTER(Taps), P]

@@ -87,7 +87,23 @@ int tc_tile_n(int M, int N, int kind);
 size_t tc_workspace_bytes(int M, int N, int TN, int kind);
 size_t tc_row_grid(int M, int N, int TN);  // CTAs of a 1-CTA row-epilogue launch
 size_t tc_counter_bytes(int M);  // the rendezvous counters at the start of a row-epilogue workspace
-cudaError_t launch_floor_kernel(int ctas, cudaStream_t s);  // empty PDL kernel (measurement only)
+cudaError_t launch_floor_kernel(int ctas, cudaStream_t s);  // (declared below the GEMM args too)
+// NEXT-4: 2:4-sparse W4A4 (gemm_sparse.cu)
+struct SparseArgs {
+  const uint8_t* a_codes;  // [M, K/2] packed INT4 activations
+  const float* a_scales;   // [M]
+  const int8_t* w_vals;    // [N, K/2] compressed 16*q weights (two kept values per group of four)
+  const uint32_t* w_meta;  // [N, K/32] 2:4 position nibbles
+  const float* w_scales;   // [N]
+  const __half* bias;      // [N] or nullptr
+  int M, N, K;
+  int32_t* out_i32;        // I32 epilogue (exclusive with out_f16)
+  __half* out_f16;         // F16 epilogue
+};
+cudaError_t launch_w4a4_sparse24(const SparseArgs& a, cudaStream_t s, const char** why);
+cudaError_t launch_prune24(const __half* w, int64_t N, int64_t K, __half* out, cudaStream_t s);
+cudaError_t launch_sparse24_compress(const uint8_t* codes, int64_t N, int64_t K, int8_t* vals, uint32_t* meta,
+                                     int* violations, cudaStream_t s);  // empty PDL kernel (measurement only)
 cudaError_t launch_w4a4_legacy(const GemmArgs& g, bool s4, cudaStream_t s, const char** why);
 // i8: W8A8 baseline -- int8 ctx codes [B*S, h] with scale amax/127 instead of packed INT4
 cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __half* ctx_f16,

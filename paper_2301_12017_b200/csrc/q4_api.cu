@@ -428,6 +428,63 @@ q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, const ui
   return Q4_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-4: 2:4-sparse weights
+
+q4_status q4_prune_24(const uint16_t* w, int64_t N, int64_t K, uint16_t* out, void* stream) {
+  g_err[0] = 0;
+  if (N < 0 || K <= 0 || K % 4) return fail(Q4_ESHAPE, "q4_prune_24: N=%lld K=%lld (K %% 4 == 0)", (long long)N, (long long)K);
+  if (N == 0) return Q4_OK;
+  if (!w || !out) return fail(Q4_EINVAL, "q4_prune_24: NULL w/out");
+  if (!al8(w) || !al8(out)) return fail(Q4_EALIGN, "q4_prune_24: w/out must be 8-byte aligned");
+  cudaError_t e = q4::launch_prune24(reinterpret_cast<const __half*>(w), N, K, reinterpret_cast<__half*>(out),
+                                     (cudaStream_t)stream);
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_prune_24");
+}
+
+q4_status q4_sparse24_compress(const uint8_t* w_codes, int64_t N, int64_t K, int8_t* w_vals, uint32_t* w_meta,
+                               int32_t* violations, void* stream) {
+  g_err[0] = 0;
+  if (N < 0 || K <= 0 || K % 256) return fail(Q4_ESHAPE, "q4_sparse24_compress: N=%lld K=%lld (K %% 256 == 0)", (long long)N, (long long)K);
+  if (N == 0) return Q4_OK;
+  if (!w_codes || !w_vals || !w_meta) return fail(Q4_EINVAL, "q4_sparse24_compress: NULL w_codes/w_vals/w_meta");
+  if (!al16(w_codes) || !al16(w_vals) || !al16(w_meta) || (violations && !al4(violations)))
+    return fail(Q4_EALIGN, "q4_sparse24_compress: pointers must be 16-byte aligned (violations 4)");
+  cudaError_t e = q4::launch_sparse24_compress(w_codes, N, K, w_vals, w_meta, violations, (cudaStream_t)stream);
+  return e == cudaSuccess ? Q4_OK : cuda_fail(e, "q4_sparse24_compress");
+}
+
+q4_status q4_w4a4_sparse24_linear(const uint8_t* a_codes, const float* a_scales, const int8_t* w_vals,
+                                  const uint32_t* w_meta, const float* w_scales, int64_t M, int64_t N, int64_t K,
+                                  const q4_epilogue* epi, void* stream) {
+  g_err[0] = 0;
+  if (!epi) return fail(Q4_EINVAL, "q4_w4a4_sparse24_linear: epi is NULL");
+  if (epi->kind != Q4_EPI_F16 && epi->kind != Q4_EPI_I32)
+    return fail(Q4_EUNSUPPORTED, "q4_w4a4_sparse24_linear: epilogue kind %d (F16 or I32)", epi->kind);
+  if (M < 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N % 128 || K % 256 || K > 8192)
+    return fail(Q4_ESHAPE, "q4_w4a4_sparse24_linear: M=%lld N=%lld K=%lld (N %% 128 == 0, K %% 256 == 0, K <= 8192)",
+                (long long)M, (long long)N, (long long)K);
+  if (M == 0) return Q4_OK;
+  if (!a_codes || !a_scales || !w_vals || !w_meta || !w_scales)
+    return fail(Q4_EINVAL, "q4_w4a4_sparse24_linear: NULL operand");
+  if (!al16(a_codes) || !al16(w_vals) || !al16(w_meta) || !al4(w_scales) || !al4(a_scales) ||
+      (epi->bias && !al4(epi->bias)))
+    return fail(Q4_EALIGN, "q4_w4a4_sparse24_linear: codes / values / metadata 16-byte aligned, scales / bias 4-byte");
+  if ((epi->kind == Q4_EPI_F16 && (!epi->out_f16 || !al16(epi->out_f16))) ||
+      (epi->kind == Q4_EPI_I32 && (!epi->out_i32 || !al16(epi->out_i32))))
+    return fail(Q4_EINVAL, "q4_w4a4_sparse24_linear: output NULL or not 16-byte aligned");
+  q4::SparseArgs g;
+  g.a_codes = a_codes; g.a_scales = a_scales; g.w_vals = w_vals; g.w_meta = w_meta; g.w_scales = w_scales;
+  g.bias = reinterpret_cast<const __half*>(epi->bias);
+  g.M = (int)M; g.N = (int)N; g.K = (int)K;
+  g.out_i32 = epi->kind == Q4_EPI_I32 ? epi->out_i32 : nullptr;
+  g.out_f16 = epi->kind == Q4_EPI_F16 ? reinterpret_cast<__half*>(epi->out_f16) : nullptr;
+  const char* why = "";
+  cudaError_t e = q4::launch_w4a4_sparse24(g, (cudaStream_t)stream, &why);
+  if (e == cudaErrorNotSupported) return fail(Q4_EUNSUPPORTED, "q4_w4a4_sparse24_linear: %s", why);
+  if (e != cudaSuccess) return fail(Q4_ECUDA, "q4_w4a4_sparse24_linear: %s %s", cudaGetErrorString(e), why);
+  return Q4_OK;
+}
+
 q4_status q4_prepack_weights(const uint8_t* w_codes, int64_t N, int64_t K, int8_t* w_i8, void* stream) {
   g_err[0] = 0;
   if (N < 0 || K <= 0 || K % 32) return fail(Q4_ESHAPE, "q4_prepack_weights: N=%lld K=%lld (need K %% 32 == 0)", (long long)N, (long long)K);

@@ -263,6 +263,40 @@ def layer_cfg(cfg: dict) -> LayerCfg:
                     int(cfg.get("fp16_parts", 0)), int(cfg.get("asym_acts", 0)))
 
 
+def prune_24(w: torch.Tensor) -> torch.Tensor:
+    """NEXT-4 offline: l1 Pair-(2:4) pruning of fp16 [N, K] weight rows (q4_prune_24)."""
+    _need(w, torch.float16, "w", 2)
+    out = torch.empty_like(w)
+    check(lib().q4_prune_24(_ptr(w), w.shape[0], w.shape[1], _ptr(out), _stream()))
+    return out
+
+
+def sparse24_compress(w_codes: torch.Tensor):
+    """NEXT-4 offline: packed 2:4-sparse INT4 codes -> (values int8 [N, K/2], metadata int32
+    [N, K/32], violations) (q4_sparse24_compress)."""
+    _need(w_codes, torch.uint8, "w_codes", 2)
+    N, K = w_codes.shape[0], w_codes.shape[1] * 2
+    vals = torch.empty(N, K // 2, dtype=torch.int8, device=w_codes.device)
+    meta = torch.empty(N, K // 32, dtype=torch.int32, device=w_codes.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=w_codes.device)
+    check(lib().q4_sparse24_compress(_ptr(w_codes), N, K, _ptr(vals), _ptr(meta), _ptr(bad), _stream()))
+    return vals, meta, bad
+
+
+def w4a4_sparse24_linear(a_codes, a_scales, w_vals, w_meta, w_scales, kind=EPI_F16, *, bias=None, out=None):
+    """NEXT-4: INT4 activations x 2:4-sparse INT4 weights (compressed), F16 or I32 epilogue."""
+    _need(a_codes, torch.uint8, "a_codes", 2)
+    M, K = a_codes.shape[0], a_codes.shape[1] * 2
+    N = w_vals.shape[0]
+    o = dict(out or {})
+    key = "i32" if kind == EPI_I32 else "f16"
+    o.setdefault(key, torch.empty(M, N, dtype=torch.int32 if kind == EPI_I32 else torch.float16, device=a_codes.device))
+    e = Epilogue(kind=kind, bias=_ptr(bias), out_i32=_ptr(o.get("i32")), out_f16=_ptr(o.get("f16")))
+    check(lib().q4_w4a4_sparse24_linear(_ptr(a_codes), _ptr(a_scales), _ptr(w_vals), _ptr(w_meta), _ptr(w_scales),
+                                        M, N, K, C.byref(e), _stream()))
+    return o
+
+
 def launch_floor(n: int, ctas: int = 32):
     """Measurement only: n empty PDL kernels on the current stream (q4_launch_floor)."""
     _lib.check(_lib.lib().q4_launch_floor(int(n), int(ctas), _stream()), "q4_launch_floor")
