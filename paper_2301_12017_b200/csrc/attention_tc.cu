@@ -64,11 +64,14 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
 
 }  // namespace
 
+// QM: ctx code mode -- 0 symmetric INT4 (a1), 1 int8 (W8A8 baseline, O-11), 2 asymmetric INT4
+// (NEXT-3, O-15); one instantiation each, so the hot symmetric kernel carries no other mode.
+template <int QM>
 __global__ void __launch_bounds__(AT_THREADS, 2)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tq, int S, int heads, __half* __restrict__ ctx_f16,
                         uint8_t* __restrict__ ctx_codes, float* __restrict__ ctx_scales,
-                        unsigned long long* __restrict__ trace, int dbg, int G, int i8,
-                        float* __restrict__ ctx_zeros) {
+                        unsigned long long* __restrict__ trace, int dbg, int G, float* __restrict__ ctx_zeros) {
+  constexpr bool i8 = QM == 1, asym = QM == 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* kv_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -84,7 +87,6 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
   const int b = blockIdx.x / G, g = blockIdx.x % G;
   const int hpc = heads / G, j0 = g * hpc;
   const int row0 = b * S;  // first token of this sequence
-  const bool asym = ctx_zeros != nullptr;  // asymmetric ctx codes (NEXT-3)
 
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tq);
@@ -456,34 +458,20 @@ cluster_tail:
       if (g == 0 && r < S && !asym) ctx_scales[row0 + r] = a > 0.f ? __fdiv_rn(a, qm) : 1.0f;
     }
     __syncthreads();
-    // this CTA's columns [64 j0, 64 (j0 + hpc)): cpr 16-byte chunks (8 values) per row; eight
-    // L2 loads in flight per thread before their codes are computed
-    const int cpr = hpc * 8, tot = S * cpr;
-    for (int base = threadIdx.x; base < tot; base += 8 * AT_THREADS) {
-      uint4 xs[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = base + u * AT_THREADS;
-        if (idx < tot) {
-          const int rw = idx / cpr, c = idx - rw * cpr;
-          xs[u] = __ldcg(reinterpret_cast<const uint4*>(ctx_f16 + (size_t)(row0 + rw) * h + j0 * 64 + c * 8));
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = base + u * AT_THREADS;
-        if (idx >= tot) break;
-        const int rw = idx / cpr, c = idx - rw * cpr;
-        const float a = amx[rw];
-        const uint32_t hh[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
-        if (asym)
-          reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] = requant8_asym(hh, zmn[rw], zmx[rw]);
-        else if (i8)
-          reinterpret_cast<uint2*>(ctx_codes + (size_t)(row0 + rw) * h + j0 * 64)[c] = requant8_i8(hh, a, rr7[rw], 0.f);
-        else
-          reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] =
-              a > 0.f ? requant8(hh, a, rr7[rw], 0.f) : 0u;
-      }
+    // this CTA's columns [64 j0, 64 (j0 + hpc)): cpr 16-byte chunks (8 values) per row
+    const int cpr = hpc * 8;
+    for (int idx = threadIdx.x; idx < S * cpr; idx += AT_THREADS) {
+      const int rw = idx / cpr, c = idx - rw * cpr;
+      const float a = amx[rw];
+      const uint4 x = __ldcg(reinterpret_cast<const uint4*>(ctx_f16 + (size_t)(row0 + rw) * h + j0 * 64 + c * 8));
+      const uint32_t hh[4] = {x.x, x.y, x.z, x.w};
+      if (asym)
+        reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] = requant8_asym(hh, zmn[rw], zmx[rw]);
+      else if (i8)
+        reinterpret_cast<uint2*>(ctx_codes + (size_t)(row0 + rw) * h + j0 * 64)[c] = requant8_i8(hh, a, rr7[rw], 0.f);
+      else
+        reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] =
+            a > 0.f ? requant8(hh, a, rr7[rw], 0.f) : 0u;
     }
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
@@ -506,8 +494,10 @@ cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __ha
   }
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_AT);
-    if (e != cudaSuccess) return e;
+    for (auto k : {attention_tc_kernel<0>, attention_tc_kernel<1>, attention_tc_kernel<2>}) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_AT);
+      if (e != cudaSuccess) return e;
+    }
     configured = true;
   }
   const int h = heads * 64;
@@ -548,8 +538,9 @@ cudaError_t launch_attention_tc(const __half* qkv, int B, int S, int heads, __ha
   cfg.attrs = attr;
   static const bool no_pdl = prof_env("Q4_NO_PDL") != nullptr;  // profiling only
   cfg.numAttrs = (no_pdl || (int64_t)B * S > kPdlMaxRows) ? 1 : 2;
-  cudaError_t le = cudaLaunchKernelEx(&cfg, attention_tc_kernel, tq, S, heads, ctx_f16, ctx_codes, ctx_scales,
-                                      trace_path ? trace_buf : nullptr, dbg, G, i8 ? 1 : 0, ctx_zeros);
+  auto kern = ctx_zeros ? attention_tc_kernel<2> : i8 ? attention_tc_kernel<1> : attention_tc_kernel<0>;
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, tq, S, heads, ctx_f16, ctx_codes, ctx_scales,
+                                      trace_path ? trace_buf : nullptr, dbg, G, ctx_zeros);
   if (le != cudaSuccess) return le;
   if (trace_path) {  // profiling only: dump this launch's stamps
     static unsigned long long host[512 * 16 * 16];

@@ -633,7 +633,9 @@ Q4_DEV void gelu_epilogue(const TcParams& p, TileIter& it, uint32_t tmem, uint64
 // strategy).  The byte-level staging is the A8 path unchanged (a 128-byte
 // k-block row = 64 fp16), the MMA is kind::f16 with fp32 accumulators, and the epilogue
 // reads the accumulator as fp32 with unit scales.
-template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false>
+// ASY: a row-epilogue instantiation that also takes asymmetric input (a_zeros) and / or writes
+// asymmetric codes (out_zeros), NEXT-3; the symmetric instantiations carry none of that code.
+template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false, bool ASY = false>
 __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>::THREADS, 1)
     w4a4_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
   static_assert(!A8 || BI8, "W8A8 takes int8 weights through the BI8 path");
@@ -911,7 +913,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
       prm0[i] = p.w_scales ? p.w_scales[c0 + i] : 1.0f;
       prm0[TN + i] = p.bias ? __half2float(p.bias[c0 + i]) : 0.f;
       if (KIND == EPI_F16 && p.a_zeros) prm0[2 * TN + i] = p.w_sums[c0 + i];
-      if (E::ROW && p.a_zeros) prm0[4 * TN + i] = p.w_sums[c0 + i];  // asymmetric input: colsum
+      if (ASY && E::ROW && p.a_zeros) prm0[4 * TN + i] = p.w_sums[c0 + i];  // asymmetric input: colsum
       if constexpr (KIND == EPI_RESLN_Q4) {
         prm0[2 * TN + i] = __half2float(p.gamma[c0 + i]);
         prm0[3 * TN + i] = __half2float(p.beta[c0 + i]);
@@ -1065,7 +1067,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
             for (int u = 0; u < 4; ++u) rr[u] = rn[u];
           }
           };
-          if (p.a_zeros) pass1(std::true_type{}); else pass1(std::false_type{});
+          if (ASY && p.a_zeros) pass1(std::true_type{}); else pass1(std::false_type{});
           tmem_wait_st();
           stamp(2);
           {
@@ -1107,7 +1109,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
         // pass A: y = fp16(GELU(t)) or fp16(LN(z)); row max-abs; y -> TMEM as packed halves
         __half2 hmax = __float2half2_rn(0.f);
         // asymmetric output (NEXT-3): the row min and max of y instead of max |y|
-        const bool aout = !A8 && p.out_zeros != nullptr;
+        const bool aout = ASY && !A8 && p.out_zeros != nullptr;
         __half2 hmn = __float2half2_rn(65504.f), hmx = __float2half2_rn(-65504.f);
         const bool want_f16 = p.out_f16 != nullptr;
         const float2 nmean2 = f2(-mean), rstd2 = f2(rstd);
@@ -1136,7 +1138,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
               uint32_t v0[16], v1[16], h0[8], h1[8];
 #pragma unroll
               for (int u = 0; u < 16; ++u) { v0[u] = v[u]; v1[u] = v[16 + u]; }
-              if (p.a_zeros) {  // asymmetric input (O-16)
+              if (ASY && p.a_zeros) {  // asymmetric input (O-16)
                 gelu16<H16, true>(v0, sa2, prm + 32 * j, prm + TN + 32 * j, h0, za2, prm + 4 * TN + 32 * j);
                 gelu16<H16, true>(v1, sa2, prm + 32 * j + 16, prm + TN + 32 * j + 16, h1, za2, prm + 4 * TN + 32 * j + 16);
               } else {
@@ -1344,12 +1346,12 @@ int num_sms() {
   return n;
 }
 
-template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false>
+template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false, bool ASY = false>
 cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {
   constexpr bool R4 = PAIR && (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4);
   using C = TcCfg<TN, BI8, A8, PAIR, R4>;
   constexpr int THREADS = EpiCfg<KIND, R4>::THREADS;
-  auto kern = w4a4_tc_kernel<TN, KIND, BI8, A8, H16, PAIR>;
+  auto kern = w4a4_tc_kernel<TN, KIND, BI8, A8, H16, PAIR, ASY>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1524,8 +1526,14 @@ cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s
   switch (g.kind) {
     case EPI_I32: return run_tc<TN, EPI_I32, BI8, A8>(g, ws, wsb, s, why);
     case EPI_F16: return run_tc<TN, EPI_F16, BI8, A8>(g, ws, wsb, s, why);
-    case EPI_GELU_Q4: return run_tc<TN, EPI_GELU_Q4, BI8, A8>(g, ws, wsb, s, why);
-    case EPI_RESLN_Q4: return run_tc<TN, EPI_RESLN_Q4, BI8, A8>(g, ws, wsb, s, why);
+    case EPI_GELU_Q4:
+      if constexpr (!A8)
+        if (g.a_zeros || g.out_zeros) return run_tc<TN, EPI_GELU_Q4, BI8, false, false, false, true>(g, ws, wsb, s, why);
+      return run_tc<TN, EPI_GELU_Q4, BI8, A8>(g, ws, wsb, s, why);
+    case EPI_RESLN_Q4:
+      if constexpr (!A8)
+        if (g.a_zeros || g.out_zeros) return run_tc<TN, EPI_RESLN_Q4, BI8, false, false, false, true>(g, ws, wsb, s, why);
+      return run_tc<TN, EPI_RESLN_Q4, BI8, A8>(g, ws, wsb, s, why);
   }
   *why = "unknown epilogue kind";
   return cudaErrorInvalidValue;
