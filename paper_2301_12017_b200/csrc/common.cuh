@@ -555,17 +555,36 @@ Q4_DEV uint32_t asym_code(float x, double mn, double D, double r15) {
   return (uint32_t)(int)fmin(n, 15.0);
 }
 // 8 fp16 values (4 packed words) -> 8 asymmetric codes in one word (element i at bits 4i);
-// D <= 0 (constant row) gives all-zero codes.
+// D <= 0 (constant row) gives all-zero codes.  Fast path in fp32: d = x - mn and p = d * fl(15/D)
+// carry a relative error <= 3 * 2^-24, so |p - p_exact| <= 15 * 1.8e-7 < 3e-6 and rint(p) is the
+// exact code unless p is within 1e-5 of a half-integer; those 8-value chunks take asym_code's
+// exact fp64 residual path.
 Q4_DEV uint32_t requant8_asym(const uint32_t (&h)[4], float mn, float mx) {
   const double D = (double)mx - (double)mn;
   if (!(D > 0.0)) return 0u;
-  const double r15 = 15.0 / D, m = (double)mn;
+  const float r15f = (float)(15.0 / D);
+  const float2 mn2 = f2(-mn), r2 = f2(r15f);
   uint32_t w = 0;
+  float dmax = 0.f;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const float2 f = unpack_half2(h[j]);
-    w |= asym_code(f.x, m, D, r15) << (8 * j);
-    w |= asym_code(f.y, m, D, r15) << (8 * j + 4);
+    const float2 p = fmul2(fadd2(unpack_half2(h[j]), mn2), r2);
+    const float2 sm = fadd2(p, f2(12582912.0f));                  // rint(p) in the low bits
+    const float2 d = ffma2(fadd2(sm, f2(-12582912.0f)), f2(-1.f), p);  // p - rint(p)
+    dmax = fmaxf(dmax, fmaxf(fabsf(d.x), fabsf(d.y)));
+    const uint32_t c0 = min((uint32_t)(__float_as_int(sm.x) - 0x4B400000), 15u);
+    const uint32_t c1 = min((uint32_t)(__float_as_int(sm.y) - 0x4B400000), 15u);
+    w |= (c0 | (c1 << 4)) << (8 * j);
+  }
+  if (dmax > 0.49999f) {
+    const double r15 = 15.0 / D, m = (double)mn;
+    w = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_half2(h[j]);
+      w |= asym_code(f.x, m, D, r15) << (8 * j);
+      w |= asym_code(f.y, m, D, r15) << (8 * j + 4);
+    }
   }
   return w;
 }
