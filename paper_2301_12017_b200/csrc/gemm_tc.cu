@@ -112,7 +112,10 @@ template <int KIND, bool R4 = false> struct EpiCfg {
 template <int TN, bool BI8, bool A8 = false, bool PAIR = false, bool R4 = false>
 struct TcCfg {
   static constexpr int BM = 128, BK = 128;  // BK in int8 elements = 64 packed bytes
-  static constexpr int SP = A8 ? 1 : BI8 ? 4 : 3, SU = PAIR ? 4 : BI8 ? 3 : 2;  // packed / unpacked smem stages
+  // packed / unpacked smem stages; narrow tiles (the latency configs: few CTAs, each streaming
+  // its weight rows from HBM) keep more k-blocks in flight
+  static constexpr int SP = A8 ? 1 : BI8 ? (TN <= 64 ? 5 : 4) : 3;
+  static constexpr int SU = PAIR ? 4 : BI8 ? (TN <= 64 ? 5 : 3) : 2;
   static constexpr int A_PK = A8 ? 0 : BM * 64, B_PK = BI8 ? 0 : TN * 64;
   static constexpr int A_UN = BM * 128, B_UN = (PAIR ? TN / 2 : TN) * 128;
   static constexpr int UN_STAGE = A_UN + B_UN, PK_STAGE = A_PK + B_PK;
