@@ -72,6 +72,7 @@ struct TcParams {
   __half* yscr;       // GELU_Q4 without an fp16 tap: [grid][2 groups][2 slots][128][TN] y parking (L2)
   int pair;           // CTA-pair (cta_group::2) mainloop: cluster of 2, CTA r owns m-block 2 c + r
   int lin;            // linear tile schedule (R4): `groups` units walk the row-major tile order
+  int split;          // split-K cluster of two CTAs on the same tiles (SPLIT)
   int dbg;            // profiling only (env Q4_DEBUG_SKIP): 1 skip TMA, 2 skip unpack, 4 skip MMA, 8 skip epilogue math
   unsigned long long* trace;  // profiling only (env Q4_TRACE): [grid][64 tiles][8] %globaltimer stamps
 };
@@ -109,13 +110,17 @@ template <int KIND, bool R4 = false> struct EpiCfg {
 // PAIR (with BI8): CTA-pair mainloop -- tcgen05.mma.cta_group::2 with M = 256; each CTA
 // stages its own 128 rows of A and half of the N tile of B, so the B stage halves and the
 // unpacked ring deepens to 4 stages.
-template <int TN, bool BI8, bool A8 = false, bool PAIR = false, bool R4 = false>
+// SPLIT (small M, narrow tiles): split-K over a cluster of two CTAs; each runs half of the
+// k-blocks into its own TMEM accumulator, rank 1 pushes its partial into rank 0's shared memory
+// (DSMEM) and rank 0 adds it before the unchanged epilogue -- twice the CTAs for the latency
+// configs, whose GEMMs otherwise leave most SMs idle.
+template <int TN, bool BI8, bool A8 = false, bool PAIR = false, bool R4 = false, bool SPLIT = false>
 struct TcCfg {
   static constexpr int BM = 128, BK = 128;  // BK in int8 elements = 64 packed bytes
   // packed / unpacked smem stages; narrow tiles (the latency configs: few CTAs, each streaming
   // its weight rows from HBM) keep more k-blocks in flight
-  static constexpr int SP = A8 ? 1 : BI8 ? (TN <= 64 ? 5 : 4) : 3;
-  static constexpr int SU = PAIR ? 4 : BI8 ? (TN <= 64 ? 5 : 3) : 2;
+  static constexpr int SP = A8 ? 1 : BI8 ? (SPLIT ? 3 : TN <= 64 ? 5 : 4) : 3;
+  static constexpr int SU = PAIR ? 4 : BI8 ? (SPLIT ? 3 : TN <= 64 ? 5 : 3) : 2;
   static constexpr int A_PK = A8 ? 0 : BM * 64, B_PK = BI8 ? 0 : TN * 64;
   static constexpr int A_UN = BM * 128, B_UN = (PAIR ? TN / 2 : TN) * 128;
   static constexpr int UN_STAGE = A_UN + B_UN, PK_STAGE = A_PK + B_PK;
@@ -125,8 +130,9 @@ struct TcCfg {
   static constexpr int OFF_STG = OFF_PK + SP * PK_STAGE;
   static constexpr int OFF_PRM = OFF_STG + NSLAB * 4096;  // [R4 ? 4 groups : 1][5][TN] fp32 column params
   static constexpr int OFF_ROW = OFF_PRM + (R4 ? 4 : 1) * 5 * TN * 4;  // [2 groups][2 sides][128] float4 row partials
-  static constexpr int OFF_BAR = OFF_ROW + (R4 ? 0 : 2 * 2 * 128 * 16);
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int OFF_SRED = OFF_ROW + (R4 ? 0 : 2 * 2 * 128 * 16);  // SPLIT: [2][128][TN] int32 partials
+  static constexpr int OFF_BAR = OFF_SRED + (SPLIT ? 2 * 128 * TN * 4 : 0);
+  static constexpr int SMEM = OFF_BAR + 512 + 1024;
   static constexpr int NBUF = R4 ? 4 : 2;
   static constexpr int TMEM_COLS = NBUF * TN <= 64 ? 64 : NBUF * TN <= 128 ? 128 : NBUF * TN <= 256 ? 256 : 512;
   static_assert(NBUF * TN <= 512, "TMEM");
@@ -149,7 +155,7 @@ struct TileIter {
     pair = p.pair;
     lin = p.lin;
     ntn = p.ntn;
-    const int c = pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int c = (pair || p.split) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     sub = pair ? (int)(blockIdx.x & 1) : 0;
     mblocks = pair ? p.mblocks / 2 : p.mblocks;
     rank = lin ? 0 : c % p.ntn;
@@ -638,7 +644,8 @@ Q4_DEV void gelu_epilogue(const TcParams& p, TileIter& it, uint32_t tmem, uint64
 // reads the accumulator as fp32 with unit scales.
 // ASY: a row-epilogue instantiation that also takes asymmetric input (a_zeros) and / or writes
 // asymmetric codes (out_zeros), NEXT-3; the symmetric instantiations carry none of that code.
-template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false, bool ASY = false>
+template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false, bool ASY = false,
+          bool SPLIT = false>
 __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>::THREADS, 1)
     w4a4_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
   static_assert(!A8 || BI8, "W8A8 takes int8 weights through the BI8 path");
@@ -648,7 +655,8 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
   constexpr bool R4 = PAIR && (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4);
   static_assert(!R4 || TN == 128, "R4 tiles are 256 x 128 per pair");
   using E = EpiCfg<KIND, R4>;
-  using C = TcCfg<TN, BI8, A8, PAIR, R4>;
+  static_assert(!(SPLIT && (PAIR || R4)), "split-K runs on the 1-CTA mainloop");
+  using C = TcCfg<TN, BI8, A8, PAIR, R4, SPLIT>;
   constexpr int NBUF = E::NBUF;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -658,7 +666,9 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
   uint64_t* empty_u = full_u + C::SU;
   uint64_t* tfull = empty_u + C::SU;   // [NBUF]
   uint64_t* tempty = tfull + NBUF;     // [NBUF]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+  uint64_t* redfull = tempty + NBUF;   // SPLIT [2]: rank 0 -- rank 1's partial of buffer b has landed
+  uint64_t* redempty = redfull + 2;    // SPLIT [2]: rank 1 -- rank 0 has consumed it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(redempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (p.K + C::BK - 1) / C::BK;
@@ -677,6 +687,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
     // counts both CTAs' epilogue warps
     for (int i = 0; i < C::SU; ++i) { mbar_init(&full_u[i], A8 ? 1 : PAIR ? 9 : BI8 ? 5 : 4); mbar_init(&empty_u[i], 1); }
     for (int i = 0; i < NBUF; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], (PAIR ? 2 : 1) * E::EPW); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&redfull[i], E::EPW); mbar_init(&redempty[i], E::EPW); }
     fence_mbar_init();
   }
   if constexpr (PAIR) {
@@ -692,10 +703,12 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
   } else {
     if (warp == WM) tmem_alloc(tmem_slot, C::TMEM_COLS);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (SPLIT) cluster_sync(); else __syncthreads();  // SPLIT: remote arrives need both CTAs' barriers
     tc_fence_after();
   }
-  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+  const uint32_t crank = (PAIR || SPLIT) ? cluster_ctarank() : 0u;
+  // SPLIT: this CTA's half of the k-blocks (rank 0 the first half)
+  const int kb0 = SPLIT ? (int)crank * (KB / 2) : 0, kb1 = SPLIT ? (crank ? KB : KB / 2) : KB;
   // pair: shared::cluster address of a barrier in the leader CTA (rank 0)
   auto lead = [&](uint64_t* bar) -> uint32_t { return PAIR ? mapa(smem_u32(bar), 0) : smem_u32(bar); };
   const uint32_t tmem = *tmem_slot;
@@ -716,7 +729,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
       while (it.next(mb, nb)) {
         if constexpr (A8) {
           // both int8 operands straight into the swizzled MMA stage
-          for (int kb = 0; kb < KB; ++kb, ++g) {
+          for (int kb = kb0; kb < kb1; ++kb, ++g) {
             const int su = g % C::SU;
             mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
             uint8_t* ub = smem + C::OFF_UN + su * C::UN_STAGE;
@@ -741,7 +754,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
           }
           continue;
         }
-        for (int kb = 0; kb < KB; ++kb, ++g) {
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % C::SP;
           mbar_wait(&empty_p[s], ((g / C::SP) & 1u) ^ 1u);
           uint8_t* pk = smem + C::OFF_PK + s * C::PK_STAGE;
@@ -793,7 +806,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
         const unsigned long long m1 = mtr ? gtimer() : 0;
         unsigned long long mw = 0;
         const uint32_t dt = tmem + b * TN;
-        for (int kb = 0; kb < KB; ++kb, ++g) {
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int su = g % C::SU;
           const unsigned long long w0 = mtr ? gtimer() : 0;
           if constexpr (PAIR) mbar_wait_cluster(&full_u[su], (g / C::SU) & 1u);
@@ -810,14 +823,14 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                     "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
                     "l"(umma_smem_desc(ua + ks * 32, 1024, 2)), "l"(umma_smem_desc(ub + ks * 32, 1024, 2)),
-                    "r"(idesc), "r"((uint32_t)((kb | ks) != 0))
+                    "r"(idesc), "r"((uint32_t)(kb != kb0 || ks != 0))
                     : "memory");
               else if constexpr (H16)
                 umma_f16kk(dt, umma_smem_desc(ua + ks * 32, 1024, 2), umma_smem_desc(ub + ks * 32, 1024, 2), idesc,
-                           (kb | ks) != 0);
+                           kb != kb0 || ks != 0);
               else
                 umma_i8(dt, umma_smem_desc(ua + ks * 32, 1024, 2), umma_smem_desc(ub + ks * 32, 1024, 2), idesc,
-                        (kb | ks) != 0);
+                        kb != kb0 || ks != 0);
             }
           }
           if constexpr (PAIR)
@@ -848,7 +861,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
     // profiling only (Q4_TRACE): k-block phase durations of thread 64, trace slot 63 of this CTA
     unsigned long long* utr = (p.trace && t == 0) ? p.trace + ((size_t)blockIdx.x * 64 + 63) * 8 : nullptr;
     while (!A8 && it.next(mb, nb)) {
-      for (int kb = 0; kb < KB; ++kb, ++g) {
+      for (int kb = kb0; kb < kb1; ++kb, ++g) {
         const int s = g % C::SP, su = g % C::SU;
         const unsigned long long u0 = utr ? gtimer() : 0;
         // Row epilogues: the first unpack warp polls both barriers and the other three block
@@ -974,6 +987,58 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
       named_bar(gbar, GT);
       tc_fence_after();
       stamp(1);
+      if constexpr (SPLIT) {
+        // split-K: sred[b][row] holds rank 1's partial accumulator row, 16-byte chunks XOR-swizzled
+        // by row (conflict-free row-per-thread reads); chunks owned as in the epilogue (j = sub + NS i)
+        const uint32_t rph = (tcount / NBUF) & 1u;
+        uint8_t* srow = smem + C::OFF_SRED + (size_t)b * 128 * TN * 4 + (size_t)r * TN * 4;
+        auto soff = [&](int c16) { return (uint32_t)((c16 & ~7) | ((c16 ^ r) & 7)) << 4; };
+        if (crank == 1) {
+          if (ew % EPW == 0) mbar_wait(&redempty[b], rph ^ 1u);  // rank 0 consumed the previous one
+          named_bar(gbar, GT);
+          const uint32_t rbase = mapa(smem_u32(srow), 0);
+          for (int j = sub; j < TN / 32; j += NS) {
+            uint32_t v[32];
+            tmem_ld32(tbase + 32 * j, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + soff(8 * j + u)),
+                           "r"(v[4 * u]), "r"(v[4 * u + 1]), "r"(v[4 * u + 2]), "r"(v[4 * u + 3])
+                           : "memory");
+          }
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa(smem_u32(&redfull[b]), 0))
+                         : "memory");
+          // this CTA's accumulator is no longer needed: the MMA of its next tile may start
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[b]);
+          ++tcount;
+          continue;
+        }
+        if (ew % EPW == 0) mbar_wait_cluster(&redfull[b], rph);
+        named_bar(gbar, GT);
+        for (int j = sub; j < TN / 32; j += NS) {
+          uint32_t v[32];
+          tmem_ld32(tbase + 32 * j, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint4 x = *reinterpret_cast<const uint4*>(srow + soff(8 * j + u));
+            v[4 * u] += x.x; v[4 * u + 1] += x.y; v[4 * u + 2] += x.z; v[4 * u + 3] += x.w;
+          }
+          tmem_st32(tbase + 32 * j, v);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(mapa(smem_u32(&redempty[b]), 1)) : "memory");
+        named_bar(gbar, GT);
+        tc_fence_after();
+      }
 
       if constexpr (KIND == EPI_I32) {
         for (int j = sub; j < NCH; j += NS) {
@@ -1297,6 +1362,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS)
                    : "memory");
   } else {
+    if constexpr (SPLIT) cluster_sync();  // rank 1's remote stores / arrives into rank 0 have landed
     if (warp == WM) tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
@@ -1349,12 +1415,13 @@ int num_sms() {
   return n;
 }
 
-template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false, bool ASY = false>
+template <int TN, int KIND, bool BI8, bool A8, bool H16 = false, bool PAIR = false, bool ASY = false,
+          bool SPLIT = false>
 cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s, const char** why) {
   constexpr bool R4 = PAIR && (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4);
-  using C = TcCfg<TN, BI8, A8, PAIR, R4>;
+  using C = TcCfg<TN, BI8, A8, PAIR, R4, SPLIT>;
   constexpr int THREADS = EpiCfg<KIND, R4>::THREADS;
-  auto kern = w4a4_tc_kernel<TN, KIND, BI8, A8, H16, PAIR, ASY>;
+  auto kern = w4a4_tc_kernel<TN, KIND, BI8, A8, H16, PAIR, ASY, SPLIT>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1379,6 +1446,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.a_zeros = g.a_zeros; p.w_sums = g.w_sums;
   p.pair = PAIR ? 1 : 0;
   p.lin = R4 ? 1 : 0;
+  p.split = SPLIT ? 1 : 0;
   p.bias = g.bias; p.residual = g.residual; p.gamma = g.gamma; p.beta = g.beta;
   p.ln_eps = g.ln_eps; p.clip = g.clip;
   p.out_i32 = g.out_i32; p.out_f16 = g.out_f16; p.out_codes = g.out_codes; p.out_scales = g.out_scales;
@@ -1397,7 +1465,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   const int sms = num_sms();
   // groups of ntn co-resident CTAs (one per SM); a group walks the m-blocks.  Pairs: the unit
   // is a 2-CTA cluster (two SMs) walking m-block pairs.
-  const int units = PAIR ? sms / 2 : sms, mwalk = PAIR ? p.mblocks / 2 : p.mblocks;
+  const int units = (PAIR || SPLIT) ? sms / 2 : sms, mwalk = PAIR ? p.mblocks / 2 : p.mblocks;
   int grid;
   if constexpr (R4) {
     // linear schedule over every co-resident CTA pair (the row rendezvous spins, so all
@@ -1426,7 +1494,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     if (p.ntn > units) { *why = "N/TN exceeds the number of SMs"; return cudaErrorNotSupported; }
     p.groups = units / p.ntn;
     if (p.groups > mwalk) p.groups = mwalk;
-    grid = p.groups * p.ntn * (PAIR ? 2 : 1);
+    grid = p.groups * p.ntn * ((PAIR || SPLIT) ? 2 : 1);
   }
   if (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4) {
     const size_t need = tc_workspace_bytes(g.M, g.N, TN, KIND);
@@ -1449,19 +1517,22 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   note_launch();
   {
     cudaError_t le;
-    if constexpr (PAIR) {
+    if constexpr (PAIR || SPLIT) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
       cfg.blockDim = dim3(THREADS);
       cfg.dynamicSmemBytes = C::SMEM;
       cfg.stream = s;
-      cudaLaunchAttribute at[1];
+      cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = 2;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // SPLIT: the small-M latency path
+      at[1].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = at;
-      cfg.numAttrs = 1;
+      static const bool no_pdl = prof_env("Q4_NO_PDL") != nullptr;  // profiling only
+      cfg.numAttrs = (SPLIT && !no_pdl) ? 2 : 1;
       le = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
     } else {
       le = launch_pdl(g.M <= kPdlMaxRows, kern, dim3(grid), dim3(THREADS), C::SMEM, s, ta, tb, p);
@@ -1498,8 +1569,28 @@ bool tc_pair_enabled() {
   return env != 0;
 }
 
+// Split-K over a CTA cluster for the latency configs (M <= 512, TN = 64, >= 4 k-blocks): correct
+// (the small-M parity tests pass through it) but measured slower -- BERT-base bs 1 per layer QKV
+// 7.1 -> 9.7 us, O-proj 14.3 -> 18.1, FFN1 11.4 -> 14.4, FFN2 21.0 -> 21.5 (cluster prologue,
+// shallower rings, the DSMEM reduction on the chain) -- so it is off; Q4_SPLIT=1 in the
+// profiling build selects it (A/B only).
+bool tc_split_enabled() {
+  static const int env = [] { const char* e = prof_env("Q4_SPLIT"); return e ? atoi(e) : 0; }();
+  return env == 1;
+}
+
 template <int TN, bool BI8, bool A8 = false>
 cudaError_t run_tc_kind2(const GemmArgs& g, void* ws, size_t wsb, cudaStream_t s, const char** why) {
+  if constexpr (TN == 64 && BI8) {
+    if (!g.f16_ops && !g.a_zeros && !g.out_zeros && g.M <= 512 && g.K / 128 >= 4 && tc_split_enabled()) {
+      switch (g.kind) {
+        case EPI_I32: return run_tc<64, EPI_I32, true, A8, false, false, false, true>(g, ws, wsb, s, why);
+        case EPI_F16: return run_tc<64, EPI_F16, true, A8, false, false, false, true>(g, ws, wsb, s, why);
+        case EPI_GELU_Q4: return run_tc<64, EPI_GELU_Q4, true, A8, false, false, false, true>(g, ws, wsb, s, why);
+        case EPI_RESLN_Q4: return run_tc<64, EPI_RESLN_Q4, true, A8, false, false, false, true>(g, ws, wsb, s, why);
+      }
+    }
+  }
   if constexpr (A8) {
     if (!g.f16_ops && TN == 256 && g.M % 256 == 0 && g.M >= 8192 && (g.kind == EPI_F16 || g.kind == EPI_I32) &&
         g.N / TN <= num_sms() / 2 && g.mainloop != Q4_MAINLOOP_TCGEN05_W8_1CTA && tc_pair_enabled()) {  // W8A8 on the CTA-pair mainloop
