@@ -604,6 +604,20 @@ def side_measurements(q4, synth, torch, np, dev, args):
         out[name] = t[100]
         out[name.replace("p50", "p10")] = t[20]
         out[name.replace("p50", "p90")] = t[180]
+        # cold L2: a 256 MB write (> the 126 MB L2) before every replay, timed outside the pair
+        # of events around the replay, so weights and activations come from HBM each time
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(100)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(100)]
+        for i in range(100):
+            flush.fill_(i & 0xFF)
+            ev0[i].record(stream)
+            enc.replay()
+            ev1[i].record(stream)
+        torch.cuda.synchronize()
+        t = sorted(ev0[i].elapsed_time(ev1[i]) for i in range(100))
+        out[name.replace("bs1_p50", "bs1_cold_l2_p50")] = t[50]
+        del flush
     # Latency floor (SURVEY 8(d) configs[2]): a CUDA graph of as many empty PDL kernels as the
     # 12-layer bs-1 forward launches (1 + 12 x 5), same launch attributes, p50 of 200 replays
     for nk, nm in ((61, "latency_floor_61_empty_kernels_ms"), (6, "latency_floor_6_empty_kernels_ms")):
