@@ -149,8 +149,11 @@ typedef struct {
  * (the INT32 accumulator bound |acc| <= 64 K); N / tile_n <= #SMs (every CTA owns one n-block,
  * tile_n = 256 for M > 512, 64 below: N <= 37,888 resp. 9,472 on B200; larger N returns
  * Q4_EUNSUPPORTED); all pointers 16-byte aligned.  Workspace: q4_w4a4_linear_workspace bytes
- * (row epilogues: the cross-CTA exchange slots and self-resetting counters; zero-filled once
- * before first use, left zeroed by every launch); 0 for I32 / F16. */
+ * (row epilogues: the cross-CTA exchange slots and self-resetting counters; M <= 256, every
+ * kind: the split-K region -- tile counters and INT32 partial sums that several CTAs add into
+ * with integer reductions, exact in any order, DESIGN.md 4.3 -- which the last CTA of each
+ * tile zeroes again; zero-filled once before first use, left zeroed by every launch).  I32 /
+ * F16 at M > 256 need none; a NULL / short workspace there just disables split-K. */
 Q4_API size_t q4_w4a4_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind);
 Q4_API q4_status q4_w4a4_linear(const uint8_t* a_codes, const float* a_scales, /* [M,K/2], [M] */
                          const uint8_t* w_codes, const float* w_scales, /* [N,K/2], [N] */

@@ -46,6 +46,16 @@ enum { EPI_I32 = 0, EPI_F16 = 1, EPI_GELU_Q4 = 2, EPI_RESLN_Q4 = 3 };
 #define Q4_GELU_DECOUPLED 0
 #endif
 
+// split-K only pays for long k-loops (measured, BERT-base batch 1, 12 layers eager: splitting
+// the K = 768 GEMMs too costs 0.737 -> 0.727..0.795 ms, the reduction round trip outweighs the
+// few k-blocks saved; the K = 3072 FFN2 alone: 0.737 -> 0.707 ms with slices of 4 k-blocks,
+// 0.702 with slices of 2): >= kKsplitMinLoop k-blocks of 128, slices of >= kKsplitMinKb
+constexpr int kKsplitMaxRows = 256, kKsplitMaxN = 8192, kKsplitMinKb = 2, kKsplitMinLoop = 16;
+constexpr size_t kKsplitCntBytes = 1024;  // per m-block: N / TN <= 256 tile counters
+int tc_ksplit(int M, int N, int K, int TN);
+size_t tc_ksplit_bytes(int M);
+size_t tc_counter_bytes(int M);
+
 struct TcParams {
   int M, N, K;
   int ntn;      // N / TN (tiles along N == CTAs per row group for row epilogues)
@@ -73,6 +83,14 @@ struct TcParams {
   int pair;           // CTA-pair (cta_group::2) mainloop: cluster of 2, CTA r owns m-block 2 c + r
   int lin;            // linear tile schedule (R4): `groups` units walk the row-major tile order
   int split;          // split-K cluster of two CTAs on the same tiles (SPLIT)
+  // split-K over global INT32 reductions (small M, DESIGN.md 4.3 "latency configs"): ksplit CTAs
+  // (consecutive blockIdx) share one tile, each runs K / ksplit; each adds its partial into
+  // kpart (red.add: integer sums are order-free, so the total is exact) and the last to arrive
+  // (kcnt) reads the total back into its TMEM, zeroes kpart / kcnt and runs the unchanged
+  // epilogue.  1 = off.
+  int ksplit;
+  int32_t* kpart;     // [mblocks][ntn][TN][128] INT32 partial sums (zero at rest)
+  unsigned* kcnt;     // [mblocks][ntn] arrivals (zero at rest)
   int dbg;            // profiling only (env Q4_DEBUG_SKIP): 1 skip TMA, 2 skip unpack, 4 skip MMA, 8 skip epilogue math
   unsigned long long* trace;  // profiling only (env Q4_TRACE): [grid][64 tiles][8] %globaltimer stamps
 };
@@ -155,7 +173,7 @@ struct TileIter {
     pair = p.pair;
     lin = p.lin;
     ntn = p.ntn;
-    const int c = (pair || p.split) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int c = (pair || p.split) ? (int)(blockIdx.x >> 1) : p.ksplit > 1 ? (int)blockIdx.x / p.ksplit : (int)blockIdx.x;
     sub = pair ? (int)(blockIdx.x & 1) : 0;
     mblocks = pair ? p.mblocks / 2 : p.mblocks;
     rank = lin ? 0 : c % p.ntn;
@@ -669,6 +687,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
   uint64_t* redfull = tempty + NBUF;   // SPLIT [2]: rank 0 -- rank 1's partial of buffer b has landed
   uint64_t* redempty = redfull + 2;    // SPLIT [2]: rank 1 -- rank 0 has consumed it
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(redempty + 2);
+  uint32_t* kflag = tmem_slot + 1;    // [NBUF] split-K: this CTA's slice arrived last
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (p.K + C::BK - 1) / C::BK;
@@ -708,14 +727,20 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
   }
   const uint32_t crank = (PAIR || SPLIT) ? cluster_ctarank() : 0u;
   // SPLIT: this CTA's half of the k-blocks (rank 0 the first half)
-  const int kb0 = SPLIT ? (int)crank * (KB / 2) : 0, kb1 = SPLIT ? (crank ? KB : KB / 2) : KB;
+  // split-K over global reductions: slice kslice of p.ksplit (consecutive CTAs share a tile)
+  const int ksp = TN <= 64 ? p.ksplit : 1;  // only the narrow small-M tiles split
+  const int kslice = ksp > 1 ? (int)(blockIdx.x % (unsigned)ksp) : 0;
+  const int kb0 = SPLIT ? (int)crank * (KB / 2) : ksp > 1 ? kslice * KB / ksp : 0;
+  const int kb1 = SPLIT ? (crank ? KB : KB / 2) : ksp > 1 ? (kslice + 1) * KB / ksp : KB;
   // pair: shared::cluster address of a barrier in the leader CTA (rank 0)
   auto lead = [&](uint64_t* bar) -> uint32_t { return PAIR ? mapa(smem_u32(bar), 0) : smem_u32(bar); };
   const uint32_t tmem = *tmem_slot;
   TileIter it(p);
   int mb, nb;
   pdl_launch_dependents();
-  pdl_wait();  // everything below may read the previous kernel's outputs
+  // everything below may read the previous kernel's outputs -- except the TMA producer's first
+  // weight tiles, which it issues before its own wait (the weights are constant)
+  if (warp != WP) pdl_wait();
 
   // Register rebalancing (row epilogues): one setmaxnreg per side, executed by whole
   // warpgroups at a single call site that dominates that side's code.
@@ -724,6 +749,23 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(E::MAINLOOP_REGS));
   if (warp == WP) {
     // ---------------------------------------------------------------- TMA producer
+    // Weight (B) tiles of the first k-blocks of the first tile, up to one ring's worth, start
+    // before griddepcontrol.wait: under programmatic dependent launch they stream in while the
+    // previous kernel is still running (the latency configs' GEMMs wait on their weights).
+    uint32_t pre = 0;
+    if constexpr (BI8 && !PAIR && !SPLIT) {
+      if (lane == 0) {
+        TileIter it0(p);
+        int mb0, nb0;
+        if (it0.next(mb0, nb0))
+          for (int kb = kb0; kb < kb1 && pre < (uint32_t)C::SU; ++kb, ++pre) {
+            uint8_t* ub = smem + C::OFF_UN + pre * C::UN_STAGE;
+            mbar_arrive_expect_tx(&full_u[pre], (uint32_t)(A8 ? C::UN_STAGE : C::B_UN));
+            tma_load_2d(ub + C::A_UN, &tmB, &full_u[pre], kb * 128, nb0 * TN);
+          }
+      }
+    }
+    pdl_wait();
     if (lane == 0) {
       uint32_t g = 0;
       while (it.next(mb, nb)) {
@@ -746,6 +788,8 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
                   " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(ub + C::A_UN)), "l"(reinterpret_cast<uint64_t>(&tmB)),
                   "r"(lead(&full_u[su])), "r"(kb * 128), "r"(nb * TN + (int)crank * (TN / 2))
                   : "memory");
+            } else if (g < pre) {
+              tma_load_2d(ub, &tmA, &full_u[su], kb * 128, mb * C::BM);  // B (and the tx count) went first
             } else {
               mbar_arrive_expect_tx(&full_u[su], (uint32_t)C::UN_STAGE);
               tma_load_2d(ub, &tmA, &full_u[su], kb * 128, mb * C::BM);
@@ -768,6 +812,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
           if constexpr (BI8) {
             // int8 weights straight into the (swizzled) operand stage of this k-block
             const int su = g % C::SU;
+            if (g < pre) continue;  // issued before griddepcontrol.wait
             mbar_wait(&empty_u[su], ((g / C::SU) & 1u) ^ 1u);
             uint8_t* ub = smem + C::OFF_UN + su * C::UN_STAGE + C::A_UN;
             if constexpr (PAIR) {
@@ -987,6 +1032,47 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
       named_bar(gbar, GT);
       tc_fence_after();
       stamp(1);
+      if constexpr (!H16 && !PAIR && TN <= 64) {  // the narrow small-M tiles only
+        if (p.ksplit > 1) {
+          // split-K over global reductions: add this slice's INT32 partial (coalesced: lane = row),
+          // count the arrival; the last slice reads the exact total back into its TMEM.
+          const size_t tile = (size_t)mb * p.ntn + nb;
+          int32_t* kp = p.kpart + tile * (TN * 128) + r;
+          for (int j = sub; j < NCH; j += NS) {
+            uint32_t v[32];
+            tmem_ld32(tbase + 32 * j, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+              asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(kp + (32 * j + u) * 128), "r"(v[u]) : "memory");
+          }
+          named_bar(gbar, GT);
+          if (leader) {
+            unsigned old;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.kcnt + tile) : "memory");
+            kflag[grp] = old == (unsigned)p.ksplit - 1u;
+            if (old == (unsigned)p.ksplit - 1u) p.kcnt[tile] = 0u;  // every slice has arrived: reset
+          }
+          named_bar(gbar, GT);
+          if (!kflag[grp]) {
+            // not the last slice: this CTA's part of the tile is done
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[b]);
+            ++tcount;
+            continue;
+          }
+          for (int j = sub; j < NCH; j += NS) {
+            uint32_t v[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] = (uint32_t)__ldcg(kp + (32 * j + u) * 128);
+#pragma unroll
+            for (int u = 0; u < 32; ++u) __stcg(kp + (32 * j + u) * 128, 0);  // zero at rest again
+            tmem_st32(tbase + 32 * j, v);
+          }
+          tmem_wait_st();
+        }
+      }
       if constexpr (SPLIT) {
         // split-K: sred[b][row] holds rank 1's partial accumulator row, 16-byte chunks XOR-swizzled
         // by row (conflict-free row-per-thread reads); chunks owned as in the epilogue (j = sub + NS i)
@@ -1447,6 +1533,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.pair = PAIR ? 1 : 0;
   p.lin = R4 ? 1 : 0;
   p.split = SPLIT ? 1 : 0;
+  p.ksplit = 1; p.kpart = nullptr; p.kcnt = nullptr;
   p.bias = g.bias; p.residual = g.residual; p.gamma = g.gamma; p.beta = g.beta;
   p.ln_eps = g.ln_eps; p.clip = g.clip;
   p.out_i32 = g.out_i32; p.out_f16 = g.out_f16; p.out_codes = g.out_codes; p.out_scales = g.out_scales;
@@ -1492,9 +1579,20 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     grid = 2 * p.groups;
   } else {
     if (p.ntn > units) { *why = "N/TN exceeds the number of SMs"; return cudaErrorNotSupported; }
-    p.groups = units / p.ntn;
+    if constexpr (!PAIR && !SPLIT && !H16 && TN <= 64) {
+      // split-K over global reductions (small M): needs the workspace's zero-at-rest prefix
+      const int ks = tc_ksplit(g.M, g.N, g.K, TN);
+      const size_t cb = tc_counter_bytes(g.M);
+      if (ks > 1 && ws && ws_bytes >= cb + tc_ksplit_bytes(g.M)) {
+        uint8_t* w = reinterpret_cast<uint8_t*>(ws) + cb;
+        p.ksplit = ks;
+        p.kcnt = reinterpret_cast<unsigned*>(w);
+        p.kpart = reinterpret_cast<int32_t*>(w + (size_t)p.mblocks * kKsplitCntBytes);
+      }
+    }
+    p.groups = units / (p.ntn * p.ksplit);
     if (p.groups > mwalk) p.groups = mwalk;
-    grid = p.groups * p.ntn * ((PAIR || SPLIT) ? 2 : 1);
+    grid = p.groups * p.ntn * p.ksplit * ((PAIR || SPLIT) ? 2 : 1);
   }
   if (KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4) {
     const size_t need = tc_workspace_bytes(g.M, g.N, TN, KIND);
@@ -1503,7 +1601,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     // and any N (a layer's RESLN N = hidden and GELU N = ffn) share one workspace, and one
     // launch's float partials never land on another launch's counters
     uint8_t* w = reinterpret_cast<uint8_t*>(ws);
-    const size_t nslot = (size_t)p.mblocks * p.ntn * 128, cnt_bytes = tc_counter_bytes(g.M);
+    const size_t nslot = (size_t)p.mblocks * p.ntn * 128, cnt_bytes = tc_counter_bytes(g.M) + tc_ksplit_bytes(g.M);
     p.xcnt = reinterpret_cast<unsigned*>(w);
     p.xstat = reinterpret_cast<float2*>(w + cnt_bytes);
     p.xamax = reinterpret_cast<float*>(w + cnt_bytes + nslot * 8);
@@ -1663,6 +1761,28 @@ size_t tc_counter_bytes(int M) {
   return (4 * mblocks * sizeof(unsigned) + 255) & ~(size_t)255;
 }
 
+// Split-K over global reductions for the latency configs (M <= kKsplitMaxRows): slices of at
+// least kKsplitMinKb k-blocks, as many as fit one CTA per SM next to the other tiles.
+int tc_ksplit(int M, int N, int K, int TN) {
+  // profiling only: Q4_KSPLIT forces the split (0 = off), Q4_KSPLIT_MINKB the k-loop threshold
+  static const int env = prof_env("Q4_KSPLIT") && *prof_env("Q4_KSPLIT") ? atoi(prof_env("Q4_KSPLIT")) : -1;
+  static const int minkb = prof_env("Q4_KSPLIT_MINKB") ? atoi(prof_env("Q4_KSPLIT_MINKB")) : kKsplitMinLoop;
+  if (M <= 0 || M > kKsplitMaxRows || N > kKsplitMaxN || TN > 64 || env == 0) return 1;
+  const int KB = (K + 127) / 128, tiles = ((M + 127) / 128) * (N / TN);
+  if (KB < minkb) return 1;
+  int s = num_sms() / tiles;
+  if (s > KB / kKsplitMinKb) s = KB / kKsplitMinKb;
+  if (env > 1 && env <= KB && env * tiles <= num_sms()) s = env;
+  return s >= 2 ? s : 1;
+}
+// The zero-at-rest split-K region after the rendezvous counters: [mblocks] x (tile counters |
+// INT32 partials for N <= kKsplitMaxN); its offset and size depend on M only.
+size_t tc_ksplit_bytes(int M) {
+  if (M <= 0 || M > kKsplitMaxRows) return 0;
+  const size_t mblocks = (size_t)(M + 127) / 128;
+  return mblocks * (kKsplitCntBytes + (size_t)kKsplitMaxN * 128 * 4);
+}
+
 // CTAs of a row-epilogue launch (the grid run_tc picks): groups of ntn co-resident CTAs
 size_t tc_row_grid(int M, int N, int TN) {
   const size_t mblocks = (size_t)(M + 127) / 128, ntn = (size_t)N / TN;
@@ -1673,9 +1793,13 @@ size_t tc_row_grid(int M, int N, int TN) {
 
 size_t tc_workspace_bytes(int M, int N, int TN, int kind) {
   if (TN <= 0) return 0;
+  if (kind != EPI_GELU_Q4 && kind != EPI_RESLN_Q4) {
+    const size_t k = tc_ksplit_bytes(M);
+    return k ? tc_counter_bytes(M) + k : 0;  // F16 / I32: the split-K region only
+  }
   // partial slots for ntn = N / min(TN, 128): the R4 row kernel (TN = 128) may run instead
   const size_t mblocks = (size_t)(M + 127) / 128, ntn = (size_t)N / (TN < 128 ? TN : 128);
-  size_t b = tc_counter_bytes(M) + mblocks * ntn * 128 * 20;  // stats (8) | amax (4) | asym min/max (8)
+  size_t b = tc_counter_bytes(M) + tc_ksplit_bytes(M) + mblocks * ntn * 128 * 20;  // stats (8) | amax (4) | asym min/max (8)
   // GELU_Q4: two y parking slots per epilogue group (pass B of tile t runs after pass A of t + 2)
   if (kind == EPI_GELU_Q4 && Q4_GELU_DECOUPLED) b += tc_row_grid(M, N, TN) * 4 * 128 * (size_t)TN * 2;
   return b;

@@ -338,7 +338,7 @@ q4_status q4_f16_linear(const uint16_t* a, const uint16_t* w, int64_t M, int64_t
 
 size_t q4_w4a4_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t kind) {
   (void)K;
-  if (kind != Q4_EPI_GELU_Q4 && kind != Q4_EPI_RESLN_Q4) return 0;
+  if (kind != Q4_EPI_GELU_Q4 && kind != Q4_EPI_RESLN_Q4 && kind != Q4_EPI_F16 && kind != Q4_EPI_I32) return 0;
   if (M <= 0 || N <= 0 || M > (1ll << 31) - 1 || N > (1 << 24)) return 0;
   return q4::tc_workspace_bytes((int)M, (int)N, q4::tc_tile_n((int)M, (int)N, kind), kind);
 }

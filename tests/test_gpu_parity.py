@@ -561,3 +561,64 @@ def test_r4_row_epilogues(q4, M, N, K, kind):
     for _ in range(2):
         o2 = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), epi, **args)
         assert np.array_equal(host(o2["codes"]), c2) and np.array_equal(host(o2["f16"]), y)
+
+
+# ------------------------------------------------------------------ split-K (latency configs)
+# split-K applies to k-loops of >= 16 k-blocks of 128 (K >= 2048): the BERT FFN2 and the
+# like; K = 2240 gives ragged slices (18 k-blocks, the last one partial, over 4 slices)
+SPLITK_SHAPES = [(128, 768, 3072, "resln"), (128, 768, 2240, "resln"), (128, 3072, 2048, "gelu"),
+                 (128, 2304, 2240, "f16"), (77, 1024, 4096, "f16"), (200, 768, 3072, "i32"),
+                 (256, 1024, 4096, "resln"), (1, 768, 2240, "i32"), (130, 768, 3072, "gelu"),
+                 (64, 1024, 8192, "i32")]
+
+
+@pytest.mark.parametrize("M,N,K,kind", SPLITK_SHAPES)
+@pytest.mark.parametrize("mainloop", [1, 4], ids=["tcgen05", "tcgen05_w8"])
+def test_split_k_small_m(q4, M, N, K, kind, mainloop):
+    """M <= 256: the narrow-tile GEMMs split K over up to #SMs / tiles CTAs that add INT32
+    partials with global integer reductions (exact in any order); the last CTA of a tile
+    runs the epilogue on the total.  Ragged k-slices (K / 128 not a multiple of the split)
+    and ragged M included; three launches on one workspace check that the partial sums and
+    tile counters are left zeroed."""
+    x, wt, b = synth.hidden(M, K, f"skx{M}_{K}"), synth.weight(N, K, f"skw{N}_{K}"), synth.bias(N, f"skb{N}")
+    a, sa = orc.quantize_rows(x)
+    w, sw = orc.quantize_rows(wt)
+    wd = dev(w)
+    w8 = q4.prepack_weights(wd) if mainloop == 4 else None
+    ek = {"i32": q4.EPI_I32, "f16": q4.EPI_F16, "gelu": q4.EPI_GELU_Q4, "resln": q4.EPI_RESLN_Q4}[kind]
+    kw = dict(mainloop=mainloop, w_i8=w8)
+    okw = {}
+    if kind != "i32":
+        kw["bias"] = dev(b)
+        okw["bias"] = b
+    if kind == "resln":
+        res = synth.hidden(M, N, f"skr{M}_{N}")
+        gam, bet = synth.ln_params(N, f"skln{N}")
+        kw.update(residual=dev(res), gamma=dev(gam), beta=dev(bet), ln_eps=1e-12)
+        okw.update(residual=res, gamma=gam, beta=bet, ln_eps=1e-12)
+    if kind == "gelu":
+        kw["f16_tap"] = True
+    ws_bytes = q4.lib().q4_w4a4_linear_workspace(M, N, K, ek)
+    assert ws_bytes > 0
+    ws = torch.zeros(ws_bytes, dtype=torch.uint8, device="cuda")
+    outs = [q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), ek, workspace=ws, **kw) for _ in range(3)]
+    # the counters and the split-K partial sums are zero at rest again
+    pre = q4.lib().q4_w4a4_linear_workspace(M, N, K, q4.EPI_F16)
+    assert 0 < pre <= ws_bytes and not host(ws[:pre]).any()
+    if kind == "i32":
+        ref = orc.gemm_i32(a, w, M, N, K)
+        for o in outs:
+            assert np.array_equal(host(o["i32"]), ref)
+        return
+    ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, {"f16": orc.EPI_F16, "gelu": orc.EPI_GELU_Q4,
+                                                  "resln": orc.EPI_RESLN_Q4}[kind], **okw)
+    y = host(outs[0]["f16"])
+    assert_f16_close(y, ref["f16"], kind)
+    if kind == "f16":
+        for o in outs[1:]:
+            assert np.array_equal(host(o["f16"]), y)
+        return
+    c2, s2 = orc.quantize_rows(y)
+    for o in outs:
+        assert np.array_equal(host(o["codes"]), c2)
+        assert np.array_equal(host(o["scales"]), s2)

@@ -134,6 +134,12 @@ def test_workspace_sizes(L):
     # 16 resp. 4 n-blocks
     assert g >= 256 * 16 * 128 * 20 and r >= 256 * 4 * 128 * 20
     assert ws(1024, 4096, 1024, _lib.EPI_GELU_Q4) < g
+    # M <= 256: every kind carries the split-K region (tile counters + INT32 partials for
+    # N <= 8192 per m-block) at an offset that depends on M only
+    f = ws(128, 2304, 768, _lib.EPI_F16)
+    assert f >= 8192 * 128 * 4 and f == ws(128, 768, 3072, _lib.EPI_I32)
+    assert ws(128, 768, 3072, _lib.EPI_RESLN_Q4) > f and ws(256, 2304, 768, _lib.EPI_F16) > f
+    assert ws(257, 2304, 768, _lib.EPI_F16) == 0
     cfg = _lib.LayerCfg(1024, 16, 64, 4096, 1e-12, 0, 0)
     lw = L.q4_encoder_layer_workspace(C.byref(cfg), 256, 128)
     sw = L.q4_encoder_stack_workspace(C.byref(cfg), 256, 128)
