@@ -54,16 +54,19 @@ class OutputGather:
     tensor is the single-GPU output of the same global batch (shards are equal-sized here).
 
     Buffers are allocated once (graph- and replay-friendly); `__call__` is stream-ordered
-    and does not synchronize.  World size 1: the local tensor itself (no collective)."""
+    and does not synchronize.  Without a process group: the local tensor itself (no
+    collective); with one, the collective runs at any world size (size 1 included, so a
+    single-GPU box exercises the NCCL path)."""
 
     def __init__(self, B: int, S: int, h: int, mode: str = "cls", device=None, dtype=torch.float16):
         if mode not in ("cls", "full"):
             raise ValueError(f"gather mode {mode!r} (expected 'cls' or 'full')")
         self.B, self.S, self.h, self.mode = B, S, h, mode
-        self.world = dist.get_world_size() if (dist.is_available() and dist.is_initialized()) else 1
+        self.pg = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size() if self.pg else 1
         rows = B if mode == "cls" else B * S
         self.local = torch.empty(rows, h, dtype=dtype, device=device) if mode == "cls" else None
-        self.out = torch.empty(self.world * rows, h, dtype=dtype, device=device) if self.world > 1 else None
+        self.out = torch.empty(self.world * rows, h, dtype=dtype, device=device) if self.pg else None
 
     @property
     def bytes_per_rank(self) -> int:
@@ -78,7 +81,7 @@ class OutputGather:
             src = self.local
         else:
             src = hidden
-        if self.world == 1:
+        if not self.pg:
             return src
         dist.all_gather_into_tensor(self.out, src.contiguous())
         return self.out

@@ -11,7 +11,7 @@ rm -f gpurun_out/d_trace.bin gpurun_out/d_probe.jsonl
 for args in "128 768 768 3 4" "128 768 3072 3 4" "128 3072 768 2 4" "128 2304 768 1 4"; do
   Q4_LIB_PATH=$P Q4_TRACE=gpurun_out/d_trace.bin timeout -s KILL 60 python scripts/probe_gemm.py $args >> gpurun_out/d_probe.jsonl 2>&1
 done
-python scripts/trace_report.py gpurun_out/d_trace.bin > gpurun_out/d_trace.txt 2>&1
+python scripts/trace_report.py gpurun_out/d_trace.bin > gpurun_out/d_trace.txt 2>&1; rm -f gpurun_out/d_trace.bin
 for args in "32768 1024 1024 3 4" "32768 1024 4096 3 4" "32768 4096 1024 2 4"; do
   Q4_LIB_PATH=$P timeout -s KILL 60 python scripts/probe_gemm.py $args >> gpurun_out/d_probe.jsonl 2>&1
   Q4_LIB_PATH=$P Q4_R4=1 timeout -s KILL 60 python scripts/probe_gemm.py $args >> gpurun_out/d_probe.jsonl 2>&1
