@@ -86,6 +86,31 @@ if os.path.exists(f"{P}/layer_raw.csv"):
             rd = float(d[hh.index("dram__bytes_read.sum")]); wr = float(d[hh.index("dram__bytes_write.sum")])
             mult = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}[units[hh.index("dram__bytes_read.sum")]]
             traffic[f"large:{roles[j]}:M32768"] = (rd + wr) * mult
+# ---- latency config: BERT-base 12 layers, batch 1 (warm launch list, scripts/probe_latency.py)
+if os.path.exists(f"{G}/{R}_bs1_launches.csv"):
+    shutil.copy(f"{G}/{R}_bs1_launches.csv", f"{P}/bs1_launches.csv")
+if os.path.exists(f"{P}/bs1_launches.csv"):
+    rows = list(csv.reader(open(f"{P}/bs1_launches.csv")))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, vi, gi = h.index("Kernel Name"), h.index("Metric Value"), h.index("Grid Size")
+    ls = [(re.sub(r"\(.*", "", r[ki]).replace("void ", "").replace("q4::", ""), float(r[vi]), r[gi])
+          for r in rows[hi + 1:] if len(r) > vi and r[vi]]
+    last = ls[-61:]  # the last eager forward: quantize + 12 x 5 kernels
+    roles1 = ["qkv_gemm_f16", "attention_q4", "attn_out_gemm_resln_q4", "ffn1_gemm_gelu_q4", "ffn2_gemm_resln_q4"]
+    per1 = {r: [] for r in roles1}
+    grid1 = {}
+    for j, (n, t, g) in enumerate(last[1:]):
+        per1[roles1[j % 5]].append(t)
+        grid1[roles1[j % 5]] = g
+    tot1 = sum(t for _, t, _ in last)
+    out.append(f"\nLatency config (BERT-base, 12 layers, batch 1, seq 128): ncu launch list with "
+               f"`--cache-control none` (warm L2, serialised: no PDL overlap) of `scripts/probe_latency.py 12 1` "
+               f"(file `{P}/bs1_launches.csv`); {len(last)} launches, {tot1/1e3:.1f} us summed.\n")
+    out.append("| kernel | grid | median us |\n|---|---|---|")
+    out.append(f"| quantize_rows (layer-0 input) | {last[0][2]} | {last[0][1]/1e3:.2f} |")
+    for r in roles1:
+        out.append(f"| {r} | {grid1[r]} | {statistics.median(per1[r])/1e3:.2f} |")
 open(f"{P}/summary.md", "w").write("\n".join(out) + "\n")
 if traffic:
     json.dump(traffic, open(f"{P}/traffic.json", "w"), indent=1)
