@@ -618,9 +618,46 @@ def side_measurements(q4, synth, torch, np, dev, args):
         t = sorted(ev0[i].elapsed_time(ev1[i]) for i in range(100))
         out[name.replace("bs1_p50", "bs1_cold_l2_p50")] = t[50]
         del flush
+    # configs[0]: one W4A4 linear, M = 128 (batch 1 x seq 128), K = N = 768, fp16 out (and the
+    # fused residual + LayerNorm + requant epilogue of the same shape), prepacked weights; a CUDA
+    # graph of one launch replayed, p50 of 200 (the floor of one launch in a graph: 1 empty kernel)
+    Mq, Kq, Nq = 128, 768, 768
+    xq = torch.from_numpy(synth.hidden(Mq, Kq, "c1x")).to(dev)
+    aq, saq = q4.quantize_rows(xq)
+    wq, swq = q4.quantize_rows(torch.from_numpy(synth.weight(Nq, Kq, "c1w")).to(dev))
+    w8q = q4.prepack_weights(wq)
+    bq = torch.from_numpy(synth.bias(Nq, "c1b")).to(dev)
+    resq = torch.from_numpy(synth.hidden(Mq, Nq, "c1r")).to(dev)
+    gq = torch.ones(Nq, dtype=torch.float16, device=dev)
+    for kind, nm, kw in ((q4.EPI_F16, "config1_linear_m128_k768_n768_f16_p50_us", {}),
+                         (q4.EPI_RESLN_Q4, "config1_linear_m128_k768_n768_resln_q4_p50_us",
+                          dict(residual=resq, gamma=gq, beta=bq))):
+        wsq = torch.zeros(max(q4.lib().q4_w4a4_linear_workspace(Mq, Nq, Kq, kind), 1), dtype=torch.uint8, device=dev)
+        oq = q4.w4a4_linear(aq, saq, wq, swq, kind, bias=bq, w_i8=w8q, workspace=wsq, **kw)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s2 = torch.cuda.Stream()
+        s2.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s2):
+            q4.w4a4_linear(aq, saq, wq, swq, kind, bias=bq, w_i8=w8q, workspace=wsq, out=oq, **kw)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            q4.w4a4_linear(aq, saq, wq, swq, kind, bias=bq, w_i8=w8q, workspace=wsq, out=oq, **kw)
+        for _ in range(20):
+            g.replay()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(201)]
+        torch.cuda.synchronize()
+        evs[0].record(stream)
+        for i in range(200):
+            g.replay()
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        t = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(200))
+        out[nm] = t[100] * 1e3
     # Latency floor (SURVEY 8(d) configs[2]): a CUDA graph of as many empty PDL kernels as the
     # 12-layer bs-1 forward launches (1 + 12 x 5), same launch attributes, p50 of 200 replays
-    for nk, nm in ((61, "latency_floor_61_empty_kernels_ms"), (6, "latency_floor_6_empty_kernels_ms")):
+    for nk, nm in ((61, "latency_floor_61_empty_kernels_ms"), (6, "latency_floor_6_empty_kernels_ms"),
+                   (1, "latency_floor_1_empty_kernel_ms")):
         g = torch.cuda.CUDAGraph()
         s2 = torch.cuda.Stream()
         with torch.cuda.stream(s2):
