@@ -79,7 +79,7 @@ def w4a4_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None
                  out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")), w_i8=_ptr(w_i8),
                  out_zeros=_ptr(o.get("zeros")))
     ws_bytes = lib().q4_w4a4_linear_workspace(M, N, K, kind)
-    if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
+    if ws_bytes and workspace is None:  # a caller's workspace goes to the C ABI as given
         workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
     check(lib().q4_w4a4_linear(_ptr(a_codes), _ptr(a_scales), _ptr(w_codes), _ptr(w_scales),
                                M, N, K, C.byref(e), _ptr(workspace),
@@ -127,7 +127,7 @@ def w8a8_linear(a_codes, a_scales, w_codes, w_scales, kind=EPI_F16, *, bias=None
                  out_i32=_ptr(o.get("i32")), out_f16=_ptr(o.get("f16")),
                  out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")), w_i8=None)
     ws_bytes = lib().q4_w8a8_linear_workspace(M, N, K, kind)
-    if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
+    if ws_bytes and workspace is None:  # a caller's workspace goes to the C ABI as given
         workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
     check(lib().q4_w8a8_linear(_ptr(a_codes), _ptr(a_scales), _ptr(w_codes), _ptr(w_scales),
                                M, N, K, C.byref(e), _ptr(workspace),
@@ -159,7 +159,7 @@ def f16_linear(a, w, kind=EPI_F16, *, bias=None, residual=None, gamma=None, beta
                  out_i32=None, out_f16=_ptr(o.get("f16")),
                  out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")), w_i8=None)
     ws_bytes = lib().q4_f16_linear_workspace(M, N, K, kind)
-    if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
+    if ws_bytes and workspace is None:  # a caller's workspace goes to the C ABI as given
         workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
     check(lib().q4_f16_linear(_ptr(a), _ptr(w), M, N, K, C.byref(e), _ptr(workspace),
                               0 if workspace is None else workspace.numel(), _stream()))
@@ -210,7 +210,7 @@ def w4a4_asym_linear(a_codes, a_scales, a_zeros, w_codes, w_scales, w_sums, kind
                  out_f16=_ptr(o.get("f16")), out_codes=_ptr(o.get("codes")), out_scales=_ptr(o.get("scales")),
                  w_i8=_ptr(w_i8), out_zeros=_ptr(o.get("zeros")))
     ws_bytes = lib().q4_w4a4_linear_workspace(M, N, K, kind)
-    if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
+    if ws_bytes and workspace is None:  # a caller's workspace goes to the C ABI as given
         workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
     check(lib().q4_w4a4_asym_linear(_ptr(a_codes), _ptr(a_scales), _ptr(a_zeros), _ptr(w_codes), _ptr(w_scales),
                                     _ptr(w_sums), M, N, K, C.byref(e), _ptr(workspace),

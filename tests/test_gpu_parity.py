@@ -622,3 +622,28 @@ def test_split_k_small_m(q4, M, N, K, kind, mainloop):
     for o in outs:
         assert np.array_equal(host(o["codes"]), c2)
         assert np.array_equal(host(o["scales"]), s2)
+
+
+@pytest.mark.parametrize("kind", ["i32", "f16"])
+def test_split_k_without_workspace(q4, kind):
+    """F16 / I32 at M <= 256 take the split-K path only with the workspace the query asks for;
+    with a too-small workspace they run unsplit (no error) and give the same bits."""
+    M, N, K = 128, 768, 3072
+    x, wt, b = synth.hidden(M, K, "skn_x"), synth.weight(N, K, "skn_w"), synth.bias(N, "skn_b")
+    a, sa = orc.quantize_rows(x)
+    w, sw = orc.quantize_rows(wt)
+    wd = dev(w)
+    w8 = q4.prepack_weights(wd)
+    ek = q4.EPI_I32 if kind == "i32" else q4.EPI_F16
+    kw = {} if kind == "i32" else {"bias": dev(b)}
+    full = q4.lib().q4_w4a4_linear_workspace(M, N, K, ek)
+    assert full > 0
+    ws_full = torch.zeros(full, dtype=torch.uint8, device="cuda")
+    ws_tiny = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    o1 = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), ek, w_i8=w8, workspace=ws_full, **kw)
+    o2 = q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), ek, w_i8=w8, workspace=ws_tiny, **kw)
+    key = "i32" if kind == "i32" else "f16"
+    g1, g2 = host(o1[key]), host(o2[key])
+    assert np.array_equal(g1.view(np.uint8), g2.view(np.uint8))
+    if kind == "i32":
+        assert np.array_equal(g1, orc.gemm_i32(a, w, M, N, K))
