@@ -137,10 +137,16 @@ struct TcCfg {
   static constexpr int BM = 128, BK = 128;  // BK in int8 elements = 64 packed bytes
   // packed / unpacked smem stages; narrow tiles (the latency configs: few CTAs, each streaming
   // its weight rows from HBM) keep more k-blocks in flight
+  // ATM (the narrow small-M tiles with prepacked weights): the unpack warps write the int8
+  // activation tile straight into TMEM (tcgen05.st) and the MMA reads A from there (TS form), so
+  // A never touches shared memory after its packed TMA stage -- the small-M mainloop is
+  // shared-memory bound, and this removes half of its traffic (16 KB written + 16 KB read per
+  // k-block).  TMEM: the NBUF accumulators, then SU A stages of 32 columns (128 B of K per row).
+  static constexpr bool ATM = BI8 && !A8 && !PAIR && !R4 && !SPLIT && TN <= 64;
   static constexpr int SP = A8 ? 1 : BI8 ? (SPLIT ? 3 : TN <= 64 ? 5 : 4) : 3;
-  static constexpr int SU = PAIR ? 4 : BI8 ? (SPLIT ? 3 : TN <= 64 ? 5 : 3) : 2;
+  static constexpr int SU = PAIR ? 4 : ATM ? 4 : BI8 ? (SPLIT ? 3 : TN <= 64 ? 5 : 3) : 2;
   static constexpr int A_PK = A8 ? 0 : BM * 64, B_PK = BI8 ? 0 : TN * 64;
-  static constexpr int A_UN = BM * 128, B_UN = (PAIR ? TN / 2 : TN) * 128;
+  static constexpr int A_UN = ATM ? 0 : BM * 128, B_UN = (PAIR ? TN / 2 : TN) * 128;
   static constexpr int UN_STAGE = A_UN + B_UN, PK_STAGE = A_PK + B_PK;
   static constexpr int OFF_UN = 0;
   static constexpr int OFF_PK = SU * UN_STAGE;
@@ -152,8 +158,10 @@ struct TcCfg {
   static constexpr int OFF_BAR = OFF_SRED + (SPLIT ? 2 * 128 * TN * 4 : 0);
   static constexpr int SMEM = OFF_BAR + 512 + 1024;
   static constexpr int NBUF = R4 ? 4 : 2;
-  static constexpr int TMEM_COLS = NBUF * TN <= 64 ? 64 : NBUF * TN <= 128 ? 128 : NBUF * TN <= 256 ? 256 : 512;
-  static_assert(NBUF * TN <= 512, "TMEM");
+  static constexpr int ACOL = NBUF * TN;  // ATM: first A-stage column
+  static constexpr int TCOLS = NBUF * TN + (ATM ? SU * 32 : 0);
+  static constexpr int TMEM_COLS = TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
+  static_assert(TCOLS <= 512, "TMEM");
   static_assert(TN % 32 == 0 && TN >= 32 && TN <= 256, "tile N");
   static_assert(SMEM <= 227 * 1024, "smem");
 };
@@ -881,6 +889,13 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
               else if constexpr (H16)
                 umma_f16kk(dt, umma_smem_desc(ua + ks * 32, 1024, 2), umma_smem_desc(ub + ks * 32, 1024, 2), idesc,
                            kb != kb0 || ks != 0);
+              else if constexpr (C::ATM)  // A from TMEM: 32 k (8 columns) per MMA
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dt),
+                    "r"(tmem + C::ACOL + (uint32_t)su * 32 + ks * 8), "l"(umma_smem_desc(ub + ks * 32, 1024, 2)),
+                    "r"(idesc), "r"((uint32_t)(kb != kb0 || ks != 0))
+                    : "memory");
               else
                 umma_i8(dt, umma_smem_desc(ua + ks * 32, 1024, 2), umma_smem_desc(ub + ks * 32, 1024, 2), idesc,
                         kb != kb0 || ks != 0);
@@ -929,12 +944,33 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
         const unsigned long long u2 = utr ? gtimer() : 0;
         const uint8_t* pk = smem + C::OFF_PK + s * C::PK_STAGE;
         uint8_t* un = smem + C::OFF_UN + su * C::UN_STAGE;
-        if (!(p.dbg & 2)) {
+        if constexpr (C::ATM) {
+          // row r = this warp's TMEM lane quarter (WU is a multiple of 4); its 64 packed bytes
+          // sit in the SWIZZLE_64B TMA stage (16-byte chunk c at c ^ ((r >> 1) & 3): conflict-
+          // free) and become 32 TMEM columns in the MMA's K order: per chunk, 16 even-k bytes
+          // (lo nibbles, 16 q) then 16 odd-k bytes (hi nibbles) -- the prepacked weights' order
+          const int uw = warp - WU, r = 32 * uw + lane;
+          const uint8_t* prow = pk + r * 64;
+          const uint32_t swz = ((uint32_t)r >> 1) & 3u;
+          uint32_t v[32];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 w = *reinterpret_cast<const uint4*>(prow + ((c ^ swz) << 4));
+            v[8 * c + 0] = nib_lo16(w.x); v[8 * c + 1] = nib_lo16(w.y);
+            v[8 * c + 2] = nib_lo16(w.z); v[8 * c + 3] = nib_lo16(w.w);
+            v[8 * c + 4] = nib_hi16(w.x); v[8 * c + 5] = nib_hi16(w.y);
+            v[8 * c + 6] = nib_hi16(w.z); v[8 * c + 7] = nib_hi16(w.w);
+          }
+          tc_fence_after();  // the MMA that read this A stage has completed (empty_u)
+          tmem_st32(tmem + ((uint32_t)(32 * uw) << 16) + C::ACOL + su * 32, v);
+          tmem_wait_st();
+          tc_fence_before();
+        } else if (!(p.dbg & 2)) {
           unpack_rows<C::BM>(pk, un, t);
           if constexpr (!BI8) unpack_rows<TN>(pk + C::A_PK, un + C::A_UN, t);
         }
         const unsigned long long u3 = utr ? gtimer() : 0;
-        fence_proxy_async_smem();
+        if constexpr (!C::ATM) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
           if constexpr (PAIR)
@@ -1489,7 +1525,7 @@ EncodeTiledFn get_encode() {
 
 // 2-D uint8 tensor map over a row-major [rows, row_bytes] buffer, box [box_rows, box_bytes].
 bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t row_bytes, uint32_t box_rows,
-               uint32_t box_bytes, bool swizzle128 = false) {
+               uint32_t box_bytes, bool swizzle128 = false, bool swizzle64 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {row_bytes, rows};
@@ -1497,7 +1533,8 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t row_byt
   cuuint32_t box[2] = {box_bytes, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : swizzle64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -1532,7 +1569,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   const bool okb = BI8 ? make_tmap(&tb, g.w_i8, (uint64_t)g.N, (uint64_t)g.K, PAIR ? TN / 2 : TN, 128, true)
                        : make_tmap(&tb, g.w_codes, (uint64_t)g.N, kb, TN, 64);
   const bool oka = A8 ? make_tmap(&ta, g.a_i8, (uint64_t)g.M, (uint64_t)g.K, 128, 128, true)
-                     : make_tmap(&ta, g.a_codes, (uint64_t)g.M, kb, 128, 64);
+                     : make_tmap(&ta, g.a_codes, (uint64_t)g.M, kb, 128, 64, false, C::ATM);
   if (!oka || !okb) {
     *why = "cuTensorMapEncodeTiled failed (driver entry point or alignment)";
     return cudaErrorInvalidValue;
