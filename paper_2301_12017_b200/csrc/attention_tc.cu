@@ -437,12 +437,25 @@ cluster_tail:
         asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(ra) : "memory");
         return x;
       };
-      for (int c = 0; c < G; ++c) {
-        a = fmaxf(a, fmaxf(rd(red + r, c), rd(red + 128 + r, c)));
-        if (asym) {
+      if (asym) {
+        for (int c = 0; c < G; ++c) {
+          a = fmaxf(a, fmaxf(rd(red + r, c), rd(red + 128 + r, c)));
           mn = fminf(mn, fminf(rd(red + 256 + r, c), rd(red + 384 + r, c)));
           mx = fmaxf(mx, fmaxf(rd(red + 512 + r, c), rd(red + 640 + r, c)));
         }
+      } else {
+        // all 2 G distributed-shared-memory loads in flight before the first use (one round
+        // trip instead of 2 G serialised ones; G <= 16)
+        float pv[32];
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c < G) {
+            pv[2 * c] = rd(red + r, c);
+            pv[2 * c + 1] = rd(red + 128 + r, c);
+          }
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c < G) a = fmaxf(a, fmaxf(pv[2 * c], pv[2 * c + 1]));
       }
       if (asym) {
         zmn[r] = mn;
@@ -461,10 +474,29 @@ cluster_tail:
     __syncthreads();
     // this CTA's columns [64 j0, 64 (j0 + hpc)): cpr 16-byte chunks (8 values) per row
     const int cpr = hpc * 8;
-    for (int idx = threadIdx.x; idx < S * cpr; idx += AT_THREADS) {
+    // the ctx chunks this thread codes: the first four loads in flight together (the whole job
+    // at one head per CTA: S * 8 chunks over 320 threads), then the rest one by one
+    constexpr int PF = 4;
+    uint4 xp[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int idx = threadIdx.x + u * AT_THREADS;
+      if (idx < S * cpr) {
+        const int rw = idx / cpr, c = idx - rw * cpr;
+        xp[u] = __ldcg(reinterpret_cast<const uint4*>(ctx_f16 + (size_t)(row0 + rw) * h + j0 * 64 + c * 8));
+      }
+    }
+    for (int idx = threadIdx.x, u = 0; idx < S * cpr; idx += AT_THREADS, ++u) {
       const int rw = idx / cpr, c = idx - rw * cpr;
       const float a = amx[rw];
-      const uint4 x = __ldcg(reinterpret_cast<const uint4*>(ctx_f16 + (size_t)(row0 + rw) * h + j0 * 64 + c * 8));
+      uint4 x;
+      if (u < PF) {
+#pragma unroll
+        for (int k = 0; k < PF; ++k)
+          if (k == u) x = xp[k];
+      } else {
+        x = __ldcg(reinterpret_cast<const uint4*>(ctx_f16 + (size_t)(row0 + rw) * h + j0 * 64 + c * 8));
+      }
       const uint32_t hh[4] = {x.x, x.y, x.z, x.w};
       if (asym)
         reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] = requant8_asym(hh, zmn[rw], zmx[rw]);
