@@ -88,6 +88,17 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
   const int b = blockIdx.x / G, g = blockIdx.x % G;
   const int hpc = heads / G, j0 = g * hpc;
   const int row0 = b * S;  // first token of this sequence
+  // profiling only (Q4_TRACE): thread 0's kernel-level stamps in head slot 15 (unused at one
+  // head per CTA): [0] kernel entry, [1] after the prologue, [2] tail: first cluster barrier
+  // passed, [3] row scales ready, [4] codes written, [5] exit
+  auto kstamp = [&](int k) {
+    if (trace && threadIdx.x == 0 && blockIdx.x < 512) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      trace[(size_t)blockIdx.x * 256 + 15 * 16 + k] = t;
+    }
+  };
+  kstamp(0);
 
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tq);
@@ -103,6 +114,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  kstamp(1);
   pdl_launch_dependents();
   pdl_wait();  // everything below may read the previous kernel's outputs
   // TMEM columns: S / P at [0, 128), O at [128, 192) (single-buffered; two CTAs per SM overlap)
@@ -278,6 +290,14 @@ __global__ void __launch_bounds__(AT_THREADS, 2)
         }
         hw4[u] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
       }
+      if (G > 1 && hpc == 1) {
+        // one head per CTA: the ctx tile [128 x 64] fp16 also stays in shared memory (the Q/K/V
+        // stage is idle once O is complete) for the cluster tail's codes; 16-byte chunk c of row
+        // r at c ^ (r & 7)
+        uint8_t* ct = smem + r * 128;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(ct + (((hf * 4 + u) ^ (r & 7)) << 4)) = hw4[u];
+      }
       stamp(j, 9);
       // coalesced store through a 16-row x 64-byte slab, two passes of 16 rows per warp
 #pragma unroll
@@ -424,7 +444,22 @@ cluster_tail:
     float* red = reinterpret_cast<float*>(smem + OFF_RED);        // [2][128] this CTA's partials
     float* amx = reinterpret_cast<float*>(smem + OFF_SLAB);       // [128] combined max-abs
     float* rr7 = amx + 128;                                       // [128] 7 / amax
+    // One head per CTA, symmetric / int8 codes: PUSH -- each CTA stores its rows' max-abs into
+    // slot g of every CTA's gather buffer [G][128] before the cluster barrier (in the second
+    // Q/K/V stage, which one head per CTA never loads: a slower peer may still be in its head),
+    // so after it every read is local and no CTA touches another's shared memory any more (no
+    // second barrier).  Otherwise PULL: remote reads after the barrier, a second barrier
+    // before exit.
+    const bool push = hpc == 1 && !asym;
+    float* gbuf = reinterpret_cast<float*>(smem + STAGE);
+    if (push && threadIdx.x < 128) {
+      const int r = threadIdx.x;
+      const float al = fmaxf(red[r], red[128 + r]);
+      const uint32_t la = smem_u32(gbuf + g * 128 + r);
+      for (int c = 0; c < G; ++c) st_cluster_f32(mapa(la, (uint32_t)c), al);
+    }
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    kstamp(2);
     float* zmn = rr7 + 128;                                       // [128] asym: min
     float* zmx = zmn + 128;                                       // [128] asym: max
     if (threadIdx.x < 128) {
@@ -437,7 +472,9 @@ cluster_tail:
         asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(ra) : "memory");
         return x;
       };
-      if (asym) {
+      if (push) {
+        for (int c = 0; c < G; ++c) a = fmaxf(a, gbuf[c * 128 + r]);
+      } else if (asym) {
         for (int c = 0; c < G; ++c) {
           a = fmaxf(a, fmaxf(rd(red + r, c), rd(red + 128 + r, c)));
           mn = fminf(mn, fminf(rd(red + 256 + r, c), rd(red + 384 + r, c)));
@@ -472,16 +509,21 @@ cluster_tail:
       if (g == 0 && r < S && !asym) ctx_scales[row0 + r] = a > 0.f ? __fdiv_rn(a, qm) : 1.0f;
     }
     __syncthreads();
+    // pull: every remote read of this CTA is done -- arrive now (release), wait only before
+    // exit, so the other CTAs' red[] lifetime costs nothing on this CTA's path
+    if (!push) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    kstamp(3);
     // this CTA's columns [64 j0, 64 (j0 + hpc)): cpr 16-byte chunks (8 values) per row
     const int cpr = hpc * 8;
     // the ctx chunks this thread codes: the first four loads in flight together (the whole job
     // at one head per CTA: S * 8 chunks over 320 threads), then the rest one by one
     constexpr int PF = 4;
     uint4 xp[PF];
+    const bool ctile = hpc == 1;  // the epilogue kept this CTA's ctx tile in shared memory
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
       const int idx = threadIdx.x + u * AT_THREADS;
-      if (idx < S * cpr) {
+      if (!ctile && idx < S * cpr) {
         const int rw = idx / cpr, c = idx - rw * cpr;
         xp[u] = __ldcg(reinterpret_cast<const uint4*>(ctx_f16 + (size_t)(row0 + rw) * h + j0 * 64 + c * 8));
       }
@@ -490,7 +532,9 @@ cluster_tail:
       const int rw = idx / cpr, c = idx - rw * cpr;
       const float a = amx[rw];
       uint4 x;
-      if (u < PF) {
+      if (ctile) {
+        x = *reinterpret_cast<const uint4*>(smem + rw * 128 + ((c ^ (rw & 7)) << 4));
+      } else if (u < PF) {
 #pragma unroll
         for (int k = 0; k < PF; ++k)
           if (k == u) x = xp[k];
@@ -502,14 +546,23 @@ cluster_tail:
         reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] = requant8_asym(hh, zmn[rw], zmx[rw]);
       else if (i8)
         reinterpret_cast<uint2*>(ctx_codes + (size_t)(row0 + rw) * h + j0 * 64)[c] = requant8_i8(hh, a, rr7[rw], 0.f);
-      else
-        reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] =
-            a > 0.f ? requant8(hh, a, rr7[rw], 0.f) : 0u;
+      else {
+        // batched fast requant; near a half-integer the exact per-element tie-break (R2, R3)
+        uint32_t wq = 0u;
+        if (a > 0.f) {
+          float dm = 0.f;
+          wq = requant8_nofix(hh, rr7[rw], dm);
+          if (dm > 0.499998f) wq = requant8(hh, a, rr7[rw], 0.f);
+        }
+        reinterpret_cast<uint32_t*>(ctx_codes + (size_t)(row0 + rw) * (h / 2) + j0 * 32)[c] = wq;
+      }
     }
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    kstamp(4);
+    if (!push) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
+  kstamp(5);
   if (warp == 9) tmem_dealloc(tmem, 256);
 }
 
