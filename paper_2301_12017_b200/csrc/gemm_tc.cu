@@ -53,6 +53,12 @@ enum { EPI_I32 = 0, EPI_F16 = 1, EPI_GELU_Q4 = 2, EPI_RESLN_Q4 = 3 };
 constexpr int kKsplitMaxRows = 256, kKsplitMaxN = 8192, kKsplitMinKb = 2, kKsplitMinLoop = 16;
 constexpr size_t kKsplitCntBytes = 1024;  // per m-block: N / TN <= 256 tile counters
 int tc_ksplit(int M, int N, int K, int TN);
+// CX (single-m-block row GEMMs as one cluster, DSMEM exchange): on; Q4_CX=0 in the profiling
+// build disables it (A/B only).
+inline bool tc_cx_enabled() {
+  static const int env = [] { const char* e = prof_env("Q4_CX"); return e ? atoi(e) : 1; }();
+  return env != 0;
+}
 size_t tc_ksplit_bytes(int M);
 size_t tc_counter_bytes(int M);
 
@@ -89,6 +95,10 @@ struct TcParams {
   // (kcnt) reads the total back into its TMEM, zeroes kpart / kcnt and runs the unchanged
   // epilogue.  1 = off.
   int ksplit;
+  // cluster exchange (CX: one m-block, ntn <= 16 n-tiles, TN <= 64 -- the batch-1 row GEMMs):
+  // the ntn CTAs run as one thread-block cluster and push their row partials into every peer's
+  // shared memory (st.async, completing on the receiver's mbarrier) instead of the L2 rendezvous
+  int cx;
   int32_t* kpart;     // [mblocks][ntn][TN][128] INT32 partial sums (zero at rest)
   unsigned* kcnt;     // [mblocks][ntn] arrivals (zero at rest)
   int dbg;            // profiling only (env Q4_DEBUG_SKIP): 1 skip TMA, 2 skip unpack, 4 skip MMA, 8 skip epilogue math
@@ -155,7 +165,8 @@ struct TcCfg {
   static constexpr int OFF_PRM = OFF_STG + NSLAB * 4096;  // [R4 ? 4 groups : 1][5][TN] fp32 column params
   static constexpr int OFF_ROW = OFF_PRM + (R4 ? 4 : 1) * 5 * TN * 4;  // [2 groups][2 sides][128] float4 row partials
   static constexpr int OFF_SRED = OFF_ROW + (R4 ? 0 : 2 * 2 * 128 * 16);  // SPLIT: [2][128][TN] int32 partials
-  static constexpr int OFF_BAR = OFF_SRED + (SPLIT ? 2 * 128 * TN * 4 : 0);
+  static constexpr int OFF_CX = OFF_SRED + (SPLIT ? 2 * 128 * TN * 4 : 0);  // CX: [2 exchanges][16][128] float2
+  static constexpr int OFF_BAR = OFF_CX + (TN <= 64 && !SPLIT ? 2 * 16 * 128 * 8 : 0);
   static constexpr int SMEM = OFF_BAR + 512 + 1024;
   static constexpr int NBUF = R4 ? 4 : 2;
   static constexpr int ACOL = NBUF * TN;  // ATM: first A-stage column
@@ -455,6 +466,32 @@ Q4_DEV void exchange_depart(unsigned* cnt, size_t dep, int ntn, bool leader, int
     }
   }
 }
+// CX (one m-block as one cluster): push a row partial into slot `dst` of every CTA of the cluster
+// (rank c = n-block c), completing on that CTA's mbarrier `bar` (complete_tx, 8 or 4 bytes).
+Q4_DEV void cx_push2(const void* dst, float x, float y, const uint64_t* bar, int ntn) {
+  const uint32_t la = smem_u32(dst), lb = smem_u32(bar);
+  for (int c = 0; c < ntn; ++c)
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(
+                     mapa(la, (uint32_t)c)),
+                 "f"(x), "f"(y), "r"(mapa(lb, (uint32_t)c))
+                 : "memory");
+}
+Q4_DEV void cx_push1(const void* dst, float x, const uint64_t* bar, int ntn) {
+  const uint32_t la = smem_u32(dst), lb = smem_u32(bar);
+  for (int c = 0; c < ntn; ++c)
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                     mapa(la, (uint32_t)c)),
+                 "r"(__float_as_uint(x)), "r"(mapa(lb, (uint32_t)c))
+                 : "memory");
+}
+// CX rendezvous: the leader announces the bytes this CTA receives; one warp of the group waits for
+// them; the bar.sync hands the local partials to the whole group
+Q4_DEV void cx_wait(uint64_t* bar, uint32_t bytes, bool leader, bool poll_warp, int bar_id, int nthreads) {
+  if (leader) mbar_arrive_expect_tx(bar, bytes);
+  if (poll_warp) mbar_wait(bar, 0);
+  named_bar(bar_id, nthreads);
+}
+
 // Partial-slab variant for warps sharing one slab: rows [r0, r0 + nrows).
 Q4_DEV void slab_store16(const uint8_t* stg, uint8_t* gbase, int row0, int r0, int nrows, int M, size_t ldb,
                          size_t colb, int bytes_per_row, int lane) {
@@ -702,11 +739,14 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
   uint64_t* tempty = tfull + NBUF;     // [NBUF]
   uint64_t* redfull = tempty + NBUF;   // SPLIT [2]: rank 0 -- rank 1's partial of buffer b has landed
   uint64_t* redempty = redfull + 2;    // SPLIT [2]: rank 1 -- rank 0 has consumed it
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(redempty + 2);
+  uint64_t* cxbar = redempty + 2;      // CX [2]: the ntn partials of exchange 1 / 2 have landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cxbar + 2);
   uint32_t* kflag = tmem_slot + 1;    // [NBUF] split-K: this CTA's slice arrived last
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (p.K + C::BK - 1) / C::BK;
+  // CX (cluster exchange) exists only in the narrow 1-CTA instantiations; elsewhere it folds away
+  const bool cx = (TN <= 64 && !PAIR && !SPLIT) ? p.cx != 0 : false;
   // Warp roles.  The issue arbiter favours higher warp ids, so the mainloop's critical
   // path (unpack, TMA producer, MMA issuer) sits above the epilogue warps.
   constexpr int NE = NBUF * E::EPW;          // epilogue warps 0 .. NE-1
@@ -723,6 +763,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
     for (int i = 0; i < C::SU; ++i) { mbar_init(&full_u[i], A8 ? 1 : PAIR ? 9 : BI8 ? 5 : 4); mbar_init(&empty_u[i], 1); }
     for (int i = 0; i < NBUF; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], (PAIR ? 2 : 1) * E::EPW); }
     for (int i = 0; i < 2; ++i) { mbar_init(&redfull[i], E::EPW); mbar_init(&redempty[i], E::EPW); }
+    for (int i = 0; i < 2; ++i) mbar_init(&cxbar[i], 1);
     fence_mbar_init();
   }
   if constexpr (PAIR) {
@@ -738,7 +779,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
   } else {
     if (warp == WM) tmem_alloc(tmem_slot, C::TMEM_COLS);
     tc_fence_before();
-    if constexpr (SPLIT) cluster_sync(); else __syncthreads();  // SPLIT: remote arrives need both CTAs' barriers
+    if (SPLIT || cx) cluster_sync(); else __syncthreads();  // SPLIT / CX: remote arrives need every CTA's barriers
     tc_fence_after();
   }
   const uint32_t crank = (PAIR || SPLIT) ? cluster_ctarank() : 0u;
@@ -1281,17 +1322,24 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
               cm = a0.x + 0.5f * d;
               cm2 = a0.y + a1.y + d * d * (nh * 0.5f);
             }
-            if (sub == 0) p.xstat[((size_t)mb * ntn + nb) * 128 + r] = make_float2(cm, cm2);
-            exchange_sync(p.xcnt + mb, ntn, gbar, GT, leader, p.dbg);
+            float2* gx1 = reinterpret_cast<float2*>(smem + C::OFF_CX);  // CX: [16][128]
+            if (cx) {
+              if (sub == 0) cx_push2(gx1 + nb * 128 + r, cm, cm2, &cxbar[0], ntn);
+              cx_wait(&cxbar[0], (uint32_t)ntn * 128 * 8, leader, ew % EPW == 0, gbar, GT);
+            } else {
+              if (sub == 0) p.xstat[((size_t)mb * ntn + nb) * 128 + r] = make_float2(cm, cm2);
+              exchange_sync(p.xcnt + mb, ntn, gbar, GT, leader, p.dbg);
+            }
             stamp(3);
             // every partial covers TN columns: mean = average of the means, M2 = sum of the M2s
             // + TN * sum of squared deviations of the means.  One pass, deviations taken
             // from partial 0's mean (the partial means are close, so no cancellation).
             const float2* xs = p.xstat + ((size_t)mb * ntn) * 128 + r;
-            const float2 o0 = __ldcg(xs);
+            const float2* xl = gx1 + r;
+            const float2 o0 = cx ? xl[0] : __ldcg(xs);
             float dsum = 0.f, dsq = 0.f, m2 = o0.y;
             for (int kk = 1; kk < ntn; ++kk) {
-              const float2 o = __ldcg(xs + (size_t)kk * 128);
+              const float2 o = cx ? xl[kk * 128] : __ldcg(xs + (size_t)kk * 128);
               const float dd = o.x - o0.x;
               dsum += dd;
               dsq = fmaf(dd, dd, dsq);
@@ -1389,10 +1437,16 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
             mn = fminf(rowp[r].z, rowp[128 + r].z);
             mx = fmaxf(rowp[r].w, rowp[128 + r].w);
           }
-          if (sub == 0) p.xmm[((size_t)mb * ntn + nb) * 128 + r] = make_float2(mn, mx);
-          exchange_sync(p.xcnt + p.mblocks + mb, ntn, gbar, GT, leader, p.dbg);
+          float2* gx2 = reinterpret_cast<float2*>(smem + C::OFF_CX + 16 * 128 * 8);  // CX: [16][128]
+          if (cx) {
+            if (sub == 0) cx_push2(gx2 + nb * 128 + r, mn, mx, &cxbar[1], ntn);
+            cx_wait(&cxbar[1], (uint32_t)ntn * 128 * 8, leader, ew % EPW == 0, gbar, GT);
+          } else {
+            if (sub == 0) p.xmm[((size_t)mb * ntn + nb) * 128 + r] = make_float2(mn, mx);
+            exchange_sync(p.xcnt + p.mblocks + mb, ntn, gbar, GT, leader, p.dbg);
+          }
           for (int kk = 0; kk < ntn; ++kk) {
-            const float2 o = __ldcg(&p.xmm[((size_t)mb * ntn + kk) * 128 + r]);
+            const float2 o = cx ? gx2[kk * 128 + r] : __ldcg(&p.xmm[((size_t)mb * ntn + kk) * 128 + r]);
             mn = fminf(mn, o.x);
             mx = fmaxf(mx, o.y);
           }
@@ -1424,10 +1478,17 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
           named_bar(gbar, GT);
           amax = fmaxf(rowp[r].z, rowp[128 + r].z);
         }
-        if (sub == 0) p.xamax[((size_t)mb * ntn + nb) * 128 + r] = amax;
-        exchange_sync(p.xcnt + p.mblocks + mb, ntn, gbar, GT, leader, p.dbg);
+        float* gxa = reinterpret_cast<float*>(smem + C::OFF_CX + 16 * 128 * 8);  // CX: [16][128]
+        if (cx) {
+          if (sub == 0) cx_push1(gxa + nb * 128 + r, amax, &cxbar[1], ntn);
+          cx_wait(&cxbar[1], (uint32_t)ntn * 128 * 4, leader, ew % EPW == 0, gbar, GT);
+          for (int kk = 0; kk < ntn; ++kk) amax = fmaxf(amax, gxa[kk * 128 + r]);
+        } else {
+          if (sub == 0) p.xamax[((size_t)mb * ntn + nb) * 128 + r] = amax;
+          exchange_sync(p.xcnt + p.mblocks + mb, ntn, gbar, GT, leader, p.dbg);
+          for (int kk = 0; kk < ntn; ++kk) amax = fmaxf(amax, __ldcg(&p.xamax[((size_t)mb * ntn + kk) * 128 + r]));
+        }
         stamp(5);
-        for (int kk = 0; kk < ntn; ++kk) amax = fmaxf(amax, __ldcg(&p.xamax[((size_t)mb * ntn + kk) * 128 + r]));
         // pass B: codes (R1-R3), packed, staged, coalesced stores
         if constexpr (A8 && !H16) {
           // W8A8: int8 codes (O-11), 64 bytes per 64-column slab row
@@ -1470,7 +1531,7 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
         }
         }
       }
-      if constexpr (E::ROW) {
+      if (E::ROW && !cx) {
         // leave this m-block's rendezvous (off the critical path: after every partial read)
         if constexpr (KIND == EPI_RESLN_Q4) exchange_depart(p.xcnt + mb, 2 * (size_t)p.mblocks, p.ntn, leader, p.dbg);
         exchange_depart(p.xcnt + p.mblocks + mb, 2 * (size_t)p.mblocks, p.ntn, leader, p.dbg);
@@ -1562,6 +1623,10 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
+    if constexpr (!PAIR && !SPLIT && TN <= 64) {  // CX clusters of up to 16 CTAs (> the portable 8)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
     configured = true;
   }
   CUtensorMap ta, tb;
@@ -1583,7 +1648,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
   p.pair = PAIR ? 1 : 0;
   p.lin = R4 ? 1 : 0;
   p.split = SPLIT ? 1 : 0;
-  p.ksplit = 1; p.kpart = nullptr; p.kcnt = nullptr;
+  p.ksplit = 1; p.kpart = nullptr; p.kcnt = nullptr; p.cx = 0;
   p.bias = g.bias; p.residual = g.residual; p.gamma = g.gamma; p.beta = g.beta;
   p.ln_eps = g.ln_eps; p.clip = g.clip;
   p.out_i32 = g.out_i32; p.out_f16 = g.out_f16; p.out_codes = g.out_codes; p.out_scales = g.out_scales;
@@ -1662,10 +1727,38 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
       return cudaErrorInvalidValue;
     }
   }
+  // CX: a single m-block whose ntn <= 16 CTAs can form one cluster exchanges its row partials
+  // through distributed shared memory (the batch-1 row GEMMs without split-K)
+  if constexpr ((KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4) && !PAIR && !SPLIT && TN <= 64) {
+    if (p.mblocks == 1 && p.ntn <= 16 && p.ksplit == 1 && grid == p.ntn && tc_cx_enabled()) p.cx = 1;
+  }
   note_launch();
   {
     cudaError_t le;
-    if constexpr (PAIR || SPLIT) {
+    if (p.cx) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(THREADS);
+      cfg.dynamicSmemBytes = C::SMEM;
+      cfg.stream = s;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)grid;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      le = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+      if (le != cudaSuccess) {  // a cluster the GPU cannot place: the L2 rendezvous instead
+        (void)cudaGetLastError();
+        p.cx = 0;
+      }
+    }
+    if (p.cx) {
+      le = cudaSuccess;
+    } else if constexpr (PAIR || SPLIT) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
       cfg.blockDim = dim3(THREADS);
