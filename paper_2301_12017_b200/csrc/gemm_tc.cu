@@ -52,7 +52,7 @@ enum { EPI_I32 = 0, EPI_F16 = 1, EPI_GELU_Q4 = 2, EPI_RESLN_Q4 = 3 };
 // 0.702 with slices of 2): >= kKsplitMinLoop k-blocks of 128, slices of >= kKsplitMinKb
 constexpr int kKsplitMaxRows = 256, kKsplitMaxN = 8192, kKsplitMinKb = 2, kKsplitMinLoop = 16;
 constexpr size_t kKsplitCntBytes = 1024;  // per m-block: N / TN <= 256 tile counters
-int tc_ksplit(int M, int N, int K, int TN);
+int tc_ksplit(int M, int N, int K, int TN, bool row = false);
 // CX (single-m-block row GEMMs as one cluster, DSMEM exchange): on; Q4_CX=0 in the profiling
 // build disables it (A/B only).
 inline bool tc_cx_enabled() {
@@ -1696,7 +1696,7 @@ cudaError_t run_tc(const GemmArgs& g, void* ws, size_t ws_bytes, cudaStream_t s,
     if (p.ntn > units) { *why = "N/TN exceeds the number of SMs"; return cudaErrorNotSupported; }
     if constexpr (!PAIR && !SPLIT && !H16 && TN <= 64) {
       // split-K over global reductions (small M): needs the workspace's zero-at-rest prefix
-      const int ks = tc_ksplit(g.M, g.N, g.K, TN);
+      const int ks = tc_ksplit(g.M, g.N, g.K, TN, KIND == EPI_GELU_Q4 || KIND == EPI_RESLN_Q4);
       const size_t cb = tc_counter_bytes(g.M);
       if (ks > 1 && ws && ws_bytes >= cb + tc_ksplit_bytes(g.M)) {
         uint8_t* w = reinterpret_cast<uint8_t*>(ws) + cb;
@@ -1906,13 +1906,17 @@ size_t tc_counter_bytes(int M) {
 
 // Split-K over global reductions for the latency configs (M <= kKsplitMaxRows): slices of at
 // least kKsplitMinKb k-blocks, as many as fit one CTA per SM next to the other tiles.
-int tc_ksplit(int M, int N, int K, int TN) {
+int tc_ksplit(int M, int N, int K, int TN, bool row) {
   // profiling only: Q4_KSPLIT forces the split (0 = off), Q4_KSPLIT_MINKB the k-loop threshold
   static const int env = prof_env("Q4_KSPLIT") && *prof_env("Q4_KSPLIT") ? atoi(prof_env("Q4_KSPLIT")) : -1;
   static const int minkb = prof_env("Q4_KSPLIT_MINKB") ? atoi(prof_env("Q4_KSPLIT_MINKB")) : kKsplitMinLoop;
   if (M <= 0 || M > kKsplitMaxRows || N > kKsplitMaxN || TN > 64 || env == 0) return 1;
   const int KB = (K + 127) / 128, tiles = ((M + 127) / 128) * (N / TN);
   if (KB < minkb) return 1;
+  // a row epilogue that runs as one cluster (CX) is faster unsplit inside the layer (BERT-base
+  // batch 1, 12 layers eager: FFN2 split 12 ways 0.608 ms, unsplit with CX 0.578 ms -- the 12
+  // CTAs start under PDL while the previous kernel runs, 144 cannot)
+  if (row && M <= 128 && N / TN <= 16 && tc_cx_enabled() && env < 0) return 1;
   int s = num_sms() / tiles;
   if (s > KB / kKsplitMinKb) s = KB / kKsplitMinKb;
   if (env > 1 && env <= KB && env * tiles <= num_sms()) s = env;

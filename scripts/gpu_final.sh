@@ -9,3 +9,6 @@ echo "bench rc=$?" >> gpurun_out/f_tests.log
 timeout -s KILL 200 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f_smoke.log 2>&1
 echo "smoke rc=$?" >> gpurun_out/f_tests.log
 echo done
+timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv \
+  --log-file gpurun_out/f_bs1_launches.csv python scripts/probe_latency.py 12 1 > gpurun_out/f_ncu.log 2>&1
+echo done2
