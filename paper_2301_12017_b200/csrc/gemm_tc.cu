@@ -1486,6 +1486,8 @@ __global__ void __launch_bounds__(EpiCfg<KIND, PAIR && (KIND == 2 || KIND == 3)>
         } else {
           if (sub == 0) p.xamax[((size_t)mb * ntn + nb) * 128 + r] = amax;
           exchange_sync(p.xcnt + p.mblocks + mb, ntn, gbar, GT, leader, p.dbg);
+          // narrow tiles (batch 1: up to 48 partials) keep every load in flight at once
+#pragma unroll(TN <= 64 ? 48 : 16)
           for (int kk = 0; kk < ntn; ++kk) amax = fmaxf(amax, __ldcg(&p.xamax[((size_t)mb * ntn + kk) * 128 + r]));
         }
         stamp(5);
