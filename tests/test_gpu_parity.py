@@ -647,3 +647,56 @@ def test_split_k_without_workspace(q4, kind):
     assert np.array_equal(g1.view(np.uint8), g2.view(np.uint8))
     if kind == "i32":
         assert np.array_equal(g1, orc.gemm_i32(a, w, M, N, K))
+
+
+# ------------------------------------------------------------------ cluster exchange (single m-block)
+@pytest.mark.parametrize("M,N,K,kind", [(100, 1024, 1024, "resln"), (128, 1024, 3072, "resln"),
+                                         (128, 1024, 1024, "gelu"), (64, 128, 512, "gelu"), (1, 1024, 768, "resln")])
+def test_cluster_exchange_single_mblock(q4, M, N, K, kind):
+    """M <= 128 with N / 64 <= 16: the row GEMM runs as one thread-block cluster (up to 16 CTAs,
+    non-portable) and exchanges its row partials through distributed shared memory (st.async +
+    mbarrier complete_tx); K >= 2048 is then not split.  Oracle parity, and three launches on one
+    workspace give the same bits (fresh mbarrier phases per launch)."""
+    x, wt, b = synth.hidden(M, K, f"cx{M}_{K}"), synth.weight(N, K, f"cxw{N}_{K}"), synth.bias(N, f"cxb{N}")
+    a, sa = orc.quantize_rows(x)
+    w, sw = orc.quantize_rows(wt)
+    wd = dev(w)
+    w8 = q4.prepack_weights(wd)
+    kw, okw = dict(bias=dev(b), w_i8=w8), dict(bias=b)
+    if kind == "resln":
+        res = synth.hidden(M, N, f"cxr{M}_{N}")
+        gam, bet = synth.ln_params(N, f"cxln{N}")
+        kw.update(residual=dev(res), gamma=dev(gam), beta=dev(bet), ln_eps=1e-12)
+        okw.update(residual=res, gamma=gam, beta=bet, ln_eps=1e-12)
+        ek, ok = q4.EPI_RESLN_Q4, orc.EPI_RESLN_Q4
+    else:
+        kw["f16_tap"] = True
+        ek, ok = q4.EPI_GELU_Q4, orc.EPI_GELU_Q4
+    ws = torch.zeros(q4.lib().q4_w4a4_linear_workspace(M, N, K, ek), dtype=torch.uint8, device="cuda")
+    outs = [q4.w4a4_linear(dev(a), dev(sa), wd, dev(sw), ek, workspace=ws, **kw) for _ in range(3)]
+    ref = orc.w4a4_linear(a, sa, w, sw, M, N, K, ok, **okw)
+    y = host(outs[0]["f16"])
+    assert_f16_close(y, ref["f16"], kind)
+    c2, s2 = orc.quantize_rows(y)
+    for o in outs:
+        assert np.array_equal(host(o["f16"]).view(np.uint16), y.view(np.uint16))
+        assert np.array_equal(host(o["codes"]), c2)
+        assert np.array_equal(host(o["scales"]), s2)
+
+
+def test_cluster_exchange_w8a8(q4):
+    """The W8A8 baseline's single-m-block RESLN GEMM takes the same cluster exchange."""
+    M, N, K = 96, 1024, 1024
+    x, wt, b = synth.hidden(M, K, "cx8x"), synth.weight(N, K, "cx8w"), synth.bias(N, "cx8b")
+    res = synth.hidden(M, N, "cx8r")
+    gam, bet = synth.ln_params(N, "cx8ln")
+    a, sa = orc.quantize_rows_i8(x)
+    w, sw = orc.quantize_rows_i8(wt)
+    out = q4.w8a8_linear(dev(a), dev(sa), dev(w), dev(sw), q4.EPI_RESLN_Q4, bias=dev(b), residual=dev(res),
+                         gamma=dev(gam), beta=dev(bet), ln_eps=1e-12)
+    ref = orc.w8a8_linear(a, sa, w, sw, M, N, K, orc.EPI_RESLN_Q4, bias=b, residual=res, gamma=gam, beta=bet,
+                          ln_eps=1e-12)
+    y = host(out["f16"])
+    assert_f16_close(y, ref["f16"], "w8a8 resln")
+    c2, s2 = orc.quantize_rows_i8(y)
+    assert np.array_equal(host(out["codes"]), c2) and np.array_equal(host(out["scales"]), s2)
