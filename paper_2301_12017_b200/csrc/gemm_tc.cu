@@ -29,6 +29,10 @@
 // step and exchange per-row partials (max-abs; shifted LayerNorm moments combined in one
 // pass) through L2 with a per-m-block arrival counter.  The grid is sized so all CTAs are
 // co-resident (persistent, <= 1 CTA per SM).
+// Narrow tiles (TN <= 64, the latency configs, M <= 512): ATM -- the unpack warps write the
+// int8 activations straight into TMEM and the MMA reads A from there (TS form); split-K over
+// global integer reductions for long k-loops (ksplit); and a single m-block of <= 16 CTAs runs
+// as one cluster whose row partials go through distributed shared memory (cx).  DESIGN.md 4.3.
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
